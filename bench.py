@@ -1,0 +1,300 @@
+"""Benchmark: space-time DoF/s per Uzawa iteration on BASELINE config 2.
+
+Workload (BASELINE.json configs[1]): 2D heat equation on the
+unit square, cells=256 (255x255 = 65,025 interior nodes, the MG-compatible
+mesh for "256x256"), implicit Euler N=1024, T=1, fp64, u(0)=0, load
+f = g - (4/5) D_A^-1 (A g) with g ~ N(0,1) seeded 0 (one damped-Jacobi
+smoothing sweep), MG V-cycles (1 pre + 1 post sweep), omega=0.9, tol=1e-8.
+
+One bench "step" = one Uzawa iteration over the whole space-time slab
+(r1, A~^-1, z, H~^-1, updates, residual), state resident in HBM (each slab
+is 533 MB > 126 MB L2, so no L2 flush is needed between steps).
+``value``  = N*n / device time per iteration (CUDA events on the library stream).
+``e2e``    = the same metric through the public API (uzawa_solve) from host
+             numpy arrays to host numpy arrays, to convergence, wall clock
+             including H2D of f and D2H of p, u (time-to-1e-8 also reported).
+``roofline`` = dominant kernel's algorithmic bytes / its event-timed duration.
+``cpu_baseline`` = the CPU oracle port (oracle/, the reference algorithm in
+             numpy/scipy) on an N=64 slice of the same grid, per iteration.
+
+--impl reference runs that CPU oracle arm alone (the reference is pure
+Python and is not installable on the GPU box; oracle/ restates it and is
+pinned bit-for-bit to it, tests/test_oracle.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CELLS, NSTEPS, T_END = 256, 1024, 1.0
+WORKLOAD = ("c2: 2D heat u_t - Lap u = f, unit square, cells=256 (255^2=65025 interior), "
+            "implicit Euler N=1024, T=1, f=Jacobi-smoothed N(0,1) seed 0, u0=0, "
+            "MG V(1,1), omega=0.9, tol=1e-8")
+
+
+def c2_load(cells=CELLS, N=NSTEPS, seed=0):
+    """g ~ N(0,1) (seed) smoothed by one damped Jacobi sweep: g - (4/5) D^-1 A g."""
+    import scipy.sparse as sp  # noqa: F401
+
+    from paper_1802_08126_b200 import assemble_mass_stiffness_2d
+
+    _, a = assemble_mass_stiffness_2d(cells)
+    g = np.random.default_rng(seed).standard_normal((N, a.dim))
+    dinv = (4.0 / 5.0) / a.diagonal()
+    return g - dinv[None, :] * a.dot(g.T).T
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle arm (reference algorithm restated in numpy/scipy)
+# ----------------------------------------------------------------------------
+
+def cpu_oracle_rate(cells=CELLS, n_slice=64, iters=4, repeats=1):
+    """Marginal per-iteration time of the oracle Uzawa on an N-slice of the
+    c2 grid ((t(k=iters) - t(k=iters/2)) / (iters/2))."""
+    import oracle as orc
+
+    load = c2_load(cells, n_slice)
+    n = (cells - 1) ** 2
+    nodes = orc.time_nodes("uniform", n_slice, T_END * n_slice / NSTEPS)
+    pb = orc.heat_problem("2d", cells, nodes, load=load, u_init=np.zeros(n))
+    lev = orc.mg_levels("2d", cells)
+    at, ht = orc.BlockInv(pb, lev), orc.SchurInv(pb, lev)
+    best = None
+    for _ in range(repeats):
+        times = []
+        res = orc.uzawa(pb, at, ht, 0.9, 1e-300, iters,
+                        on_iter=lambda j, r: times.append(time.perf_counter()))
+        half = iters // 2
+        dt = (times[-1] - times[half - 1]) / (iters - half)
+        best = dt if best is None else min(best, dt)
+        del res
+    return n_slice * n / best, best
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    iters = 2 * max(1, min(steps, 3))
+    rates = []
+    t0 = time.perf_counter()
+    for k in range(warm + steps):
+        rate, dt = cpu_oracle_rate(iters=iters)
+        if k >= warm:
+            rates.append((rate, dt))
+    wall = time.perf_counter() - t0
+    val = float(np.median([r for r, _ in rates]))
+    line = {
+        "metric": "space-time DoF/s per Uzawa iteration", "value": val,
+        "unit": "DoF/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": float(np.median([d for _, d in rates])) * 1e3 * (NSTEPS / 64),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "sample": "N=64 slice of the c2 grid, marginal "
+                   "per-iteration time of the CPU oracle; ms_per_step scaled linearly to N=1024"},
+        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle uzawa, cells=256, N=64 slice, {iters} iterations "
+                                   f"per step, marginal; wall {wall:.1f}s"},
+        "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+
+def build_solver(load, device):
+    import paper_1802_08126_b200 as pg
+
+    grid = pg.build_time_grid("uniform", NSTEPS, T_END)
+    n = (CELLS - 1) ** 2
+    spec = pg.problem_from_arrays("2d", CELLS, grid, load, np.zeros(n), alpha=1.0)
+    system = pg.TimeGlobalSystem(spec, device=device)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("2d", CELLS))
+    ht = pg.build_schur_preconditioner(spec, "mg", vcycles=1)
+    return pg, spec, system, at, ht
+
+
+def run_gpu(args):
+    import ctypes
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    load = c2_load()
+    pg, spec, system, at, ht = build_solver(load, local)
+    gp = system._gp
+    ctx = gp.ctx
+    f = np.ascontiguousarray(system.rhs)
+    N, n = spec.N, spec.dim
+    steps, warm = args.steps, max(3, args.warmup)
+
+    # ---- device-resident timed region -------------------------------------
+    ref = ctypes.c_double()
+    ctx.call("pint_uzawa_begin", f.ctypes.data, None, None, ctypes.byref(ref))
+    nums = np.zeros(max(warm, steps))
+    ms = ctypes.c_double()
+    ctx.call("pint_uzawa_run", 0.9, warm, nums.ctypes.data, ctypes.byref(ms))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    with ClockSampler(local) as clk:
+        ctx.call("pint_uzawa_run", 0.9, steps, nums.ctypes.data, ctypes.byref(ms))
+    launches = (ctx.launches() - l0)
+    torch.cuda.synchronize()
+    ms_step = ms.value / steps
+    if dist:
+        t = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * N * n / (ms_step / 1e3)
+
+    # ---- per-kernel roofline (profiling pass, outside the timed region) ----
+    ctx.call("pint_profile", 1)
+    ctx.call("pint_uzawa_run", 0.9, 2, nums.ctypes.data, ctypes.byref(ms))
+    stats = ctx.kernel_stats()
+    ctx.call("pint_profile", 0)
+    hbm, peak_kind = peaks()
+    tot = sum(v[0] for v in stats.values())
+    dom = max(stats.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dcnt, dbytes) = dom
+    achieved = (dbytes / dcnt) / (dms / dcnt / 1e3) / 1e9
+    kernels = {k: {"ms_per_launch": v[0] / v[1], "share": v[0] / tot,
+                   "GBps": (v[2] / v[0] / 1e6) if v[0] > 0 else None, "launches": v[1]}
+               for k, v in stats.items() if v[1] > 0}
+    iter_bytes = 224.0 * N * n  # 28 fp64 block-vector passes per iteration
+    # ---- end to end through the public API (host numpy in / out) ----------
+    t0 = time.perf_counter()
+    (p_h, u_h), hist = pg.uzawa_solve(system, at, ht, pg.UzawaConfig(omega=0.9, tol=1e-8,
+                                                                        max_iter=200))
+    wall = time.perf_counter() - t0
+    e2e_val = world * N * n * hist.iterations / wall
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, dt = cpu_oracle_rate(iters=4)
+        cpu = {"value": rate, "unit": "DoF/s", "cores": 1, "kind": "port",
+               "sample": "CPU oracle uzawa (numpy/scipy restatement of the reference), "
+                         f"cells=256, N=64 slice, marginal s/iter={dt:.3f}"}
+    if rank == 0:
+        line = {
+            "metric": "space-time DoF/s per Uzawa iteration", "value": value, "unit": "DoF/s",
+            "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "N": N,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (533 MB per slab), no flush"},
+            "e2e": {"value": e2e_val, "unit": "DoF/s", "iterations": hist.iterations,
+                    "time_to_tol_s": wall, "converged": hist.converged,
+                    "final_residual": hist.residual[-1] if hist.residual else None,
+                    "h2d_bytes_per_step": int(f.nbytes), "d2h_bytes_per_step": int(2 * f.nbytes),
+                    "step": "one uzawa_solve call from host arrays to convergence"},
+            "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None,
+                         "iteration_alg_GBps": iter_bytes / (ms_step / 1e3) / 1e9,
+                         "iteration_frac": iter_bytes / (ms_step / 1e3) / 1e9 / hbm},
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/*
+ * pint.h -- C ABI of libpint.so, the B200 (sm_100a) implementation of the
+ * inexact-Uzawa hot path of arXiv 1802.08126 (reference package `pintsolve`,
+ * /root/reference/pkg/src/pintsolve).
+ *
+ * The reference exposes this path as a duck-typed Python operator protocol
+ * (SURVEY.md 8(b)); every entry point below replaces one reference callable,
+ * cited as file:line relative to pkg/src/pintsolve/.  The Python package
+ * paper_1802_08126_b200 binds these with ctypes, and any
+ * other FFI (cffi, JNI, cgo) can bind them the same way: plain pointers and
+ * sizes, no torch or numpy types.
+ *
+ * Data layout.  A "block vector" is a time-major slab of N_local x n fp64
+ * values, row r = time step (or DST mode) r, column = interior spatial node
+ * in the reference numbering (2D: j*(c-1)+i, x fastest; 3D: (k*(c-1)+j)*(c-1)+i),
+ * i.e. exactly the C-order numpy array of shape (N, dim) the reference uses.
+ *
+ * Pointers.  Every `const double* in` / `double* out` argument may be a host
+ * pointer (pageable or pinned) or a device pointer on the context's device;
+ * the library detects which (cudaPointerGetAttributes) and stages host
+ * buffers through context-owned device memory.  All work is ordered on the
+ * context's stream; calls return after the result is in `out`.
+ *
+ * Status codes map one-to-one onto the reference exception taxonomy
+ * (errors.py:4-25): PINT_INPUT -> InputError, PINT_DIMENSION ->
+ * DimensionMismatchError, PINT_NOT_SPD -> NotSpdError, PINT_DIVERGED ->
+ * SolverDivergenceError.  pint_last_error() returns the message.
+ */
+#ifndef PINT_H
+#define PINT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PINT_OK 0
+#define PINT_INPUT 1       /* errors.py:4  InputError */
+#define PINT_DIMENSION 2   /* errors.py:8  DimensionMismatchError */
+#define PINT_NOT_SPD 3     /* errors.py:12 NotSpdError */
+#define PINT_DIVERGED 4    /* errors.py:20 SolverDivergenceError */
+#define PINT_CUDA 5        /* device / driver / NCCL failure */
+
+/* which batched multigrid set a call refers to */
+#define PINT_MG_ATILDE 0   /* per-step blocks of A~ (solvers.py:127-155) */
+#define PINT_MG_HTILDE 1   /* per-mode blocks H_k of H~ (schur.py:30-52) */
+
+typedef struct pint_ctx pint_ctx;
+
+/* Version of the ABI described by this header. */
+int pint_abi_version(void);
+
+/* Create a context on CUDA device `device`.  `rank`/`world` describe the
+ * time-axis partition (rank r owns steps [n0, n0+N_local)); world must be 1
+ * in this build.  `nccl_id` is reserved (NULL).  Replaces the process-global
+ * thread pool of parallel.py:19-43 as the unit of execution. */
+int pint_ctx_create(int device, int rank, int world, const void* nccl_id, pint_ctx** out);
+int pint_ctx_destroy(pint_ctx* ctx);
+const char* pint_last_error(const pint_ctx* ctx);
+/* Synchronise the context stream. */
+int pint_sync(pint_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Problem: the spatial stencils, step sizes and stiffness scales of one
+ * ProblemSpec (problems.py:153-182) as consumed by TimeGlobalSystem
+ * (operators.py:29-99).
+ *
+ *   dims        2 (3 reserved)
+ *   m           interior points per side (cells - 1)
+ *   N           time steps owned by this context
+ *   steps[N]    tau_n (TimeGrid.steps, problems.py:49-51)
+ *   mass[S]     mass stencil, S = 3^dims coefficients in CSR column order
+ *               (2D: SW,S,SE,W,C,E,NW,N,NE); absent entries are 0
+ *   n_a         number of distinct stiffness stencils
+ *   a_st[n_a*S] stiffness stencils
+ *   a_sid[N]    stencil used by step n
+ *   a_scale[N]  factor s_n with  A-block_n u = s_n * (a_st[a_sid[n]] u)
+ *               (operators.py:92-99: c_n*tau_n when proportional, else tau_n)
+ *   aref[S]     reference stiffness A_ref stencil (schur.py:72)
+ *   tau_ref     reference step (problems.py:283)
+ * ------------------------------------------------------------------------- */
+int pint_problem_set(pint_ctx* ctx, int dims, int m, int N,
+                     const double* steps, const double* mass,
+                     int n_a, const double* a_st, const int* a_sid, const double* a_scale,
+                     const double* aref, double tau_ref);
+
+/* fold_rhs (operators.py:22-26): f_n = tau_n load_n, f_1 += M u_init. */
+int pint_fold_rhs(pint_ctx* ctx, const double* load, const double* u_init, double* f);
+
+/* apply_K / apply_Kt / apply_Abd (operators.py:78-99). */
+int pint_apply_K(pint_ctx* ctx, const double* in, double* out);
+int pint_apply_Kt(pint_ctx* ctx, const double* in, double* out);
+int pint_apply_Abd(pint_ctx* ctx, const double* in, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Batched multigrid sets (spatial.py:116-169, one V-cycle, 1 pre + 1 post
+ * damped-Jacobi sweep, Galerkin coarse operators, direct coarsest solve).
+ *
+ *   levels        number of grids, fine to coarse (spatial.py:100-113)
+ *   level_m[L]    interior points per side on each level
+ *   n_sets        number of distinct operators (hierarchies)
+ *   tables[L*n_sets*(S+1)]  per (level, set): S stencil coefficients in CSR
+ *                 order followed by dinv = damping/diag (spatial.py:142);
+ *                 on the coarsest level only the centre coefficient is used
+ *                 (1x1 direct solve, spatial.py:143,149-150)
+ *   sid[B]        operator set of each batch plane (B = N: steps or modes)
+ * ------------------------------------------------------------------------- */
+int pint_mg_set(pint_ctx* ctx, int which, int levels, const int* level_m,
+                int n_sets, const double* tables, const int* sid);
+
+/* One V-cycle per plane, planes [0, count) of the set (spatial.py:163-169). */
+int pint_vcycle(pint_ctx* ctx, int which, int count, const double* in, double* out);
+
+/* A~^{-1}: out_n = V_n(in_n) / tau_n  (BlockDiagSolver.apply_inverse, solvers.py:143-150). */
+int pint_atilde_inv(pint_ctx* ctx, const double* in, double* out);
+
+/* H~^{-1}: DST^T, per-mode V-cycle / A_ref / V-cycle scaled by 2 tau_ref / N,
+ * DST  (SchurPreconditioner.apply_inverse, schur.py:62-76). */
+int pint_htilde_inv(pint_ctx* ctx, const double* in, double* out);
+
+/* Sine transforms along the time axis (dst.py:57-93).
+ *   kind 0 inverse            u_n  = sum_k uh_k sin((2k-1) n pi / 2N)     dst.py:67-73
+ *   kind 1 inverse_transpose  rh_k = sum_n r_n  sin((2k-1) n pi / 2N)     dst.py:86-93
+ *   kind 2 forward            (2/N) * kind1 with the last input row halved dst.py:57-65
+ *   kind 3 forward_transpose  (2/N) * kind0, last output row halved        dst.py:75-84  */
+int pint_dst(pint_ctx* ctx, int kind, const double* in, double* out);
+/* Same transforms on any (N, ncols) slab, independent of the problem
+ * (DstPlan(N) used standalone, dst.py:31-55). */
+int pint_dst_raw(pint_ctx* ctx, int kind, int N, long long ncols, const double* in, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Uzawa iteration (uzawa_solve, solvers.py:177-264), state resident on the
+ * device.  begin() copies f, p, u in (p, u may be NULL for zeros) and
+ * returns ref = sqrt(max(f.A~^-1 f + f.H~^-1 f, 0)) (solvers.py:212-217).
+ * step() runs one iteration (solvers.py:224-233) and returns
+ * the residual numerator sqrt(max(sum r1.dp + sum z.y, 0)) (not divided by ref).
+ * end() copies p, u out.  pint_uzawa() is the whole loop, with the
+ * reference's stopping rule (res < tol after recording) and divergence guard
+ * (res > 1e6*first_res -> PINT_DIVERGED); res_hist[max_iter] receives the
+ * residuals, *iters the count, phase_ms[3] = {dst, multigrid, other} device ms.
+ * ------------------------------------------------------------------------- */
+int pint_uzawa_begin(pint_ctx* ctx, const double* f, const double* p0, const double* u0,
+                     double* ref_out);
+int pint_uzawa_step(pint_ctx* ctx, double omega, double* res_num_out);
+int pint_uzawa_end(pint_ctx* ctx, double* p, double* u);
+int pint_uzawa(pint_ctx* ctx, const double* f, double* p, double* u, double omega,
+               double tol, int max_iter, int use_initial, double* res_hist, int* iters,
+               int* converged, double* phase_ms);
+
+/* Enable per-phase CUDA-event timing of pint_uzawa_step (on != 0) and read
+ * the cumulative device milliseconds {dst, multigrid, other} since begin()
+ * (the fft_seconds / spatial_seconds columns of ConvergenceHistory,
+ * solvers.py:245-253). */
+int pint_set_timing(pint_ctx* ctx, int on);
+int pint_phase_ms(pint_ctx* ctx, double* ms3);
+
+/* Per-kernel profiling: with on != 0 every launch is bracketed by CUDA
+ * events on the context stream; pint_kernel_stat() returns, for kernel family
+ * id in [0, pint_kernel_count()), its name, total device ms, launch count and
+ * total algorithmic bytes.  Turning it on resets them. */
+int pint_profile(pint_ctx* ctx, int on);
+int pint_kernel_count(void);
+int pint_kernel_stat(pint_ctx* ctx, int id, const char** name, double* ms_total,
+                     long long* launches, double* alg_bytes_total);
+
+/* Run `iters` Uzawa iterations (as pint_uzawa_step, residual numerators to
+ * res_num[iters]) and return their device time in ms, measured with CUDA
+ * events on the context stream (the bench's timed region). */
+int pint_uzawa_run(pint_ctx* ctx, double omega, int iters, double* res_num, double* ms_out);
+
+/* Number of kernel launches issued by this context so far (bench evidence). */
+long long pint_launch_count(const pint_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINT_H */

@@ -1,0 +1,677 @@
+// C ABI of libpint.so (include/pint.h): context, problem upload, operator
+// entry points and the device-resident Uzawa driver.
+//
+// The Uzawa iteration (uzawa_solve, solvers.py:177-264) runs as this launch
+// sequence per iteration, all on the context stream, state resident in HBM:
+//   r1 = (K u - A p) - f                        k_timeop<OP_R1>
+//   p  = p + V_A(r1)/tau ; s1 = sum r1.dp       V-cycle (A~ set), fused epilogue
+//   z  = (f - K^T p) - ((K u + K^T u) + A u)    k_timeop<OP_Z>
+//   zh = S z                                    DST^T   (dst.py:86-93)
+//   y1 = V_H(zh) ; b2 = A_ref y1                V-cycle (H~ set), k_aref
+//   w  = (2 tau_ref/N) V_H(b2) ; s2 = sum zh.w  V-cycle, fused epilogue
+//   u  = u + omega * S^T w                      DST, fused axpy epilogue
+//   res = sqrt(max(s1 + s2, 0))                 (sum z.y == sum zh.w, S orthogonal pairing)
+// i.e. y = H~^{-1} z is never materialised in time space and dp is never stored.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "pint_internal.cuh"
+
+void pint_throw(int code, const std::string& msg) { throw PintFail{code, msg}; }
+
+void pint_check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        pint_throw(PINT_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static const char* kKernelNames[K_COUNT] = {
+    "timeop_K", "timeop_Kt", "timeop_Abd", "timeop_r1", "timeop_z", "fold_rhs", "aref",
+    "mg_pre_fine", "mg_pre_coarse", "mg_post_fine", "mg_post_coarse",
+    "dst_inverse_transpose", "dst_inverse", "reduce"};
+
+ProfScope::ProfScope(pint_ctx* ctx, int kid, double bytes) : c(ctx), on(ctx->profile) {
+    if (!on) return;
+    if (c->prof_pool.size() < 2) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            PINT_CUDA_CHECK(cudaEventCreate(&e));
+            c->prof_pool.push_back(e);
+        }
+    }
+    r.kid = kid;
+    r.bytes = bytes;
+    r.a = c->prof_pool.back();
+    c->prof_pool.pop_back();
+    r.b = c->prof_pool.back();
+    c->prof_pool.pop_back();
+    PINT_CUDA_CHECK(cudaEventRecord(r.a, c->stream));
+}
+
+ProfScope::~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(r.b, c->stream);
+    c->prof_open.push_back(r);
+}
+
+void pint_prof_drain(pint_ctx* c) {
+    for (ProfRec& r : c->prof_open) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            c->kstat[r.kid].ms += ms;
+            c->kstat[r.kid].bytes += r.bytes;
+            c->kstat[r.kid].count += 1;
+        }
+        c->prof_pool.push_back(r.a);
+        c->prof_pool.push_back(r.b);
+    }
+    c->prof_open.clear();
+}
+
+namespace {
+
+template <typename F>
+int guarded(pint_ctx* c, F&& f) {
+    if (c == nullptr) return PINT_INPUT;
+    try {
+        PINT_CUDA_CHECK(cudaSetDevice(c->dev));
+        f();
+        c->err.clear();
+        return PINT_OK;
+    } catch (const PintFail& e) {
+        c->err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return PINT_CUDA;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    if (p == nullptr) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+    T* p = nullptr;
+    PINT_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T) + 16));
+    return p;
+}
+
+template <typename T>
+T* upload(pint_ctx* c, const T* h, size_t count) {
+    T* d = dalloc<T>(count);
+    PINT_CUDA_CHECK(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    (void)c;
+    return d;
+}
+
+size_t slab(const pint_ctx* c) { return (size_t)c->N * c->n; }
+
+// Input block vector: device pointer used in place, host pointer staged.
+const double* stage_in(pint_ctx* c, const double* p, double* staging, size_t count) {
+    if (p == nullptr) pint_throw(PINT_INPUT, "null input");
+    if (is_device_ptr(p)) return p;
+    PINT_CUDA_CHECK(
+        cudaMemcpyAsync(staging, p, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    return staging;
+}
+
+struct OutBuf {
+    double* dev;
+    double* host;
+};
+
+OutBuf stage_out(pint_ctx* c, double* p, double* staging) {
+    if (p == nullptr) pint_throw(PINT_INPUT, "null output");
+    if (is_device_ptr(p)) return {p, nullptr};
+    (void)c;
+    return {staging, p};
+}
+
+void finish_out(pint_ctx* c, const OutBuf& o, size_t count) {
+    if (o.host)
+        PINT_CUDA_CHECK(cudaMemcpyAsync(o.host, o.dev, count * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream));
+    PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    pint_prof_drain(c);
+}
+
+void require_problem(pint_ctx* c) {
+    if (!c->problem_ready) pint_throw(PINT_INPUT, "problem not set");
+}
+
+void free_slabs(pint_ctx* c) {
+    double** s[] = {&c->d_f,  &c->d_p,  &c->d_u,        &c->d_r1,        &c->d_z,
+                    &c->d_w1, &c->d_w2, &c->d_stage_in, &c->d_stage_out, &c->d_vec};
+    for (double** p : s) {
+        dfree(*p);
+        *p = nullptr;
+    }
+    for (double* p : c->lev_b) dfree(p);
+    for (double* p : c->lev_x) dfree(p);
+    c->lev_b.clear();
+    c->lev_x.clear();
+    c->lev_cap.clear();
+}
+
+void free_problem(pint_ctx* c) {
+    dfree(c->d_steps);
+    dfree(c->d_mass);
+    dfree(c->d_ast);
+    dfree(c->d_asid);
+    dfree(c->d_ascale);
+    dfree(c->d_aref);
+    c->d_steps = c->d_mass = c->d_ast = c->d_ascale = c->d_aref = nullptr;
+    c->d_asid = nullptr;
+    for (MgSet& s : c->mg) {
+        dfree(s.tab);
+        dfree(s.sid);
+        s = MgSet{};
+    }
+    free_slabs(c);
+    pint::dst_plan_free(c->dst);
+    c->problem_ready = false;
+    c->uz_ready = false;
+}
+
+// level buffers sized for N planes of every level >= 1 of either set
+void ensure_levels(pint_ctx* c, const std::vector<int>& m) {
+    if (c->lev_b.size() < m.size()) {
+        c->lev_b.resize(m.size(), nullptr);
+        c->lev_x.resize(m.size(), nullptr);
+        c->lev_cap.resize(m.size(), 0);
+    }
+    for (size_t l = 1; l < m.size(); ++l) {
+        const size_t need = (size_t)c->N * m[l] * m[l];
+        if (c->lev_cap[l] >= need) continue;
+        dfree(c->lev_b[l]);
+        dfree(c->lev_x[l]);
+        c->lev_b[l] = dalloc<double>(need);
+        c->lev_x[l] = dalloc<double>(need);
+        c->lev_cap[l] = need;
+    }
+}
+
+void rec(pint_ctx* c, int i) {
+    if (c->timing) PINT_CUDA_CHECK(cudaEventRecord(c->ev[i], c->stream));
+}
+
+float elapsed(pint_ctx* c, int a, int b) {
+    float ms = 0.f;
+    PINT_CUDA_CHECK(cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]));
+    return ms;
+}
+
+// H~^{-1} pieces shared by apply, ref-norm and the Uzawa step
+// zh = S z (into w1); y1 = V_H(zh) (w2); b2 = A_ref y1 (scratch); w = s V_H(b2)
+void schur_mode_space(pint_ctx* c, const double* z, double* scratch, int epi, double* wout,
+                      int slot) {
+    const double s = 2.0 * c->tau_ref / c->N;   // schur.py:67
+    rec(c, 1);
+    pint::dst_apply(c, 1, z, c->d_w1, nullptr, 1.0);
+    rec(c, 2);
+    pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w1, c->d_w2, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
+    pint::launch_aref(c, c->d_w2, scratch, c->N);
+    pint::vcycle(c, PINT_MG_HTILDE, c->N, scratch, wout, epi, s, nullptr, c->d_w1, slot);
+    rec(c, 3);
+}
+
+void ensure_uzawa_buffers(pint_ctx* c) {
+    const size_t S = slab(c);
+    if (!c->d_f) c->d_f = dalloc<double>(S);
+    if (!c->d_p) c->d_p = dalloc<double>(S);
+    if (!c->d_u) c->d_u = dalloc<double>(S);
+    if (!c->d_r1) c->d_r1 = dalloc<double>(S);
+    if (!c->d_z) c->d_z = dalloc<double>(S);
+    if (!c->d_w1) c->d_w1 = dalloc<double>(S);
+    if (!c->d_w2) c->d_w2 = dalloc<double>(S);
+}
+
+void ensure_stage(pint_ctx* c) {
+    const size_t S = slab(c);
+    if (!c->d_stage_in) c->d_stage_in = dalloc<double>(S);
+    if (!c->d_stage_out) c->d_stage_out = dalloc<double>(S);
+}
+
+void require_sets(pint_ctx* c) {
+    if (!c->mg[PINT_MG_ATILDE].ready || !c->mg[PINT_MG_HTILDE].ready)
+        pint_throw(PINT_INPUT, "both multigrid sets (A~ and H~) must be configured");
+}
+
+}  // namespace
+
+extern "C" {
+
+int pint_abi_version(void) { return 1; }
+
+int pint_ctx_create(int device, int rank, int world, const void* nccl_id, pint_ctx** out) {
+    (void)nccl_id;
+    if (out == nullptr) return PINT_INPUT;
+    *out = nullptr;
+    if (world != 1 || rank != 0) return PINT_INPUT;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return PINT_CUDA;
+    }
+    pint_ctx* c = new pint_ctx();
+    c->dev = device;
+    c->rank = rank;
+    c->world = world;
+    const int st = guarded(c, [&] {
+        PINT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        PINT_CUDA_CHECK(cudaMalloc(&c->d_acc, 8 * sizeof(double)));
+        PINT_CUDA_CHECK(cudaMallocHost(&c->h_acc, 8 * sizeof(double)));
+        for (auto& e : c->ev) PINT_CUDA_CHECK(cudaEventCreate(&e));
+    });
+    if (st != PINT_OK) {
+        delete c;
+        return st;
+    }
+    *out = c;
+    return PINT_OK;
+}
+
+int pint_ctx_destroy(pint_ctx* c) {
+    if (c == nullptr) return PINT_OK;
+    cudaSetDevice(c->dev);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    free_problem(c);
+    pint::dst_plan_free(c->dst_raw);
+    dfree(c->d_part);
+    dfree(c->d_acc);
+    if (c->h_acc) cudaFreeHost(c->h_acc);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->prof_pool) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return PINT_OK;
+}
+
+const char* pint_last_error(const pint_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int pint_sync(pint_ctx* c) {
+    return guarded(c, [&] { PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream)); });
+}
+
+long long pint_launch_count(const pint_ctx* c) { return c ? c->launches : 0; }
+
+int pint_profile(pint_ctx* c, int on) {
+    return guarded(c, [&] {
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        pint_prof_drain(c);
+        c->profile = on != 0;
+        for (KStat& k : c->kstat) k = KStat{};
+    });
+}
+
+int pint_kernel_stat(pint_ctx* c, int id, const char** name, double* ms_total,
+                     long long* launches, double* alg_bytes_total) {
+    return guarded(c, [&] {
+        if (id < 0 || id >= K_COUNT) pint_throw(PINT_INPUT, "kernel id out of range");
+        if (name) *name = kKernelNames[id];
+        if (ms_total) *ms_total = c->kstat[id].ms;
+        if (launches) *launches = c->kstat[id].count;
+        if (alg_bytes_total) *alg_bytes_total = c->kstat[id].bytes;
+    });
+}
+
+int pint_kernel_count(void) { return K_COUNT; }
+
+int pint_uzawa_run(pint_ctx* c, double omega, int iters, double* res_num, double* ms_out) {
+    return guarded(c, [&] {
+        if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
+        cudaEvent_t a, b;
+        PINT_CUDA_CHECK(cudaEventCreate(&a));
+        PINT_CUDA_CHECK(cudaEventCreate(&b));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        PINT_CUDA_CHECK(cudaEventRecord(a, c->stream));
+        for (int j = 0; j < iters; ++j) {
+            double num = 0.0;
+            const int st = pint_uzawa_step(c, omega, &num);
+            if (st != PINT_OK) pint_throw(st, c->err);
+            if (res_num) res_num[j] = num;
+        }
+        PINT_CUDA_CHECK(cudaEventRecord(b, c->stream));
+        PINT_CUDA_CHECK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        PINT_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        if (ms_out) *ms_out = ms;
+    });
+}
+
+int pint_set_timing(pint_ctx* c, int on) {
+    return guarded(c, [&] { c->timing = on != 0; });
+}
+
+int pint_phase_ms(pint_ctx* c, double* ms3) {
+    return guarded(c, [&] {
+        if (!ms3) pint_throw(PINT_INPUT, "null output");
+        ms3[0] = c->ms_dst;
+        ms3[1] = c->ms_mg;
+        ms3[2] = c->ms_other;
+    });
+}
+
+int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, const double* mass,
+                     int n_a, const double* a_st, const int* a_sid, const double* a_scale,
+                     const double* aref, double tau_ref) {
+    return guarded(c, [&] {
+        if (dims != 2) pint_throw(PINT_INPUT, "only 2D problems are supported by this build");
+        if (m < 1 || N < 1 || n_a < 1) pint_throw(PINT_INPUT, "bad problem dimensions");
+        if (!steps || !mass || !a_st || !a_sid || !a_scale || !aref)
+            pint_throw(PINT_INPUT, "null problem array");
+        for (int t = 0; t < N; ++t) {
+            if (!(steps[t] > 0.0)) pint_throw(PINT_INPUT, "time-step lengths must be positive");
+            if (a_sid[t] < 0 || a_sid[t] >= n_a) pint_throw(PINT_INPUT, "bad stiffness index");
+        }
+        free_problem(c);
+        c->dims = dims;
+        c->m = m;
+        c->n = m * m;
+        c->N = N;
+        c->tau_ref = tau_ref;
+        c->n_a = n_a;
+        c->h_steps.assign(steps, steps + N);
+        c->d_steps = upload(c, steps, N);
+        c->d_mass = upload(c, mass, PINT_S2);
+        c->d_ast = upload(c, a_st, (size_t)n_a * PINT_S2);
+        c->d_asid = upload(c, a_sid, N);
+        c->d_ascale = upload(c, a_scale, N);
+        c->d_aref = upload(c, aref, PINT_S2);
+        pint::dst_plan_build(c->dst, N);
+        c->problem_ready = true;
+    });
+}
+
+int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_sets,
+                const double* tables, const int* sid) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE)
+            pint_throw(PINT_INPUT, "unknown multigrid set");
+        if (levels < 2 || !level_m || !tables || !sid || n_sets < 1)
+            pint_throw(PINT_INPUT, "bad multigrid description");
+        if (level_m[0] != c->m) pint_throw(PINT_DIMENSION, "finest level does not match problem");
+        for (int l = 0; l + 1 < levels; ++l)
+            if (level_m[l] != 2 * level_m[l + 1] + 1)
+                pint_throw(PINT_INPUT, "levels must halve the cell count");
+        for (int b = 0; b < c->N; ++b)
+            if (sid[b] < 0 || sid[b] >= n_sets) pint_throw(PINT_INPUT, "bad operator-set index");
+        const size_t ntab = (size_t)levels * n_sets * PINT_TW;
+        for (int s = 0; s < n_sets; ++s) {
+            const double a = tables[((size_t)(levels - 1) * n_sets + s) * PINT_TW + 4];
+            if (!(a > 0.0)) pint_throw(PINT_NOT_SPD, "non-positive pivot: operator is not SPD");
+        }
+        MgSet& s = c->mg[which];
+        dfree(s.tab);
+        dfree(s.sid);
+        s = MgSet{};
+        s.levels = levels;
+        s.m.assign(level_m, level_m + levels);
+        s.n_sets = n_sets;
+        s.tab = upload(c, tables, ntab);
+        s.sid = upload(c, sid, c->N);
+        ensure_levels(c, s.m);
+        s.ready = true;
+    });
+}
+
+int pint_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f) {
+    return guarded(c, [&] {
+        require_problem(c);
+        ensure_stage(c);
+        if (u_init == nullptr) pint_throw(PINT_INPUT, "null u_init");
+        const double* dl = stage_in(c, load, c->d_stage_in, slab(c));
+        const double* dui = u_init;
+        if (!is_device_ptr(u_init)) {
+            if (!c->d_vec) c->d_vec = dalloc<double>(c->n);
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_vec, u_init, c->n * sizeof(double),
+                                            cudaMemcpyHostToDevice, c->stream));
+            dui = c->d_vec;
+        }
+        // the fold is element-wise in load, so a host result can overwrite the staged load
+        OutBuf o = stage_out(c, f, c->d_stage_in);
+        pint::launch_fold_rhs(c, dl, dui, o.dev);
+        finish_out(c, o, slab(c));
+    });
+}
+
+static int timeop_entry(pint_ctx* c, int op, const double* in, double* out) {
+    return guarded(c, [&] {
+        require_problem(c);
+        ensure_stage(c);
+        const double* d = stage_in(c, in, c->d_stage_in, slab(c));
+        OutBuf o = stage_out(c, out, c->d_stage_out);
+        if (o.dev == d) pint_throw(PINT_INPUT, "in-place operator application is not supported");
+        pint::launch_timeop(c, op, d, nullptr, nullptr, o.dev);
+        finish_out(c, o, slab(c));
+    });
+}
+
+int pint_apply_K(pint_ctx* c, const double* in, double* out) {
+    return timeop_entry(c, pint::OP_K, in, out);
+}
+int pint_apply_Kt(pint_ctx* c, const double* in, double* out) {
+    return timeop_entry(c, pint::OP_KT, in, out);
+}
+int pint_apply_Abd(pint_ctx* c, const double* in, double* out) {
+    return timeop_entry(c, pint::OP_ABD, in, out);
+}
+
+int pint_vcycle(pint_ctx* c, int which, int count, const double* in, double* out) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (which != 0 && which != 1) pint_throw(PINT_INPUT, "unknown multigrid set");
+        if (count < 1 || count > c->N) pint_throw(PINT_DIMENSION, "bad plane count");
+        ensure_stage(c);
+        const size_t cnt = (size_t)count * c->n;
+        const double* d = stage_in(c, in, c->d_stage_in, cnt);
+        OutBuf o = stage_out(c, out, c->d_stage_out);
+        pint::vcycle(c, which, count, d, o.dev, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
+        finish_out(c, o, cnt);
+    });
+}
+
+int pint_atilde_inv(pint_ctx* c, const double* in, double* out) {
+    return guarded(c, [&] {
+        require_problem(c);
+        ensure_stage(c);
+        const double* d = stage_in(c, in, c->d_stage_in, slab(c));
+        OutBuf o = stage_out(c, out, c->d_stage_out);
+        pint::vcycle(c, PINT_MG_ATILDE, c->N, d, o.dev, EPI_DIV_TAU, 1.0, nullptr, nullptr, 0);
+        finish_out(c, o, slab(c));
+    });
+}
+
+int pint_htilde_inv(pint_ctx* c, const double* in, double* out) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (!c->mg[PINT_MG_HTILDE].ready) pint_throw(PINT_INPUT, "H~ multigrid set not configured");
+        ensure_stage(c);
+        ensure_uzawa_buffers(c);
+        const double* d = stage_in(c, in, c->d_stage_in, slab(c));
+        OutBuf o = stage_out(c, out, c->d_stage_out);
+        schur_mode_space(c, d, c->d_z, EPI_SCALE, c->d_w2, 0);
+        pint::dst_apply(c, 0, c->d_w2, o.dev, nullptr, 1.0);
+        finish_out(c, o, slab(c));
+    });
+}
+
+int pint_dst(pint_ctx* c, int kind, const double* in, double* out) {
+    return guarded(c, [&] {
+        require_problem(c);
+        ensure_stage(c);
+        const double* d = stage_in(c, in, c->d_stage_in, slab(c));
+        OutBuf o = stage_out(c, out, c->d_stage_out);
+        pint::dst_apply(c, kind, d, o.dev, nullptr, 1.0);
+        finish_out(c, o, slab(c));
+    });
+}
+
+int pint_dst_raw(pint_ctx* c, int kind, int N, long long ncols, const double* in, double* out) {
+    return guarded(c, [&] {
+        if (N < 1 || ncols < 1) pint_throw(PINT_DIMENSION, "bad transform shape");
+        if (c->dst_raw.N != N) pint::dst_plan_build(c->dst_raw, N);
+        const size_t cnt = (size_t)N * (size_t)ncols;
+        double* tmp_in = nullptr;
+        double* tmp_out = nullptr;
+        const double* d = in;
+        double* o = out;
+        if (!is_device_ptr(in)) {
+            tmp_in = dalloc<double>(cnt);
+            PINT_CUDA_CHECK(cudaMemcpyAsync(tmp_in, in, cnt * sizeof(double),
+                                            cudaMemcpyHostToDevice, c->stream));
+            d = tmp_in;
+        }
+        if (!is_device_ptr(out)) {
+            tmp_out = dalloc<double>(cnt);
+            o = tmp_out;
+        }
+        pint::dst_run(c, c->dst_raw, kind, ncols, d, o, nullptr, 1.0);
+        if (tmp_out)
+            PINT_CUDA_CHECK(cudaMemcpyAsync(out, tmp_out, cnt * sizeof(double),
+                                            cudaMemcpyDeviceToHost, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        dfree(tmp_in);
+        dfree(tmp_out);
+    });
+}
+
+int pint_uzawa_begin(pint_ctx* c, const double* f, const double* p0, const double* u0,
+                     double* ref_out) {
+    return guarded(c, [&] {
+        require_problem(c);
+        require_sets(c);
+        ensure_uzawa_buffers(c);
+        const size_t S = slab(c), bytes = S * sizeof(double);
+        const cudaMemcpyKind any = cudaMemcpyDefault;
+        PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_f, f, bytes, any, c->stream));
+        if (p0)
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_p, p0, bytes, any, c->stream));
+        else
+            PINT_CUDA_CHECK(cudaMemsetAsync(c->d_p, 0, bytes, c->stream));
+        if (u0)
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_u, u0, bytes, any, c->stream));
+        else
+            PINT_CUDA_CHECK(cudaMemsetAsync(c->d_u, 0, bytes, c->stream));
+        // ref = sqrt(max(f.A~^-1 f + f.H~^-1 f, 0))   (solvers.py:212-217)
+        pint::vcycle(c, PINT_MG_ATILDE, c->N, c->d_f, nullptr, EPI_DOT_TAU, 1.0, nullptr,
+                     nullptr, 0);
+        schur_mode_space(c, c->d_f, c->d_z, EPI_SCALE_DOTONLY, nullptr, 1);
+        PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc, c->d_acc, 2 * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        const double q = c->h_acc[0] + c->h_acc[1];
+        c->ref = std::sqrt(q > 0.0 ? q : 0.0);
+        c->uz_ready = true;
+        c->ms_dst = c->ms_mg = c->ms_other = 0.0;
+        if (ref_out) *ref_out = c->ref;
+    });
+}
+
+int pint_uzawa_step(pint_ctx* c, double omega, double* res_num_out) {
+    return guarded(c, [&] {
+        if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
+        rec(c, 0);
+        pint::launch_timeop(c, pint::OP_R1, c->d_u, c->d_p, c->d_f, c->d_r1);
+        rec(c, 4);
+        pint::vcycle(c, PINT_MG_ATILDE, c->N, c->d_r1, c->d_p, EPI_UZAWA_P, 1.0, c->d_p,
+                     nullptr, 0);
+        rec(c, 5);
+        pint::launch_timeop(c, pint::OP_Z, c->d_u, c->d_p, c->d_f, c->d_z);
+        schur_mode_space(c, c->d_z, c->d_z, EPI_SCALE_DOT, c->d_w2, 1);
+        pint::dst_apply(c, 0, c->d_w2, c->d_u, c->d_u, omega);
+        rec(c, 6);
+        PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc, c->d_acc, 2 * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        pint_prof_drain(c);
+        if (c->timing) {
+            // events: 0 start, 4 r1 done, 5 A~ done, 1 z done, 2 DST^T done, 3 modes done, 6 end
+            c->ms_dst += elapsed(c, 1, 2) + elapsed(c, 3, 6);
+            c->ms_mg += elapsed(c, 4, 5) + elapsed(c, 2, 3);
+            c->ms_other += elapsed(c, 0, 4) + elapsed(c, 5, 1);
+        }
+        const double q = c->h_acc[0] + c->h_acc[1];
+        if (res_num_out) *res_num_out = std::sqrt(q > 0.0 ? q : 0.0);
+    });
+}
+
+int pint_uzawa_end(pint_ctx* c, double* p, double* u) {
+    return guarded(c, [&] {
+        if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
+        const size_t bytes = slab(c) * sizeof(double);
+        if (p) PINT_CUDA_CHECK(cudaMemcpyAsync(p, c->d_p, bytes, cudaMemcpyDefault, c->stream));
+        if (u) PINT_CUDA_CHECK(cudaMemcpyAsync(u, c->d_u, bytes, cudaMemcpyDefault, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pint_uzawa(pint_ctx* c, const double* f, double* p, double* u, double omega, double tol,
+               int max_iter, int use_initial, double* res_hist, int* iters, int* converged,
+               double* phase_ms) {
+    int st = pint_uzawa_begin(c, f, use_initial ? p : nullptr, use_initial ? u : nullptr, nullptr);
+    if (st != PINT_OK) return st;
+    if (iters) *iters = 0;
+    if (converged) *converged = 0;
+    if (c->ref == 0.0) {
+        if (converged) *converged = 1;
+        return pint_uzawa_end(c, p, u);
+    }
+    double first = -1.0;
+    const bool was_timing = c->timing;
+    c->timing = phase_ms != nullptr;
+    for (int j = 0; j < max_iter; ++j) {
+        double num = 0.0;
+        st = pint_uzawa_step(c, omega, &num);
+        if (st != PINT_OK) break;
+        const double res = num / c->ref;
+        if (res_hist) res_hist[j] = res;
+        if (iters) *iters = j + 1;
+        if (first < 0.0) first = res > 1e-300 ? res : 1e-300;
+        if (res > 1e6 * first) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "residual grew to %.3e from %.3e", res, first);
+            c->err = buf;
+            st = PINT_DIVERGED;
+            break;
+        }
+        if (res < tol) {
+            if (converged) *converged = 1;
+            break;
+        }
+    }
+    c->timing = was_timing;
+    if (phase_ms) {
+        phase_ms[0] = c->ms_dst;
+        phase_ms[1] = c->ms_mg;
+        phase_ms[2] = c->ms_other;
+    }
+    if (st == PINT_DIVERGED) {
+        std::string keep = c->err;
+        pint_uzawa_end(c, p, u);
+        c->err = keep;
+        return st;
+    }
+    if (st != PINT_OK) return st;
+    return pint_uzawa_end(c, p, u);
+}
+
+}  // extern "C"

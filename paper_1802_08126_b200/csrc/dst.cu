@@ -1,0 +1,325 @@
+// Sine transforms along the time axis, batched over all spatial nodes.
+//
+// Reference: DstPlan.inverse / inverse_transpose / forward /
+// forward_transpose (dst.py:57-93), i.e. products with the kernel
+//   S[k][n] = sin((2k-1) n pi / 2N),  k, n = 1..N
+// (inverse = S^T, inverse_transpose = S).  The reference calls scipy.fft.dst
+// for power-of-two N and a dense tensordot otherwise (dst.py:60-93).
+//
+// B200 design: the transform runs down time columns of the time-major slab.
+// A CTA owns 2P adjacent spatial columns (all N rows), so its global reads
+// and writes are row segments of 2P contiguous doubles.  Two real columns
+// are packed into one complex column and S / S^T are evaluated with one
+// N-point complex FFT per pair:
+//   S^T u : x_j = (-1)^j u_j; v = Makhoul permutation of x; C = FFT(v);
+//           split C into the two real-input spectra; X_m = Re(e^{-i pi m/2N} V_m);
+//           out_{N-1-m} = X_m                       (DST-II = reversed DCT-II)
+//   S r   : Z_k = r_{N-1-k}; Q = Hermitian part of e^{-i pi k/2N} Z;  D = FFT(Q);
+//           x = inverse Makhoul permutation of (Re D | Im D); out_j = (-1)^j x_j
+// The FFT is an in-place radix-4 (+ one radix-2) decimation-in-frequency
+// network in shared memory; the digit-reversed output order is undone by the
+// `rev` table at the final read.  The transform is an fp64 reassociation of
+// the reference's (scipy/ducc) FFT, so it agrees to rounding (~1e-15
+// relative), not bitwise; the parity tests bound it at the reference's own
+// 1e-13 (tests/test_dst.py:28-41 of the reference).
+#include <cmath>
+#include <vector>
+
+#include "pint_internal.cuh"
+
+namespace pint {
+
+constexpr int DST_THREADS = 256;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+    return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+    return make_double2(a.x - b.x, a.y - b.y);
+}
+
+// in-place DIF FFT (forward, e^{-2 pi i jk/N}) of P columns of length N in smem
+__device__ void fft_dif(double2* buf, int N, int P, int r2first, const double2* __restrict__ tw) {
+    const int tid = threadIdx.x;
+    int L = N;
+    if (r2first) {
+        const int s = N >> 1;
+        for (int item = tid; item < P * s; item += DST_THREADS) {
+            const int pr = item / s, j = item - pr * s;
+            double2* p = buf + (size_t)pr * N + j;
+            const double2 a = p[0], b = p[s];
+            p[0] = cadd(a, b);
+            p[s] = cmul(csub(a, b), __ldg(tw + j));
+        }
+        __syncthreads();
+        L = s;
+    }
+    const int quarter = N >> 2;
+    while (L >= 4) {
+        const int s = L >> 2;
+        const int stride = N / L;
+        for (int item = tid; item < P * quarter; item += DST_THREADS) {
+            const int pr = item / quarter, t = item - pr * quarter;
+            const int blk = t / s, j = t - blk * s;
+            double2* p = buf + (size_t)pr * N + blk * L + j;
+            const double2 x0 = p[0], x1 = p[s], x2 = p[2 * s], x3 = p[3 * s];
+            const double2 a0 = cadd(x0, x2), a1 = csub(x0, x2);
+            const double2 b0 = cadd(x1, x3), b1 = csub(x1, x3);
+            // y1 = a1 - i b1 ; y3 = a1 + i b1
+            const double2 y0 = cadd(a0, b0);
+            const double2 y2 = csub(a0, b0);
+            const double2 y1 = make_double2(a1.x + b1.y, a1.y - b1.x);
+            const double2 y3 = make_double2(a1.x - b1.y, a1.y + b1.x);
+            p[0] = y0;
+            if (j == 0) {
+                p[s] = y1;
+                p[2 * s] = y2;
+                p[3 * s] = y3;
+            } else {
+                p[s] = cmul(y1, __ldg(tw + j * stride));
+                p[2 * s] = cmul(y2, __ldg(tw + 2 * j * stride));
+                p[3 * s] = cmul(y3, __ldg(tw + 3 * j * stride));
+            }
+        }
+        __syncthreads();
+        L = s;
+    }
+}
+
+struct DstArgs {
+    int N, n, P, r2first;
+    const double2* tw;
+    const double2* tq;
+    const int* rev;
+    const double* in;
+    double* out;
+    const double* base;   // out = base + alpha*T(in) when non-null
+    double alpha;
+    double in_last;       // factor on input row N-1
+    double out_last;      // factor on output row N-1
+};
+
+// KIND 0: out = S^T in (dst.py:67-73);  KIND 1: out = S in (dst.py:86-93)
+template <int KIND>
+__global__ void __launch_bounds__(DST_THREADS) k_dst_fft(DstArgs a) {
+    extern __shared__ double2 buf[];
+    const int N = a.N, n = a.n, P = a.P, W = 2 * P;
+    const int c0 = blockIdx.x * W;
+    const int ncol = min(W, n - c0);
+    const int tid = threadIdx.x;
+    // ---- load (+ pre-processing) ----
+    for (int idx = tid; idx < N * W; idx += DST_THREADS) {
+        const int j = idx / W, cc = idx - j * W;
+        double v = (cc < ncol) ? __ldg(a.in + (size_t)j * n + c0 + cc) : 0.0;
+        if (j == N - 1) v *= a.in_last;
+        int pos;
+        if (KIND == 0) {
+            if (j & 1) {
+                v = -v;
+                pos = N - 1 - (j >> 1);
+            } else {
+                pos = j >> 1;
+            }
+        } else {
+            pos = N - 1 - j;
+        }
+        double* dst = reinterpret_cast<double*>(buf + (size_t)(cc >> 1) * N + pos) + (cc & 1);
+        *dst = v;
+    }
+    __syncthreads();
+    if (KIND == 1) {
+        // Q_k = (t_k Z_k + conj(t_k') Z_k') / 2,  k' = (N - k) mod N,  t_k = e^{-i pi k / 2N}
+        const int half = N / 2 + 1;
+        for (int item = tid; item < P * half; item += DST_THREADS) {
+            const int pr = item / half, k = item - pr * half;
+            const int kp = (N - k) & (N - 1);
+            double2* col = buf + (size_t)pr * N;
+            const double2 zk = col[k], zp = col[kp];
+            const double2 q = __ldg(a.tq + k), qp = __ldg(a.tq + kp);
+            const double2 tk = make_double2(q.x, -q.y), tp = make_double2(qp.x, -qp.y);
+            const double2 ctk = q, ctp = qp;  // conjugates
+            const double2 u1 = cadd(cmul(tk, zk), cmul(ctp, zp));
+            const double2 u2 = cadd(cmul(tp, zp), cmul(ctk, zk));
+            col[k] = make_double2(0.5 * u1.x, 0.5 * u1.y);
+            if (kp != k) col[kp] = make_double2(0.5 * u2.x, 0.5 * u2.y);
+        }
+        __syncthreads();
+    }
+    fft_dif(buf, N, P, a.r2first, a.tw);
+    // ---- post-processing + store ----
+    for (int idx = tid; idx < N * W; idx += DST_THREADS) {
+        const int j = idx / W, cc = idx - j * W;
+        if (cc >= ncol) continue;
+        const double2* col = buf + (size_t)(cc >> 1) * N;
+        double v;
+        if (KIND == 0) {
+            const int mm = N - 1 - j;  // out_{N-1-m} = X_m
+            const double2 C = col[__ldg(a.rev + mm)];
+            const double2 D = col[__ldg(a.rev + ((N - mm) & (N - 1)))];
+            const double2 q = __ldg(a.tq + mm);
+            if ((cc & 1) == 0)
+                v = 0.5 * (q.x * (C.x + D.x) + q.y * (C.y - D.y));
+            else
+                v = 0.5 * (q.x * (C.y + D.y) - q.y * (C.x - D.x));
+        } else {
+            const int pos = (j & 1) ? N - 1 - (j >> 1) : (j >> 1);
+            const double2 Dv = col[__ldg(a.rev + pos)];
+            v = (cc & 1) ? Dv.y : Dv.x;
+            if (j & 1) v = -v;
+        }
+        v = a.alpha * v;
+        if (j == N - 1) v *= a.out_last;
+        const size_t gi = (size_t)j * n + c0 + cc;
+        a.out[gi] = a.base ? __ldg(a.base + gi) + v : v;
+    }
+}
+
+// dense fallback (non power of two N): kernel[k][t] = sin((2k+1)(t+1) pi / 2N), 0-based
+template <int KIND>
+__global__ void __launch_bounds__(256) k_dst_dense(DstArgs a, const double* __restrict__ kern) {
+    const int col = blockIdx.x * 256 + threadIdx.x;
+    const int row = blockIdx.y;
+    if (col >= a.n) return;
+    const int N = a.N;
+    double s = 0.0;
+    for (int t = 0; t < N; ++t) {
+        const double w = KIND == 0 ? __ldg(kern + (size_t)t * N + row)   // S^T: sum_k S[k][row] in_k
+                                   : __ldg(kern + (size_t)row * N + t);  // S:   sum_t S[row][t] in_t
+        double v = __ldg(a.in + (size_t)t * a.n + col);
+        if (t == N - 1) v *= a.in_last;
+        s += w * v;
+    }
+    double v = a.alpha * s;
+    if (row == N - 1) v *= a.out_last;
+    const size_t gi = (size_t)row * a.n + col;
+    a.out[gi] = a.base ? __ldg(a.base + gi) + v : v;
+}
+
+void dst_plan_free(DstPlan& d) {
+    cudaFree(d.tw);
+    cudaFree(d.tq);
+    cudaFree(d.rev);
+    cudaFree(d.dense);
+    d = DstPlan{};
+}
+
+void dst_plan_build(DstPlan& d, int N) {
+    dst_plan_free(d);
+    d.N = N;
+    d.fast = N >= 1 && (N & (N - 1)) == 0;
+    const long double PI = 3.141592653589793238462643383279502884L;
+    std::vector<double2> tq(N);
+    for (int k = 0; k < N; ++k) {
+        const long double ang = PI * k / (2.0L * N);
+        tq[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+    PINT_CUDA_CHECK(cudaMalloc(&d.tq, N * sizeof(double2)));
+    PINT_CUDA_CHECK(cudaMemcpy(d.tq, tq.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
+    if (d.fast) {
+        std::vector<double2> tw(N);
+        for (int j = 0; j < N; ++j) {
+            const long double ang = -2.0L * PI * j / N;
+            tw[j] = make_double2((double)cosl(ang), (double)sinl(ang));
+        }
+        int lg = 0;
+        while ((1 << lg) < N) ++lg;
+        d.radix2_first = lg & 1;
+        // radix schedule, first stage first
+        std::vector<int> radix;
+        if (d.radix2_first) radix.push_back(2);
+        for (int L = d.radix2_first ? N / 2 : N; L >= 4; L /= 4) radix.push_back(4);
+        // DIF output position of DFT index k:
+        // pos(k; L, r0, rest) = (k mod r0) * (L / r0) + pos(k / r0; L / r0, rest)
+        std::vector<int> rev(N);
+        for (int k = 0; k < N; ++k) {
+            int pos = 0, L = N, kk = k;
+            for (int r : radix) {
+                pos += (kk % r) * (L / r);
+                kk /= r;
+                L /= r;
+            }
+            rev[k] = pos;
+        }
+        PINT_CUDA_CHECK(cudaMalloc(&d.tw, N * sizeof(double2)));
+        PINT_CUDA_CHECK(cudaMalloc(&d.rev, N * sizeof(int)));
+        PINT_CUDA_CHECK(cudaMemcpy(d.tw, tw.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
+        PINT_CUDA_CHECK(cudaMemcpy(d.rev, rev.data(), N * sizeof(int), cudaMemcpyHostToDevice));
+        int P = 65536 / (16 * N);
+        if (P < 1) P = 1;
+        if (P > 16) P = 16;
+        if ((size_t)P * N * 16 > 200 * 1024)
+            pint_throw(PINT_INPUT, "time axis too long for the single-CTA sine transform");
+        d.pairs = P;
+        const int smem = P * N * 16;
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<0>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    } else {
+        std::vector<double> kern((size_t)N * N);
+        for (int k = 0; k < N; ++k)
+            for (int t = 0; t < N; ++t)
+                kern[(size_t)k * N + t] =
+                    (double)sinl((2.0L * k + 1.0L) * (t + 1.0L) * PI / (2.0L * N));
+        PINT_CUDA_CHECK(cudaMalloc(&d.dense, kern.size() * sizeof(double)));
+        PINT_CUDA_CHECK(cudaMemcpy(d.dense, kern.data(), kern.size() * sizeof(double),
+                                   cudaMemcpyHostToDevice));
+    }
+}
+
+void dst_apply(pint_ctx* c, int kind, const double* in, double* out, const double* base,
+               double alpha) {
+    if (c->dst.N != c->N) pint_throw(PINT_DIMENSION, "transform plan does not match problem");
+    dst_run(c, c->dst, kind, c->n, in, out, base, alpha);
+}
+
+void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const double* in,
+             double* out, const double* base, double alpha) {
+    if (ncols > 0x7fffffffLL) pint_throw(PINT_INPUT, "too many columns");
+    DstArgs a{};
+    a.N = d.N;
+    a.n = (int)ncols;
+    a.P = d.pairs;
+    a.r2first = d.radix2_first;
+    a.tw = d.tw;
+    a.tq = d.tq;
+    a.rev = d.rev;
+    a.in = in;
+    a.out = out;
+    a.base = base;
+    a.alpha = alpha;
+    a.in_last = 1.0;
+    a.out_last = 1.0;
+    int K;
+    switch (kind) {
+        case 0: K = 0; break;
+        case 1: K = 1; break;
+        case 2: K = 1; a.in_last = 0.5; a.alpha *= 2.0 / d.N; break;
+        case 3: K = 0; a.out_last = 0.5; a.alpha *= 2.0 / d.N; break;
+        default: pint_throw(PINT_INPUT, "unknown transform kind");
+    }
+    ProfScope prof(c, K == 0 ? K_DST : K_DST_T,
+                   8.0 * (double)d.N * (double)ncols * (base ? 3.0 : 2.0));
+    if (d.fast) {
+        const int W = 2 * d.pairs;
+        const dim3 g((unsigned)((ncols + W - 1) / W));
+        const size_t smem = (size_t)d.pairs * d.N * 16;
+        if (K == 0)
+            k_dst_fft<0><<<g, DST_THREADS, smem, c->stream>>>(a);
+        else
+            k_dst_fft<1><<<g, DST_THREADS, smem, c->stream>>>(a);
+    } else {
+        const dim3 g((unsigned)((ncols + 255) / 256), d.N);
+        if (K == 0)
+            k_dst_dense<0><<<g, 256, 0, c->stream>>>(a, d.dense);
+        else
+            k_dst_dense<1><<<g, 256, 0, c->stream>>>(a, d.dense);
+    }
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace pint

@@ -1,0 +1,182 @@
+// Internal declarations shared by the libpint translation units.
+//
+// Layout conventions (SURVEY.md 7 / DESIGN.md "Data layout"):
+//   * a block vector is a time-major slab double[N][n], n = m*m (2D), the
+//     C-order (N, dim) array of the reference (linalg.py:1-6);
+//   * a spatial plane is row-major m x m, x fastest (problems.py:133-135);
+//   * stencils are 9 coefficients in CSR column order of an interior row
+//     (SW, S, SE, W, C, E, NW, N, NE), absent entries 0;  the CSR row sum is
+//     evaluated in exactly that order, starting from 0, without FMA
+//     contraction (the library is compiled with -fmad=false), which makes
+//     every stencil / multigrid result bit-identical to scipy's csr_matvec
+//     on the same coefficients (tests/test_gpu_parity.py).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "pint.h"
+
+#define PINT_S2 9   // 2D stencil size
+#define PINT_TW 10  // table row: 9 coefficients + dinv
+
+struct PintFail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void pint_throw(int code, const std::string& msg);
+void pint_check_cuda(cudaError_t e, const char* what);
+
+#define PINT_CUDA_CHECK(x) pint_check_cuda((x), #x)
+
+// epilogues of the finest post-smoothing kernel of a V-cycle
+enum PostEpi : int {
+    EPI_PLAIN = 0,      // out = x
+    EPI_DIV_TAU = 1,    // out = x / tau_n                (solvers.py:147)
+    EPI_UZAWA_P = 2,    // dp = x/tau_n; out = pin + dp; acc += b*dp   (solvers.py:225-226,233)
+    EPI_DOT_TAU = 3,    // dp = x/tau_n; acc += b*dp, nothing stored (ref norm, solvers.py:212-214)
+    EPI_SCALE = 4,      // out = s*x                      (schur.py:73)
+    EPI_SCALE_DOT = 5,  // w = s*x; out = w; acc += aux*w (mode-space form of sum z.y)
+    EPI_SCALE_DOTONLY = 6,  // w = s*x; acc += aux*w, nothing stored (ref norm)
+};
+
+struct MgSet {
+    int levels = 0;
+    std::vector<int> m;       // interior points per side, fine to coarse
+    int n_sets = 0;
+    double* tab = nullptr;    // device [levels][n_sets][PINT_TW]
+    int* sid = nullptr;       // device [B]
+    bool ready = false;
+};
+
+struct DstPlan {
+    int N = 0;
+    bool fast = false;        // power of two -> FFT path
+    double2* tw = nullptr;    // e^{-2 pi i j / N}, j < N
+    double2* tq = nullptr;    // (cos, sin)(pi k / 2N), k < N
+    int* rev = nullptr;       // output position of DFT index k after the DIF stages
+    double* dense = nullptr;  // sin((2k-1) n pi / 2N), k-major (non power of two)
+    int radix2_first = 0;
+    int pairs = 0;            // column pairs per CTA
+};
+
+// kernel families timed individually in profiling mode (pint_profile)
+enum KernelId : int {
+    K_TIMEOP_K = 0, K_TIMEOP_KT, K_TIMEOP_ABD, K_TIMEOP_R1, K_TIMEOP_Z, K_FOLD, K_AREF,
+    K_MG_PRE_FINE, K_MG_PRE_COARSE, K_MG_POST_FINE, K_MG_POST_COARSE,
+    K_DST_T, K_DST, K_REDUCE, K_COUNT
+};
+
+struct KStat {
+    double ms = 0.0;
+    double bytes = 0.0;   // algorithmic bytes
+    long long count = 0;
+};
+
+struct ProfRec {
+    int kid;
+    double bytes;
+    cudaEvent_t a, b;
+};
+
+struct pint_ctx {
+    int dev = 0, rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    long long launches = 0;
+
+    // problem
+    int dims = 0, m = 0, n = 0, N = 0;
+    double tau_ref = 0.0;
+    int n_a = 0;
+    std::vector<double> h_steps;
+    double* d_steps = nullptr;   // [N]
+    double* d_mass = nullptr;    // [9]
+    double* d_ast = nullptr;     // [n_a][9]
+    int* d_asid = nullptr;       // [N]
+    double* d_ascale = nullptr;  // [N]
+    double* d_aref = nullptr;    // [9]
+    bool problem_ready = false;
+
+    MgSet mg[2];
+    DstPlan dst;
+    DstPlan dst_raw;   // plan of the problem-free pint_dst_raw entry
+
+    // level work buffers (levels >= 1): rhs and solution, N planes each
+    std::vector<double*> lev_b, lev_x;
+    std::vector<size_t> lev_cap;
+
+    // slabs [N][n]
+    double *d_f = nullptr, *d_p = nullptr, *d_u = nullptr;
+    double *d_r1 = nullptr, *d_z = nullptr, *d_w1 = nullptr, *d_w2 = nullptr;
+    double *d_stage_in = nullptr, *d_stage_out = nullptr, *d_vec = nullptr;
+
+    // reductions
+    double* d_part = nullptr;    // partial sums
+    size_t part_cap = 0;
+    double* d_acc = nullptr;     // [4] final sums
+    double* h_acc = nullptr;     // pinned [4]
+
+    double ref = 0.0;
+    bool uz_ready = false;
+
+    // phase timing
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    double ms_dst = 0, ms_mg = 0, ms_other = 0;
+
+    // per-kernel profiling (events around every launch)
+    bool profile = false;
+    std::vector<cudaEvent_t> prof_pool;
+    std::vector<ProfRec> prof_open;
+    KStat kstat[K_COUNT];
+};
+
+// RAII event pair around one launch when ctx->profile is on
+struct ProfScope {
+    pint_ctx* c;
+    ProfRec r{};
+    bool on;
+    ProfScope(pint_ctx* ctx, int kid, double bytes);
+    ~ProfScope();
+};
+void pint_prof_drain(pint_ctx* c);   // after a stream sync: accumulate elapsed times
+
+// ---- kernels / launchers (all on ctx->stream) ------------------------------
+namespace pint {
+
+enum TimeOp : int { OP_K = 0, OP_KT = 1, OP_ABD = 2, OP_R1 = 3, OP_Z = 4, OP_MASS0 = 5 };
+
+// time-global stencil operators (stencil_ops.cu)
+void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,
+                   double* out);
+void launch_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f);
+void launch_aref(pint_ctx* c, const double* in, double* out, int count);
+
+// multigrid (mg.cu)
+// V-cycle over planes [0,count) of set `which`; finest post kernel uses `epi`.
+// pin: EPI_UZAWA_P input p;  aux: EPI_SCALE_DOT partner vector; acc_slot: d_acc index
+void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
+            double scale, const double* pin, const double* aux, int acc_slot);
+
+// sine transforms (dst.cu)
+void dst_plan_build(DstPlan& d, int N);
+void dst_plan_free(DstPlan& d);
+// kind 0..3 as in pint_dst; out = beta*base + alpha*T(in) when base != nullptr
+void dst_apply(pint_ctx* c, int kind, const double* in, double* out, const double* base,
+               double alpha);
+// same on an arbitrary (N, ncols) slab with plan d
+void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const double* in,
+             double* out, const double* base, double alpha);
+
+// reductions (stencil_ops.cu)
+void reduce_partials(pint_ctx* c, int nparts, int slot);
+void ensure_partials(pint_ctx* c, size_t nparts);
+
+}  // namespace pint
+
+#define PINT_LAUNCHED(c) ((c)->launches++)

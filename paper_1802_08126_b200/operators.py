@@ -1,0 +1,83 @@
+"""Time-global operators on the GPU (operators.py:22-99 of the reference).
+
+``TimeGlobalSystem`` keeps the reference's interface (``spec``, ``rhs``,
+``apply_K``, ``apply_Kt``, ``apply_Abd``, ``apply_B``, ``apply_Bt``,
+``apply_saddle``) with the arithmetic done by the sm_100a kernels of
+csrc/stencil_ops.cu: block vectors of shape (N, dim), numpy (host) or CUDA
+float64 torch tensors (device), results of the same kind.  Diagnostic-mode
+operators (exact per-step inverses, S-norm, P, S; operators.py:51-214) need
+sparse factorisations and are not on the GPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._device import gpu_problem
+from ._native import as_buffer, empty_like_kind, ptr_of
+from .errors import DiagnosticModeRequiredError
+
+
+def fold_rhs(spec) -> np.ndarray:
+    """tau_n load_n, plus M u_init on block 1 (operators.py:22-26), on the GPU."""
+    gp = gpu_problem(spec)
+    load = np.ascontiguousarray(spec.load, dtype=np.float64)
+    u0 = np.ascontiguousarray(spec.u_init, dtype=np.float64)
+    out = np.empty((spec.N, spec.dim))
+    gp.ctx.call("pint_fold_rhs", load.ctypes.data, u0.ctypes.data, out.ctypes.data)
+    return out
+
+
+class TimeGlobalSystem:
+    """The time-global implicit-Euler system of one ProblemSpec, on the GPU."""
+
+    def __init__(self, spec, diagnostic: bool = False, device=None):
+        if diagnostic:
+            raise DiagnosticModeRequiredError(
+                "exact per-step factorizations are not part of the GPU path")
+        self.spec = spec
+        self._gp = gpu_problem(spec, device)
+        self.rhs = fold_rhs(spec)
+        self._scales = self._gp.scales
+
+    @property
+    def diagnostic(self) -> bool:
+        return False
+
+    def build_exact_solvers(self) -> None:
+        raise DiagnosticModeRequiredError(
+            "exact per-step factorizations are not part of the GPU path")
+
+    def _apply(self, name: str, u):
+        shape = (self.spec.N, self.spec.dim)
+        ptr, keep = as_buffer(u, shape)
+        out = empty_like_kind(keep, shape)
+        self._gp.ctx.call(name, ptr, ptr_of(out))
+        return out
+
+    def apply_K(self, u):
+        """M u_n - M u_{n-1} (operators.py:78-83)."""
+        return self._apply("pint_apply_K", u)
+
+    def apply_Kt(self, u):
+        """M u_n - M u_{n+1} (operators.py:85-90)."""
+        return self._apply("pint_apply_Kt", u)
+
+    def apply_Abd(self, u):
+        """tau_n A_n u_n (operators.py:92-99)."""
+        return self._apply("pint_apply_Abd", u)
+
+    def apply_B(self, u):
+        return self.apply_K(u) + self.apply_Abd(u)
+
+    def apply_Bt(self, u):
+        return self.apply_Kt(u) + self.apply_Abd(u)
+
+    def apply_saddle(self, p, u):
+        """Symmetric indefinite 2x2 block operator (operators.py:107-111)."""
+        top = self.apply_Abd(p) - self.apply_K(u)
+        bottom = -self.apply_Kt(p) - (self.apply_K(u) + self.apply_Kt(u) + self.apply_Abd(u))
+        return top, bottom
+
+    def a_norm(self, u) -> float:
+        return float(np.sqrt(max(float((u * self.apply_Abd(u)).sum()), 0.0)))

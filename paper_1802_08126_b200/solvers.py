@@ -1,0 +1,217 @@
+"""Inexact Uzawa iteration on the GPU (solvers.py of the reference).
+
+``uzawa_solve(system, atilde, htilde, cfg, initial=None, u_oracle=None)``
+keeps the reference signature and semantics (solvers.py:177-264):
+
+* ref = sqrt(max(f.A~^-1 f + f.H~^-1 f, 0)); ref == 0 -> converged, 0 iterations;
+* per iteration  r1 = K u - A p - f;  p += A~^-1 r1;
+  z = f - K^T p - (K u + K^T u + A u);  u += omega H~^-1 z;
+  res = sqrt(max(sum r1.dp + sum z.y, 0)) / ref, recorded before the tests;
+* divergence when res > 1e6 * first_res (SolverDivergenceError);
+* stop when res < tol (the converging iteration is counted).
+
+The iteration itself is one call per iteration into libpint
+(pint_uzawa_step); the state (f, p, u and all work slabs) stays in HBM and
+only the two partial sums come back.  ``fft_seconds`` / ``spatial_seconds``
+are cumulative device time of the DST and multigrid phases (CUDA events).
+Diagnostic mode (exact S-norm error per iteration, stopping='s_norm_error')
+needs sparse factorisations and is not on the GPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._device import gpu_problem
+from ._native import as_buffer, empty_like_kind, ptr_of
+from .errors import DiagnosticModeRequiredError, InputError
+from .spatial import MgHierarchy, _check_mg_options
+
+
+@dataclass
+class UzawaConfig:
+    """solvers.py:21-36."""
+
+    omega: float = 0.9
+    max_iter: int = 200
+    tol: float = 1e-8
+    stopping: str = "preconditioned_residual"
+    record_history: bool = True
+    diagnostics: bool = False
+
+    def __post_init__(self):
+        if self.omega <= 0.0:
+            raise InputError("damping parameter must be positive")
+        if self.tol <= 0.0:
+            raise InputError("tolerance must be positive")
+        if self.stopping not in ("preconditioned_residual", "s_norm_error"):
+            raise InputError(f"unknown stopping rule {self.stopping!r}")
+
+
+@dataclass
+class ConvergenceHistory:
+    """Per-iteration record (solvers.py:39-74); same CSV format."""
+
+    residual: list = field(default_factory=list)
+    s_norm_error: list = field(default_factory=list)
+    d_norm_error: list = field(default_factory=list)
+    wall_seconds: list = field(default_factory=list)
+    fft_seconds: list = field(default_factory=list)
+    spatial_seconds: list = field(default_factory=list)
+    converged: bool = False
+
+    @property
+    def iterations(self) -> int:
+        return len(self.residual)
+
+    def append(self, residual, s_err, d_err, wall, fft, spatial) -> None:
+        self.residual.append(residual)
+        self.s_norm_error.append(s_err)
+        self.d_norm_error.append(d_err)
+        self.wall_seconds.append(wall)
+        self.fft_seconds.append(fft)
+        self.spatial_seconds.append(spatial)
+
+    def to_csv(self) -> str:
+        head = "iter,residual,s_norm_error,d_norm_error,wall_seconds,fft_seconds,spatial_seconds"
+        out = [head]
+        for i in range(self.iterations):
+            s = "" if self.s_norm_error[i] is None else f"{self.s_norm_error[i]:.17g}"
+            d = "" if self.d_norm_error[i] is None else f"{self.d_norm_error[i]:.17g}"
+            out.append(f"{i + 1},{self.residual[i]:.17g},{s},{d},{self.wall_seconds[i]:.17g},"
+                       f"{self.fft_seconds[i]:.17g},{self.spatial_seconds[i]:.17g}")
+        return "\n".join(out) + "\n"
+
+
+@dataclass(frozen=True)
+class RateReport:
+    """Contraction quantities of the damped two-stage iteration (solvers.py:77-88)."""
+
+    rho_a: float
+    omega: float
+    lam_min: float
+    lam_max: float
+    sigma_minus: float
+    sigma_plus: float
+    rho_u: float
+    damping_ok: bool
+
+
+def safe_damping(alpha: float, margin: float = 0.9) -> float:
+    """omega with omega * 3 alpha < 2 (solvers.py:91-100)."""
+    if alpha < 1.0:
+        raise InputError("quasi-uniformity constant is at least one")
+    return margin * 2.0 / (3.0 * alpha)
+
+
+def compute_rate_report(rho_a: float, omega: float, lam_min: float, lam_max: float) -> RateReport:
+    """Proven contraction rates (solvers.py:103-124)."""
+    if not 0.0 <= rho_a < 1.0:
+        raise InputError("preconditioner quality must lie in [0, 1)")
+    if omega <= 0.0 or lam_min <= 0.0 or lam_max <= 0.0:
+        raise InputError("damping and eigenvalue bounds must be positive")
+    tm = (1.0 - rho_a) * (1.0 - omega * lam_min)
+    sm = 0.5 * (tm + np.sqrt(4.0 * rho_a + tm ** 2))
+    tp = (1.0 + rho_a) * (1.0 + omega * lam_max) - 2.0
+    spl = 0.5 * (tp + np.sqrt(4.0 * rho_a + tp ** 2))
+    ok = omega * lam_max < 2.0 * (1.0 - rho_a) / (1.0 + rho_a)
+    return RateReport(rho_a, omega, lam_min, lam_max, float(sm), float(spl),
+                      float(max(sm, spl)), bool(ok))
+
+
+class BlockDiagSolver:
+    """A~^{-1}: one V-cycle per step on A_n, divided by tau_n (solvers.py:127-155),
+    all steps in one batched launch per level."""
+
+    def __init__(self, spec, kind: str = "mg", hierarchy: MgHierarchy | None = None,
+                 cycles: int = 1, smooth_steps: int = 1, damping: float | None = None,
+                 device=None):
+        if kind != "mg":
+            raise InputError(f"solver kind {kind!r} is not on the GPU path; use kind='mg'")
+        if hierarchy is None:
+            raise InputError("mg solver needs a grid hierarchy")
+        _check_mg_options(cycles, smooth_steps, damping)
+        self.spec = spec
+        self.kind = kind
+        self.steps = spec.grid.steps
+        self.hierarchy = hierarchy
+        self._gp = gpu_problem(spec, device)
+        self._gp.set_atilde(hierarchy, 4.0 / 5.0 if damping is None else damping)
+
+    def apply_inverse(self, b):
+        shape = (self.spec.N, self.spec.dim)
+        ptr, keep = as_buffer(b, shape)
+        out = empty_like_kind(keep, shape)
+        self._gp.ctx.call("pint_atilde_inv", ptr, ptr_of(out))
+        return out
+
+    def forward(self, x):
+        raise InputError("forward application requires direct (exact) solvers")
+
+
+def _shared_problem(system, atilde, htilde):
+    gp = system._gp
+    if getattr(atilde, "_gp", None) is not gp or getattr(htilde, "_gp", None) is not gp:
+        raise InputError("system, atilde and htilde must be built from the same ProblemSpec")
+    if not (gp.atilde_ready and gp.htilde_ready):
+        raise InputError("multigrid sets not configured")
+    return gp
+
+
+def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle=None):
+    """Damped two-stage inexact Uzawa iteration (solvers.py:177-264) on the GPU.
+
+    Returns ((p, u), ConvergenceHistory) with p, u numpy arrays (or CUDA
+    tensors when ``initial`` holds CUDA tensors).
+    """
+    if cfg.diagnostics or cfg.stopping == "s_norm_error":
+        raise DiagnosticModeRequiredError(
+            "diagnostic error norms need exact factorizations; not on the GPU path")
+    gp = _shared_problem(system, atilde, htilde)
+    ctx = gp.ctx
+    shape = (system.spec.N, system.spec.dim)
+    f_ptr, f_keep = as_buffer(system.rhs, shape)
+    if initial is not None:
+        p_ptr, p_keep = as_buffer(initial[0], shape)
+        u_ptr, u_keep = as_buffer(initial[1], shape)
+        like = p_keep
+    else:
+        p_ptr = u_ptr = None
+        like = f_keep
+    hist = ConvergenceHistory()
+    ref = ctypes.c_double(0.0)
+    ctx.call("pint_uzawa_begin", f_ptr, p_ptr, u_ptr, ctypes.byref(ref))
+    p_out = empty_like_kind(like, shape)
+    u_out = empty_like_kind(like, shape)
+    if ref.value == 0.0:
+        hist.converged = True
+        ctx.call("pint_uzawa_end", ptr_of(p_out), ptr_of(u_out))
+        return (p_out, u_out), hist
+    ctx.call("pint_set_timing", 1)
+    ms = np.zeros(3)
+    num = ctypes.c_double(0.0)
+    first = None
+    t0 = time.perf_counter()
+    try:
+        for _ in range(cfg.max_iter):
+            ctx.call("pint_uzawa_step", float(cfg.omega), ctypes.byref(num))
+            res = float(num.value) / ref.value
+            if first is None:
+                first = max(res, 1e-300)
+            ctx.call("pint_phase_ms", ms.ctypes.data)
+            hist.append(res, None, None, time.perf_counter() - t0, ms[0] / 1e3, ms[1] / 1e3)
+            if res > 1e6 * first:
+                from .errors import SolverDivergenceError
+
+                raise SolverDivergenceError(f"residual grew to {res:.3e} from {first:.3e}")
+            if res < cfg.tol:
+                hist.converged = True
+                break
+    finally:
+        ctx.call("pint_set_timing", 0)
+    ctx.call("pint_uzawa_end", ptr_of(p_out), ptr_of(u_out))
+    return (p_out, u_out), hist

@@ -1,0 +1,218 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+* stencil operators, fold_rhs, V-cycles and A~^{-1}: bit-identical to the
+  oracle (the kernels follow scipy's CSR summation order without FMA);
+* sine transforms: 1e-13 absolute against the naive sine-kernel formulas,
+  the reference's own bar (pkg/tests/test_dst.py:28-41);
+* H~^{-1}: 1e-12 relative (it inherits the transforms' rounding);
+* Uzawa: identical iteration count (+-1 allowed, 0 observed), per-iteration
+  residuals within 1e-10 relative, final u within 1e-8 relative in the
+  discrete parabolic S-norm.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_1802_08126_b200 as pg
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+CASES_2D = ["ops2d_c16_N16_coeff", "sine2d_c8_N16"]
+
+
+def _load(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    c0, c1 = (float(v) for v in d["coeff"])
+    coeff = None if (c0, c1) == (1.0, 0.0) else (lambda t: c0 + c1 * t)
+    return d, coeff
+
+
+def _pair(name):
+    """(golden, oracle problem, GPU spec) on identical inputs."""
+    d, coeff = _load(name)
+    space, cells = str(d["space"]), int(d["cells"])
+    opb = orc.heat_problem(space, cells, d["nodes"], coeff=coeff, load=d["load"],
+                           u_init=d["u_init"])
+    spec = pg.problem_from_arrays(space, cells, pg.TimeGrid(d["nodes"]), d["load"],
+                                  d["u_init"], coeff=coeff)
+    return d, opb, spec
+
+
+@pytest.fixture(scope="module", params=CASES_2D)
+def case(request):
+    d, opb, spec = _pair(request.param)
+    system = pg.TimeGlobalSystem(spec)
+    hier = pg.build_mg_hierarchy("2d", spec.meta["mesh"])
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=hier)
+    ht = pg.build_schur_preconditioner(spec, "mg", vcycles=1)
+    return d, opb, spec, system, at, ht
+
+
+def test_fold_rhs_bitwise(case):
+    d, opb, spec, system, _, _ = case
+    np.testing.assert_array_equal(system.rhs, orc.fold_rhs(opb))
+    np.testing.assert_array_equal(system.rhs, d["rhs"])
+
+
+def test_time_operators_bitwise(case):
+    d, opb, spec, system, _, _ = case
+    x = d["x"]
+    np.testing.assert_array_equal(system.apply_K(x), d["K_x"])
+    np.testing.assert_array_equal(system.apply_Kt(x), d["Kt_x"])
+    np.testing.assert_array_equal(system.apply_Abd(x), d["Abd_x"])
+
+
+def test_atilde_bitwise(case):
+    d, opb, spec, system, at, _ = case
+    np.testing.assert_array_equal(at.apply_inverse(d["x"]), d["atilde_x"])
+
+
+def test_vcycle_bitwise(case):
+    d, opb, spec, _, _, _ = case
+    hier = pg.build_mg_hierarchy("2d", spec.meta["mesh"])
+    vc = pg.MgVCycleSolver(spec.stiffness[0], hier)
+    np.testing.assert_array_equal(vc.apply(d["y"][0]), d["vcyc_a0_y"])
+
+
+def test_htilde_matches(case):
+    d, opb, spec, system, _, ht = case
+    got = ht.apply_inverse(d["x"])
+    ref = d["htilde_x"]
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_dst_kinds_match_reference(case):
+    d, _, _, _, _, _ = case
+    x = d["x"]
+    plan = pg.DstPlan(x.shape[0])
+    for kind, key in (("forward", "dst_fwd_x"), ("inverse", "dst_inv_x"),
+                      ("forward_transpose", "dst_fwdT_x"), ("inverse_transpose", "dst_invT_x")):
+        got = getattr(plan, kind)(x)
+        np.testing.assert_allclose(got, d[key], rtol=0, atol=1e-13 * max(1.0, np.abs(d[key]).max()))
+
+
+@pytest.mark.parametrize("N", list(range(1, 17)) + [24, 31, 32, 64, 100, 128, 512, 1024, 2048, 4096])
+def test_dst_naive_formulas(N):
+    """pkg/tests/test_dst.py:28-41 (naive kernel, 1e-13), batched over columns."""
+    rng = np.random.default_rng(N)
+    u = rng.standard_normal((N, 37))
+    plan = pg.DstPlan(N)
+    S = plan.kernel()  # S[k, n]
+    w = np.ones(N)
+    w[-1] = 0.5
+    tol = 1e-13 * max(1.0, np.sqrt(N))  # the dense reference sum itself drifts ~sqrt(N) ulp
+    np.testing.assert_allclose(plan.inverse(u), S.T @ u, rtol=0, atol=tol)
+    np.testing.assert_allclose(plan.inverse_transpose(u), S @ u, rtol=0, atol=tol)
+    np.testing.assert_allclose(plan.forward(u), (2.0 / N) * S @ (w[:, None] * u), rtol=0, atol=tol)
+    np.testing.assert_allclose(plan.forward_transpose(u), (2.0 / N) * w[:, None] * (S.T @ u),
+                               rtol=0, atol=tol)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 8, 64, 1024])
+def test_dst_round_trip_and_adjoint(N):
+    """pkg/tests/test_dst.py:44-70: inverse(forward(u)) = u; <Fu, v> = <u, F^T v>."""
+    rng = np.random.default_rng(N + 2)
+    plan = pg.DstPlan(N)
+    u = rng.standard_normal((N, 5))
+    v = rng.standard_normal((N, 5))
+    np.testing.assert_allclose(plan.inverse(plan.forward(u)), u, atol=1e-12)
+    np.testing.assert_allclose(plan.forward(plan.inverse(u)), u, atol=1e-12)
+    assert np.sum(plan.forward(u) * v) == pytest.approx(np.sum(u * plan.forward_transpose(v)),
+                                                        abs=1e-11)
+
+
+def test_uzawa_golden_cases(case):
+    d, opb, spec, system, at, ht = case
+    cfg = pg.UzawaConfig(omega=float(d["uz_omega"]), tol=float(d["uz_tol"]),
+                         max_iter=int(d["uz_max_iter"]))
+    (p, u), hist = pg.uzawa_solve(system, at, ht, cfg)
+    ref_res = d["uz_res"]
+    assert abs(hist.iterations - len(ref_res)) <= 1
+    k = min(hist.iterations, len(ref_res))
+    rel = np.abs(np.array(hist.residual[:k]) - ref_res[:k]) / ref_res[:k]
+    assert rel.max() <= 1e-10, rel.max()
+    assert hist.converged == bool(d["uz_converged"])
+    nrm = orc.ExactNorms(opb)
+    err = nrm.s_norm(u - d["uz_u"]) / nrm.s_norm(d["uz_u"])
+    assert err <= 1e-8
+
+
+def test_config1_uzawa_parity():
+    """BASELINE config 1 (2D, cells=32, N=64, T=1, f~N(0,1) seed 0, u0=0):
+    66 iterations with residual history and solution matching the reference."""
+    g = np.load(os.path.join(GOLDEN, "c1_uzawa.npz"))
+    grid = pg.build_time_grid("uniform", 64, 1.0)
+    load = np.random.default_rng(0).standard_normal((64, 961))
+    spec = pg.problem_from_arrays("2d", 32, grid, load, np.zeros(961))
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("2d", 32))
+    ht = pg.build_schur_preconditioner(spec, "mg", vcycles=1)
+    (p, u), hist = pg.uzawa_solve(system, at, ht, pg.UzawaConfig(omega=0.9, tol=1e-8, max_iter=200))
+    ref = g["residual"]
+    assert hist.iterations == len(ref) == 66
+    rel = np.abs(np.array(hist.residual) - ref) / ref
+    assert rel.max() <= 1e-10, rel.max()
+    opb = orc.heat_problem("2d", 32, orc.time_nodes("uniform", 64, 1.0), load=load,
+                           u_init=np.zeros(961))
+    nrm = orc.ExactNorms(opb)
+    assert nrm.s_norm(u - g["u"]) / nrm.s_norm(g["u"]) <= 1e-8
+    # solution against the exact sequential-Euler solution, as the reference reports
+    assert nrm.s_norm(u - g["u_seq"]) / float(g["s_norm_seq"]) == pytest.approx(
+        float(g["s_norm_err"]), rel=1e-3)
+    assert np.max(np.abs(p + u)) < 1e-5 * np.max(np.abs(u)) + 1e-6  # p -> -u (test_solvers.py:75-88)
+
+
+def test_zero_data_zero_iterations():
+    """solvers.py:212-217 / pkg/tests/test_solvers.py:108-115."""
+    spec = pg.make_heat_problem("2d", 4, pg.build_time_grid("uniform", 4, 1.0), data="zero")
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("2d", 4))
+    ht = pg.build_schur_preconditioner(spec, "mg")
+    (p, u), hist = pg.uzawa_solve(system, at, ht, pg.UzawaConfig())
+    assert hist.converged and hist.iterations == 0
+    assert not np.any(u) and not np.any(p)
+
+
+def test_divergence_raises():
+    """solvers.py:254-257 / pkg/tests/test_solvers.py:117-123."""
+    spec = pg.make_heat_problem("2d", 8, pg.build_time_grid("uniform", 8, 1.0), data="sine")
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("2d", 8))
+    ht = pg.build_schur_preconditioner(spec, "mg")
+    with pytest.raises(pg.SolverDivergenceError):
+        pg.uzawa_solve(system, at, ht, pg.UzawaConfig(omega=40.0, tol=1e-12, max_iter=500))
+
+
+def test_warm_start_fewer_iterations():
+    """pkg/tests/test_solvers.py:125-132."""
+    spec = pg.make_heat_problem("2d", 8, pg.build_time_grid("uniform", 16, 1.0), data="sine")
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("2d", 8))
+    ht = pg.build_schur_preconditioner(spec, "mg")
+    cfg = pg.UzawaConfig(tol=1e-9)
+    (p, u), h1 = pg.uzawa_solve(system, at, ht, cfg)
+    (_, _), h2 = pg.uzawa_solve(system, at, ht, cfg, initial=(p, u))
+    assert h2.iterations < h1.iterations
+
+
+def test_dimension_mismatch():
+    spec = pg.make_heat_problem("2d", 8, pg.build_time_grid("uniform", 4, 1.0), data="sine")
+    system = pg.TimeGlobalSystem(spec)
+    with pytest.raises(pg.DimensionMismatchError):
+        system.apply_K(np.zeros((3, spec.dim)))
+
+
+def test_device_tensors_in_place():
+    """torch CUDA tensors go through the C ABI without staging."""
+    torch = pytest.importorskip("torch")
+    d, opb, spec = _pair("sine2d_c8_N16")
+    system = pg.TimeGlobalSystem(spec)
+    x = torch.from_numpy(d["x"]).cuda()
+    out = system.apply_K(x)
+    assert out.is_cuda
+    np.testing.assert_array_equal(out.cpu().numpy(), d["K_x"])
