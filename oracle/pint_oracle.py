@@ -574,7 +574,11 @@ class SchurInv:
     with one MG V-cycle per H_k^{-1} (schur.py:30-52, 62-76)."""
 
     def __init__(self, pb: Problem, levels: MgLevels, cycles: int = 1,
-                 smooth_steps: int = 1):
+                 smooth_steps: int = 1, dense_dst: bool = False):
+        # dense_dst: evaluate both transforms with the dense sine kernel, the
+        # reference's own non-power-of-two path (dst.py:64,73,81,93); used to
+        # measure the reference's intrinsic reassociation noise
+        self.dense = dst_kernel(pb.N) if dense_dst else None
         self.N = pb.N
         self.tau_ref = pb.tau_ref
         self.a_ref = pb.a_ref
@@ -584,14 +588,14 @@ class SchurInv:
         self.solvers = [VCycle(h, levels, cycles, smooth_steps) for h in self.blocks]
 
     def apply(self, r: np.ndarray) -> np.ndarray:
-        rh = dst_inverse_T(r)
+        rh = dst_inverse_T(r) if self.dense is None else self.dense @ r
         out = np.empty_like(rh)
         s = 2.0 * self.tau_ref / self.N
         for k, sol in enumerate(self.solvers):
             y = sol.apply(rh[k])
             y = self.a_ref.dot(y)
             out[k] = s * sol.apply(y)
-        return dst_inverse(out)
+        return dst_inverse(out) if self.dense is None else self.dense.T @ out
 
 
 class BlockInv:

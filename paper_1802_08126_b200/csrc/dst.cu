@@ -253,11 +253,13 @@ void dst_plan_build(DstPlan& d, int N) {
         if ((size_t)P * N * 16 > 200 * 1024)
             pint_throw(PINT_INPUT, "time axis too long for the single-CTA sine transform");
         d.pairs = P;
-        const int smem = P * N * 16;
+        // the attribute is per function, shared by every plan in the process:
+        // allow the largest plan once instead of the current one
+        static const int kMaxSmem = 200 * 1024;
         PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<0>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
         PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     } else {
         std::vector<double> kern((size_t)N * N);
         for (int k = 0; k < N; ++k)
