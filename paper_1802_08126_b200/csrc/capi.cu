@@ -30,7 +30,7 @@ void pint_check_cuda(cudaError_t e, const char* what) {
 static const char* kKernelNames[K_COUNT] = {
     "timeop_K", "timeop_Kt", "timeop_Abd", "timeop_r1", "timeop_z", "fold_rhs", "aref",
     "mg_pre_fine", "mg_pre_coarse", "mg_post_fine", "mg_post_coarse",
-    "dst_inverse_transpose", "dst_inverse", "reduce"};
+    "dst_inverse_transpose", "dst_inverse", "reduce", "mg_tail"};
 
 ProfScope::ProfScope(pint_ctx* ctx, int kid, double bytes) : c(ctx), on(ctx->profile) {
     if (!on) return;
@@ -428,6 +428,7 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
         s.n_sets = n_sets;
         s.tab = upload(c, tables, ntab);
         s.sid = upload(c, sid, c->N);
+        pint::mg_compute_shapes(s, tables);
         ensure_levels(c, s.m);
         s.ready = true;
     });

@@ -1,0 +1,813 @@
+// Batched multigrid V-cycle, B200 edition.
+//
+// Reference: MgVCycleSolver._vcycle / apply (spatial.py:148-169), 2D
+// hierarchy of build_mg_hierarchy (spatial.py:100-113): one damped-Jacobi
+// pre- and post-sweep (dinv = damping/diag, spatial.py:142), restriction P^T
+// (unscaled bilinear full weighting), prolongation P = kron(P1, P1)
+// (spatial.py:75-84,110), Galerkin coarse stencils (host tables), 1x1 direct
+// coarsest solve b/a (SpdFactor, spatial.py:143,149-150).  Every plane of the
+// batch (all N time steps for A~, all N DST modes for H~) goes through the
+// same launches.
+//
+// Large levels (m >= 64) stream through persistent band kernels: a CTA owns
+// a row band of one plane at a time, the band's inputs arrive by TMA bulk
+// copy into a double-buffered shared-memory ring (band.cuh) while the
+// previous band is computed, so HBM latency is hidden without occupancy.
+//   k_band_pre : x0 = dinv*b, r = b - A x0, b_c = P^T r    (one pass over b)
+//   k_band_post: x = x0 + P e, x += dinv*(b - A x), epilogue (one pass)
+// Small levels (m <= 63) run in k_mg_tail: one CTA per plane holds every
+// remaining level in shared memory and does descend, coarsest solve and
+// ascend in one launch (for BASELINE config 1 that is the whole V-cycle).
+//
+// Bit-exactness: every row sum is evaluated in scipy's CSR column order
+// starting from 0, without FMA (-fmad=false); terms whose coefficient is an
+// exact zero on every plane (the SE/NW entries of the P1 diagonal split, the
+// four diagonal entries of the stiffness) are skipped, which adds +-0 and so
+// cannot change a non-zero sum.
+#include <algorithm>
+
+#include "band.cuh"
+#include "pint_device.cuh"
+#include "pint_internal.cuh"
+
+namespace pint {
+
+constexpr int BT = 256;       // threads of the band kernels
+constexpr int TT = 512;       // threads of the tail kernel
+constexpr int NSTAGE = 2;
+
+// stencil shapes: which of the 9 CSR positions can be non-zero
+enum Shape : int { SH_FULL = 0, SH_SEVEN = 1, SH_FIVE = 2 };
+
+template <int SH>
+__device__ __forceinline__ constexpr bool used(int k) {
+    return SH == SH_FULL ? true
+         : SH == SH_SEVEN ? (k != 2 && k != 6)
+                          : (k == 1 || k == 3 || k == 4 || k == 5 || k == 7);
+}
+
+// CSR-ordered row sum at column x; rm/r0/rp point at column 0 of rows y-1,
+// y, y+1; hs/hn: rows y-1 / y+1 exist; w/e: columns x-1 / x+1 exist.
+template <int SH>
+__device__ __forceinline__ double row_sum(const double* c, const double* rm, const double* r0,
+                                          const double* rp, int x, bool hs, bool hn, bool w,
+                                          bool e) {
+    double s = 0.0;
+    bool first = true;
+    auto acc = [&](double t) {
+        if (first) {
+            s = t;
+            first = false;
+        } else {
+            s = s + t;
+        }
+    };
+    if (used<SH>(0)) acc(c[0] * ((hs && w) ? rm[x - 1] : 0.0));
+    if (used<SH>(1)) acc(c[1] * (hs ? rm[x] : 0.0));
+    if (used<SH>(2)) acc(c[2] * ((hs && e) ? rm[x + 1] : 0.0));
+    if (used<SH>(3)) acc(c[3] * (w ? r0[x - 1] : 0.0));
+    if (used<SH>(4)) acc(c[4] * r0[x]);
+    if (used<SH>(5)) acc(c[5] * (e ? r0[x + 1] : 0.0));
+    if (used<SH>(6)) acc(c[6] * ((hn && w) ? rp[x - 1] : 0.0));
+    if (used<SH>(7)) acc(c[7] * (hn ? rp[x] : 0.0));
+    if (used<SH>(8)) acc(c[8] * ((hn && e) ? rp[x + 1] : 0.0));
+    return s;
+}
+
+// logical row pointer of a band buffer whose slot 0 holds plane row `first`,
+// filled by a copy of rows [r_lo, r_hi) of plane `pb` (element base of plane)
+struct BandView {
+    const double* p;  // &row(first)[0]
+    __device__ __forceinline__ const double* row(int slot, int m) const { return p + slot * m; }
+};
+
+// element shift that makes the bulk-copy destination 16-byte aligned
+__device__ __forceinline__ int band_shift(long long pb, int m, int first, int r_lo) {
+    const long long e0 = pb + (long long)r_lo * m;
+    const int off = (int)(e0 & 1);
+    const int slot = (r_lo - first) * m;
+    return (slot - off) & 1;
+}
+
+// producer: copy rows [r_lo, r_hi) (clipped to [0, rows_total)) of plane
+// `plane` into `buf` laid out with slot 0 = plane row `first`
+__device__ __forceinline__ void band_issue(double* buf, const double* slab, long long pb, int m,
+                                           int first, int r_lo, int r_hi, uint64_t* bar) {
+    if (r_hi <= r_lo) return;
+    const Span s = span_of(pb + (long long)r_lo * m, pb + (long long)r_hi * m);
+    const int sh = band_shift(pb, m, first, r_lo);
+    double* dst = buf + sh + (r_lo - first) * m - s.off;
+    bulk_g2s(dst, slab + s.g0, s.bytes, bar);
+}
+
+__device__ __forceinline__ uint32_t band_bytes(long long pb, int m, int r_lo, int r_hi) {
+    if (r_hi <= r_lo) return 0;
+    return span_of(pb + (long long)r_lo * m, pb + (long long)r_hi * m).bytes;
+}
+
+__device__ __forceinline__ BandView band_view(const double* buf, long long pb, int m, int first,
+                                              int r_lo) {
+    return BandView{buf + band_shift(pb, m, first, r_lo)};
+}
+
+// ============================================================================
+// pre-smoothing + residual + restriction, level (m -> mc)
+// ============================================================================
+struct PreParams {
+    int m, mc, B, Hc, nbands;
+    int words_b, words_x, words_r;  // smem words: stage b, x0, residual
+    const double* b;
+    double* bc;
+    const double* tab;  // level table [n_sets][10]
+    const int* sid;
+};
+
+template <int SH>
+__global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) uint64_t bars[NSTAGE];
+    const int m = P.m, mc = P.mc;
+    const long long n = (long long)m * m, nc = (long long)mc * mc;
+    double* stage[NSTAGE];
+    for (int s = 0; s < NSTAGE; ++s) stage[s] = smem + s * P.words_b;
+    double* sx = smem + NSTAGE * P.words_b;
+    double* sr = sx + P.words_x;
+    const int units = P.B * P.nbands;
+    const int tid = threadIdx.x;
+    const int TX = min(256, ((m + 31) / 32) * 32);
+    const int TY = BT / TX;
+    const int tx = tid % TX, ty = tid / TX;
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto unit_rows = [&](int u, int& plane, int& Y0, int& Y1) {
+        plane = u / P.nbands;
+        const int j = u - plane * P.nbands;
+        Y0 = j * P.Hc;
+        Y1 = min(mc, Y0 + P.Hc);
+    };
+    auto issue = [&](int u, int s) {
+        int plane, Y0, Y1;
+        unit_rows(u, plane, Y0, Y1);
+        const long long pb = plane * n;
+        const int first = 2 * Y0 - 1;
+        const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
+        fence_proxy_async();
+        mbar_expect_tx(&bars[s], band_bytes(pb, m, lo, hi));
+        band_issue(stage[s], P.b, pb, m, first, lo, hi, &bars[s]);
+    };
+    int k = 0;
+    const int u0 = blockIdx.x;
+    if (tid == 0 && u0 < units) issue(u0, 0);
+    for (int u = u0; u < units; u += gridDim.x, ++k) {
+        const int s = k % NSTAGE;
+        if (tid == 0 && u + (int)gridDim.x < units) issue(u + gridDim.x, (k + 1) % NSTAGE);
+        int plane, Y0, Y1;
+        unit_rows(u, plane, Y0, Y1);
+        const long long pb = plane * n;
+        const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+        double ca[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ca[q] = __ldg(tb + q);
+        const double d = __ldg(tb + 9);
+        const int first = 2 * Y0 - 1;
+        const int lo = max(0, first);
+        mbar_wait(&bars[s], (k / NSTAGE) & 1);
+        const BandView vb = band_view(stage[s], pb, m, first, lo);
+        const int nrow_b = 2 * (Y1 - Y0) + 3;
+        // x0 = dinv * b on the staged rows (rows outside the plane stay unused)
+        for (int r = ty; r < nrow_b; r += TY) {
+            const int gy = first + r;
+            if (gy < 0 || gy >= m) continue;
+            const double* br = vb.row(r, m);
+            double* xr = sx + r * m;
+            for (int x = tx; x < m; x += TX) xr[x] = d * br[x];
+        }
+        __syncthreads();
+        // residual r = b - A x0 on fine rows 2*Y0 .. 2*Y1
+        const int nrow_r = 2 * (Y1 - Y0) + 1;
+        for (int r = ty; r < nrow_r; r += TY) {
+            const int gy = 2 * Y0 + r;  // slot r+1 of the staged rows
+            const bool hs = gy > 0, hn = gy < m - 1;
+            const double* xm = sx + r * m;
+            const double* x0 = xm + m;
+            const double* xp = x0 + m;
+            const double* br = vb.row(r + 1, m);
+            double* rr = sr + r * m;
+            for (int x = tx; x < m; x += TX)
+                rr[x] = br[x] - row_sum<SH>(ca, xm, x0, xp, x, hs, hn, x > 0, x < m - 1);
+        }
+        __syncthreads();
+        // restriction: P^T r, ascending fine index (csc_matvec order)
+        const int ncr = Y1 - Y0;
+        const int TXC = TX, TYC = TY;
+        for (int r = ty; r < ncr; r += TYC) {
+            const double* r0 = sr + (2 * r) * m;
+            const double* r1 = r0 + m;
+            const double* r2 = r1 + m;
+            double* out = P.bc + plane * nc + (long long)(Y0 + r) * mc;
+            for (int X = tx; X < mc; X += TXC) {
+                const int f = 2 * X;
+                double v = 0.25 * r0[f];
+                v = v + 0.5 * r0[f + 1];
+                v = v + 0.25 * r0[f + 2];
+                v = v + 0.5 * r1[f];
+                v = v + 1.0 * r1[f + 1];
+                v = v + 0.5 * r1[f + 2];
+                v = v + 0.25 * r2[f];
+                v = v + 0.5 * r2[f + 1];
+                v = v + 0.25 * r2[f + 2];
+                out[X] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================================
+// prolongation + post-smoothing (+ finest-level epilogue), level (mc -> m)
+// ============================================================================
+struct PostBandParams {
+    int m, mc, B, H, nbands;
+    int words_b, words_e, words_q, words_x;  // stage: b, e, pin|aux ; work: x
+    int nq;                                  // staged epilogue inputs (0 or 1)
+    const double* b;
+    const double* ec;
+    const double* tab;
+    const int* sid;
+    double* out;
+    int epi;
+    double scale;
+    const double* steps;
+    const double* pin;
+    const double* aux;
+    double* part;
+};
+
+template <int SH, int EPI>
+__global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) uint64_t bars[NSTAGE];
+    const int m = P.m, mc = P.mc;
+    const long long n = (long long)m * m, nc = (long long)mc * mc;
+    const int wstage = P.words_b + P.words_e + P.words_q;
+    double* sx = smem + NSTAGE * wstage;
+    const int units = P.B * P.nbands;
+    const int tid = threadIdx.x;
+    const int TX = min(256, ((m + 31) / 32) * 32);
+    const int TY = BT / TX;
+    const int tx = tid % TX, ty = tid / TX;
+    constexpr bool HAS_Q = EPI == EPI_UZAWA_P || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
+    constexpr bool HAS_DOT =
+        EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
+    const double* qsrc = EPI == EPI_UZAWA_P ? P.pin : P.aux;
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto sb = [&](int s) { return smem + s * wstage; };
+    auto se = [&](int s) { return smem + s * wstage + P.words_b; };
+    auto sq = [&](int s) { return smem + s * wstage + P.words_b + P.words_e; };
+    auto unit_rows = [&](int u, int& plane, int& y0, int& y1) {
+        plane = u / P.nbands;
+        const int j = u - plane * P.nbands;
+        y0 = j * P.H;
+        y1 = min(m, y0 + P.H);
+    };
+    auto issue = [&](int u, int s) {
+        int plane, y0, y1;
+        unit_rows(u, plane, y0, y1);
+        const long long pb = plane * n, pc = plane * nc;
+        const int fb = y0 - 1, lob = max(0, fb), hib = min(m, y1 + 1);
+        const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
+        uint32_t tx_bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
+        if (HAS_Q) tx_bytes += band_bytes(pb, m, y0, y1);
+        fence_proxy_async();
+        mbar_expect_tx(&bars[s], tx_bytes);
+        band_issue(sb(s), P.b, pb, m, fb, lob, hib, &bars[s]);
+        band_issue(se(s), P.ec, pc, mc, fe, loe, hie, &bars[s]);
+        if (HAS_Q) band_issue(sq(s), qsrc, pb, m, y0, y0, y1, &bars[s]);
+    };
+    double acc = 0.0;
+    int k = 0;
+    const int u0 = blockIdx.x;
+    if (tid == 0 && u0 < units) issue(u0, 0);
+    for (int u = u0; u < units; u += gridDim.x, ++k) {
+        const int s = k % NSTAGE;
+        if (tid == 0 && u + (int)gridDim.x < units) issue(u + gridDim.x, (k + 1) % NSTAGE);
+        int plane, y0, y1;
+        unit_rows(u, plane, y0, y1);
+        const long long pb = plane * n, pc = plane * nc;
+        const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+        double ca[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ca[q] = __ldg(tb + q);
+        const double d = __ldg(tb + 9);
+        const int fb = y0 - 1, lob = max(0, fb);
+        const int fe = y0 / 2 - 1, loe = max(0, fe);
+        mbar_wait(&bars[s], (k / NSTAGE) & 1);
+        const BandView vb = band_view(sb(s), pb, m, fb, lob);
+        const BandView ve = band_view(se(s), pc, mc, fe, loe);
+        // x = dinv*b + P e on rows y0-1 .. y1 (slots 0 .. y1-y0+1)
+        const int nrx = y1 - y0 + 2;
+        for (int r = ty; r < nrx; r += TY) {
+            const int gy = fb + r;
+            double* xr = sx + r * m;
+            if (gy < 0 || gy >= m) {
+                for (int x = tx; x < m; x += TX) xr[x] = 0.0;
+                continue;
+            }
+            const double* br = vb.row(r, m);
+            // coarse rows contributing to fine row gy (ascending)
+            int ja, jb;
+            double wa, wb;
+            if (gy & 1) {
+                ja = (gy - 1) >> 1;
+                wa = 1.0;
+                jb = -1;
+                wb = 0.0;
+            } else {
+                ja = (gy >> 1) - 1;
+                wa = 0.5;
+                jb = gy >> 1;
+                wb = 0.5;
+            }
+            const bool va = ja >= 0 && ja < mc, vbb = jb >= 0 && jb < mc;
+            const double* ea = ve.row(va ? ja - fe : 0, mc);
+            const double* eb = ve.row(vbb ? jb - fe : 0, mc);
+            for (int x = tx; x < m; x += TX) {
+                int ia, ib;
+                double ua, ub;
+                if (x & 1) {
+                    ia = (x - 1) >> 1;
+                    ua = 1.0;
+                    ib = -1;
+                    ub = 0.0;
+                } else {
+                    ia = (x >> 1) - 1;
+                    ua = 0.5;
+                    ib = x >> 1;
+                    ub = 0.5;
+                }
+                const bool ha = ia >= 0, hb = ib >= 0 && ib < mc;
+                // csr_matvec over ascending coarse index: (ja,ia),(ja,ib),(jb,ia),(jb,ib)
+                double pe = 0.0;
+                bool first = true;
+                auto add = [&](bool ok, double w, double e) {
+                    if (!ok) return;
+                    const double t = w * e;
+                    pe = first ? t : pe + t;
+                    first = false;
+                };
+                add(va && ha, wa * ua, ea[ia]);
+                add(va && hb, wa * ub, ea[ib]);
+                add(vbb && ha, wb * ua, eb[ia]);
+                add(vbb && hb, wb * ub, eb[ib]);
+                xr[x] = d * br[x] + pe;
+            }
+        }
+        __syncthreads();
+        // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
+        const BandView vq = band_view(sq(s), pb, m, y0, y0);
+        for (int r = ty; r < y1 - y0; r += TY) {
+            const int gy = y0 + r;
+            const bool hs = gy > 0, hn = gy < m - 1;
+            const double* xm = sx + r * m;
+            const double* x0 = xm + m;
+            const double* xp = x0 + m;
+            const double* br = vb.row(r + 1, m);
+            const double* qr = vq.row(r, m);
+            const long long gbase = pb + (long long)gy * m;
+            const double tau = (EPI == EPI_DIV_TAU || EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU)
+                                   ? __ldg(P.steps + plane)
+                                   : 1.0;
+            for (int x = tx; x < m; x += TX) {
+                const double bv = br[x];
+                const double xn =
+                    x0[x] + d * (bv - row_sum<SH>(ca, xm, x0, xp, x, hs, hn, x > 0, x < m - 1));
+                if (EPI == EPI_PLAIN) {
+                    P.out[gbase + x] = xn;
+                } else if (EPI == EPI_DIV_TAU) {
+                    P.out[gbase + x] = xn / tau;
+                } else if (EPI == EPI_UZAWA_P) {
+                    const double dp = xn / tau;
+                    P.out[gbase + x] = qr[x] + dp;
+                    acc += bv * dp;
+                } else if (EPI == EPI_DOT_TAU) {
+                    acc += bv * (xn / tau);
+                } else if (EPI == EPI_SCALE) {
+                    P.out[gbase + x] = P.scale * xn;
+                } else if (EPI == EPI_SCALE_DOT) {
+                    const double w = P.scale * xn;
+                    P.out[gbase + x] = w;
+                    acc += qr[x] * w;
+                } else if (EPI == EPI_SCALE_DOTONLY) {
+                    acc += qr[x] * (P.scale * xn);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (HAS_DOT) {
+        const double s = block_sum<BT>(acc);
+        if (tid == 0) P.part[blockIdx.x] = s;
+    }
+}
+
+// ============================================================================
+// tail: levels lt..L-1 of one plane entirely in shared memory
+// ============================================================================
+struct TailParams {
+    int lt, L, B;
+    int m[12];
+    int off_b[12], off_x[12];  // smem word offsets per level
+    int off_r;
+    const double* tab;         // all levels [L][n_sets][10]
+    int n_sets;
+    const int* sid;
+    const double* b;           // level lt rhs, B planes
+    double* out;               // level lt solution (or finest epilogue target)
+    int epi;
+    double scale;
+    const double* steps;
+    const double* pin;
+    const double* aux;
+    double* part;
+};
+
+__device__ __forceinline__ double row_sum_any(const double* c, const double* v, int m, int y,
+                                              int x) {
+    const bool hs = y > 0, hn = y < m - 1, w = x > 0, e = x < m - 1;
+    const double* r0 = v + y * m;
+    return row_sum<SH_FULL>(c, r0 - m, r0, r0 + m, x, hs, hn, w, e);
+}
+
+__global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x;
+    double acc = 0.0;
+    for (int plane = blockIdx.x; plane < P.B; plane += gridDim.x) {
+        const int set = __ldg(P.sid + plane);
+        const int mt = P.m[P.lt];
+        const long long nt = (long long)mt * mt;
+        {
+            double* B0 = smem + P.off_b[P.lt];
+            const double* src = P.b + plane * nt;
+            for (int i = tid; i < nt; i += TT) B0[i] = __ldg(src + i);
+        }
+        __syncthreads();
+        // descend
+        for (int l = P.lt; l + 1 < P.L; ++l) {
+            const int m = P.m[l], mc = P.m[l + 1];
+            const double* tb = P.tab + ((size_t)l * P.n_sets + set) * PINT_TW;
+            double ca[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) ca[q] = __ldg(tb + q);
+            const double d = __ldg(tb + 9);
+            double* Bl = smem + P.off_b[l];
+            double* Xl = smem + P.off_x[l];
+            double* R = smem + P.off_r;
+            for (int i = tid; i < m * m; i += TT) Xl[i] = d * Bl[i];
+            __syncthreads();
+            for (int i = tid; i < m * m; i += TT) {
+                const int y = i / m, x = i - y * m;
+                R[i] = Bl[i] - row_sum_any(ca, Xl, m, y, x);
+            }
+            __syncthreads();
+            double* Bc = smem + P.off_b[l + 1];
+            for (int i = tid; i < mc * mc; i += TT) {
+                const int Y = i / mc, X = i - Y * mc;
+                const double* r0 = R + (2 * Y) * m + 2 * X;
+                const double* r1 = r0 + m;
+                const double* r2 = r1 + m;
+                double v = 0.25 * r0[0];
+                v = v + 0.5 * r0[1];
+                v = v + 0.25 * r0[2];
+                v = v + 0.5 * r1[0];
+                v = v + 1.0 * r1[1];
+                v = v + 0.5 * r1[2];
+                v = v + 0.25 * r2[0];
+                v = v + 0.5 * r2[1];
+                v = v + 0.25 * r2[2];
+                Bc[i] = v;
+            }
+            __syncthreads();
+        }
+        // coarsest 1x1 (or general single point): x = b / a
+        {
+            const int l = P.L - 1;
+            const double a = __ldg(P.tab + ((size_t)l * P.n_sets + set) * PINT_TW + 4);
+            double* Bl = smem + P.off_b[l];
+            double* Xl = smem + P.off_x[l];
+            const int mm = P.m[l] * P.m[l];
+            for (int i = tid; i < mm; i += TT) Xl[i] = Bl[i] / a;
+            __syncthreads();
+        }
+        // ascend
+        for (int l = P.L - 2; l >= P.lt; --l) {
+            const int m = P.m[l], mc = P.m[l + 1];
+            const double* tb = P.tab + ((size_t)l * P.n_sets + set) * PINT_TW;
+            double ca[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) ca[q] = __ldg(tb + q);
+            const double d = __ldg(tb + 9);
+            double* Bl = smem + P.off_b[l];
+            double* Xl = smem + P.off_x[l];
+            const double* Ec = smem + P.off_x[l + 1];
+            double* R = smem + P.off_r;
+            for (int i = tid; i < m * m; i += TT) {
+                const int y = i / m, x = i - y * m;
+                int ja, jb, ia, ib;
+                double wa, wb, ua, ub;
+                if (y & 1) { ja = (y - 1) >> 1; wa = 1.0; jb = -1; wb = 0.0; }
+                else { ja = (y >> 1) - 1; wa = 0.5; jb = y >> 1; wb = 0.5; }
+                if (x & 1) { ia = (x - 1) >> 1; ua = 1.0; ib = -1; ub = 0.0; }
+                else { ia = (x >> 1) - 1; ua = 0.5; ib = x >> 1; ub = 0.5; }
+                const bool va = ja >= 0, vb2 = jb >= 0 && jb < mc;
+                const bool ha = ia >= 0, hb = ib >= 0 && ib < mc;
+                double pe = 0.0;
+                bool first = true;
+                auto add = [&](bool ok, double w, double e) {
+                    if (!ok) return;
+                    const double t = w * e;
+                    pe = first ? t : pe + t;
+                    first = false;
+                };
+                add(va && ha, wa * ua, va && ha ? Ec[ja * mc + ia] : 0.0);
+                add(va && hb, wa * ub, va && hb ? Ec[ja * mc + ib] : 0.0);
+                add(vb2 && ha, wb * ua, vb2 && ha ? Ec[jb * mc + ia] : 0.0);
+                add(vb2 && hb, wb * ub, vb2 && hb ? Ec[jb * mc + ib] : 0.0);
+                Xl[i] = Xl[i] + pe;  // x0 (= dinv*b, kept from the descent) + P e
+            }
+            __syncthreads();
+            const bool top = (l == P.lt);
+            const long long gplane = plane * (long long)m * m;
+            for (int i = tid; i < m * m; i += TT) {
+                const int y = i / m, x = i - y * m;
+                const double bv = Bl[i];
+                const double xn = Xl[i] + d * (bv - row_sum_any(ca, Xl, m, y, x));
+                if (!top) {
+                    R[i] = xn;
+                    continue;
+                }
+                const long long gi = gplane + i;
+                switch (P.epi) {
+                    case EPI_PLAIN: P.out[gi] = xn; break;
+                    case EPI_DIV_TAU: P.out[gi] = xn / __ldg(P.steps + plane); break;
+                    case EPI_UZAWA_P: {
+                        const double dp = xn / __ldg(P.steps + plane);
+                        P.out[gi] = __ldg(P.pin + gi) + dp;
+                        acc += bv * dp;
+                        break;
+                    }
+                    case EPI_DOT_TAU: acc += bv * (xn / __ldg(P.steps + plane)); break;
+                    case EPI_SCALE: P.out[gi] = P.scale * xn; break;
+                    case EPI_SCALE_DOT: {
+                        const double w = P.scale * xn;
+                        P.out[gi] = w;
+                        acc += __ldg(P.aux + gi) * w;
+                        break;
+                    }
+                    case EPI_SCALE_DOTONLY: acc += __ldg(P.aux + gi) * (P.scale * xn); break;
+                }
+            }
+            __syncthreads();
+            if (!top) {
+                for (int i = tid; i < m * m; i += TT) Xl[i] = R[i];
+                __syncthreads();
+            }
+        }
+    }
+    if (P.part != nullptr) {
+        const double s = block_sum<TT>(acc);
+        if (tid == 0) P.part[blockIdx.x] = s;
+    }
+}
+
+// ============================================================================
+// host side
+// ============================================================================
+static bool epi_has_dot(int epi) {
+    return epi == EPI_UZAWA_P || epi == EPI_DOT_TAU || epi == EPI_SCALE_DOT ||
+           epi == EPI_SCALE_DOTONLY;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+constexpr int TAIL_MAX_M = 63;
+
+// shapes of the level tables: a position is skipped only if it is exactly 0
+// for every set of the level
+void mg_compute_shapes(MgSet& set, const double* tab) {
+    set.shape.assign(set.levels, SH_FULL);
+    for (int l = 0; l < set.levels; ++l) {
+        bool z[9] = {true, true, true, true, true, true, true, true, true};
+        for (int s = 0; s < set.n_sets; ++s)
+            for (int q = 0; q < 9; ++q)
+                if (tab[((size_t)l * set.n_sets + s) * PINT_TW + q] != 0.0) z[q] = false;
+        if (z[0] && z[2] && z[6] && z[8])
+            set.shape[l] = SH_FIVE;
+        else if (z[2] && z[6])
+            set.shape[l] = SH_SEVEN;
+    }
+}
+
+template <int SH>
+static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+    static bool attr = false;
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    k_band_pre<SH><<<grid, BT, smem, c->stream>>>(P);
+}
+
+template <int SH, int EPI>
+static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    static bool attr = false;
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    k_band_post<SH, EPI><<<grid, BT, smem, c->stream>>>(P);
+}
+
+template <int SH>
+static void launch_post_sh(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    switch (P.epi) {
+        case EPI_PLAIN: launch_post_epi<SH, EPI_PLAIN>(c, P, smem, grid); break;
+        case EPI_DIV_TAU: launch_post_epi<SH, EPI_DIV_TAU>(c, P, smem, grid); break;
+        case EPI_UZAWA_P: launch_post_epi<SH, EPI_UZAWA_P>(c, P, smem, grid); break;
+        case EPI_DOT_TAU: launch_post_epi<SH, EPI_DOT_TAU>(c, P, smem, grid); break;
+        case EPI_SCALE: launch_post_epi<SH, EPI_SCALE>(c, P, smem, grid); break;
+        case EPI_SCALE_DOT: launch_post_epi<SH, EPI_SCALE_DOT>(c, P, smem, grid); break;
+        case EPI_SCALE_DOTONLY: launch_post_epi<SH, EPI_SCALE_DOTONLY>(c, P, smem, grid); break;
+        default: pint_throw(PINT_INPUT, "unknown epilogue");
+    }
+}
+
+static int blocks_per_sm(size_t smem) {
+    const size_t per_sm = 227 * 1024;
+    int k = (int)(per_sm / (smem + 1024));
+    if (k < 1) k = 1;
+    if (k > 4) k = 4;
+    return k;
+}
+
+void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
+            double scale, const double* pin, const double* aux, int acc_slot) {
+    MgSet& s = c->mg[which];
+    if (!s.ready) pint_throw(PINT_INPUT, "multigrid set not configured");
+    const int L = s.levels;
+    auto lvl_tab = [&](int l) { return s.tab + (size_t)l * s.n_sets * PINT_TW; };
+    int lt = 0;
+    while (lt < L && s.m[lt] > TAIL_MAX_M) ++lt;
+    const int sms = num_sms();
+    const bool dot = epi_has_dot(epi);
+    // ---- descend through the band levels ----
+    const double* bl = b;
+    for (int l = 0; l < lt; ++l) {
+        PreParams P{};
+        P.m = s.m[l];
+        P.mc = s.m[l + 1];
+        P.B = count;
+        P.Hc = P.m > 300 ? 2 : 4;
+        P.nbands = (P.mc + P.Hc - 1) / P.Hc;
+        P.words_b = band_words(2 * P.Hc + 3, P.m);
+        P.words_x = (2 * P.Hc + 3) * P.m;
+        P.words_r = (2 * P.Hc + 1) * P.m;
+        P.b = bl;
+        P.bc = c->lev_b[l + 1];
+        P.tab = lvl_tab(l);
+        P.sid = s.sid;
+        const size_t smem = sizeof(double) * (NSTAGE * P.words_b + P.words_x + P.words_r);
+        const int units = P.B * P.nbands;
+        const int grid = std::min(units, sms * blocks_per_sm(smem));
+        ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
+                       8.0 * count * ((double)P.m * P.m + (double)P.mc * P.mc));
+        switch (s.shape[l]) {
+            case SH_FULL: launch_pre_sh<SH_FULL>(c, P, smem, grid); break;
+            case SH_SEVEN: launch_pre_sh<SH_SEVEN>(c, P, smem, grid); break;
+            default: launch_pre_sh<SH_FIVE>(c, P, smem, grid); break;
+        }
+        PINT_LAUNCHED(c);
+        bl = c->lev_b[l + 1];
+    }
+    PINT_CUDA_CHECK(cudaGetLastError());
+    // ---- tail: levels lt..L-1 in shared memory ----
+    {
+        TailParams T{};
+        T.lt = lt;
+        T.L = L;
+        T.B = count;
+        int off = 0;
+        int maxm2 = 0;
+        for (int l = lt; l < L; ++l) {
+            T.m[l] = s.m[l];
+            T.off_b[l] = off;
+            off += ((s.m[l] * s.m[l] + 1) / 2) * 2;
+            T.off_x[l] = off;
+            off += ((s.m[l] * s.m[l] + 1) / 2) * 2;
+            maxm2 = std::max(maxm2, s.m[l] * s.m[l]);
+        }
+        T.off_r = off;
+        off += maxm2;
+        T.tab = s.tab;
+        T.n_sets = s.n_sets;
+        T.sid = s.sid;
+        T.b = bl;
+        const bool top = lt == 0;
+        T.out = top ? out : c->lev_x[lt];
+        T.epi = top ? epi : EPI_PLAIN;
+        T.scale = scale;
+        T.steps = c->d_steps;
+        T.pin = pin;
+        T.aux = aux;
+        const size_t smem = sizeof(double) * off;
+        static bool attr = false;
+        if (!attr) {
+            PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 200 * 1024));
+            attr = true;
+        }
+        if (smem > 200 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
+        const int grid = std::min(count, sms * blocks_per_sm(smem));
+        if (top && dot) {
+            ensure_partials(c, grid);
+            T.part = c->d_part;
+        }
+        const double fine = (double)s.m[lt] * s.m[lt];
+        ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_TAIL, 8.0 * count * 2.0 * fine);
+        k_mg_tail<<<grid, TT, smem, c->stream>>>(T);
+        PINT_LAUNCHED(c);
+        PINT_CUDA_CHECK(cudaGetLastError());
+        if (top && dot) reduce_partials(c, grid, acc_slot);
+    }
+    // ---- ascend through the band levels ----
+    for (int l = lt - 1; l >= 0; --l) {
+        PostBandParams P{};
+        P.m = s.m[l];
+        P.mc = s.m[l + 1];
+        P.B = count;
+        P.H = P.m > 300 ? 4 : 8;
+        P.nbands = (P.m + P.H - 1) / P.H;
+        const bool top = l == 0;
+        P.epi = top ? epi : EPI_PLAIN;
+        const bool has_q = P.epi == EPI_UZAWA_P || P.epi == EPI_SCALE_DOT ||
+                           P.epi == EPI_SCALE_DOTONLY;
+        P.words_b = band_words(P.H + 2, P.m);
+        P.words_e = band_words(P.H / 2 + 2, P.mc);
+        P.words_q = has_q ? band_words(P.H, P.m) : 0;
+        P.words_x = (P.H + 2) * P.m;
+        P.b = top ? b : c->lev_b[l];
+        P.ec = c->lev_x[l + 1];
+        P.tab = lvl_tab(l);
+        P.sid = s.sid;
+        P.out = top ? out : c->lev_x[l];
+        P.scale = scale;
+        P.steps = c->d_steps;
+        P.pin = pin;
+        P.aux = aux;
+        const size_t smem =
+            sizeof(double) * (NSTAGE * (P.words_b + P.words_e + P.words_q) + P.words_x);
+        const int units = P.B * P.nbands;
+        const int grid = std::min(units, sms * blocks_per_sm(smem));
+        const bool dl = top && dot;
+        if (dl) {
+            ensure_partials(c, grid);
+            P.part = c->d_part;
+        }
+        const double fine = (double)P.m * P.m, coarse = (double)P.mc * P.mc;
+        double words = fine + coarse;
+        if (P.epi != EPI_DOT_TAU && P.epi != EPI_SCALE_DOTONLY) words += fine;
+        if (has_q) words += fine;
+        {
+            ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE, 8.0 * count * words);
+            switch (s.shape[l]) {
+                case SH_FULL: launch_post_sh<SH_FULL>(c, P, smem, grid); break;
+                case SH_SEVEN: launch_post_sh<SH_SEVEN>(c, P, smem, grid); break;
+                default: launch_post_sh<SH_FIVE>(c, P, smem, grid); break;
+            }
+        }
+        PINT_LAUNCHED(c);
+        PINT_CUDA_CHECK(cudaGetLastError());
+        if (dl) reduce_partials(c, grid, acc_slot);
+    }
+}
+
+}  // namespace pint

@@ -50,6 +50,7 @@ struct MgSet {
     int n_sets = 0;
     double* tab = nullptr;    // device [levels][n_sets][PINT_TW]
     int* sid = nullptr;       // device [B]
+    std::vector<int> shape;   // per level: which stencil positions can be non-zero
     bool ready = false;
 };
 
@@ -68,7 +69,7 @@ struct DstPlan {
 enum KernelId : int {
     K_TIMEOP_K = 0, K_TIMEOP_KT, K_TIMEOP_ABD, K_TIMEOP_R1, K_TIMEOP_Z, K_FOLD, K_AREF,
     K_MG_PRE_FINE, K_MG_PRE_COARSE, K_MG_POST_FINE, K_MG_POST_COARSE,
-    K_DST_T, K_DST, K_REDUCE, K_COUNT
+    K_DST_T, K_DST, K_REDUCE, K_MG_TAIL, K_COUNT
 };
 
 struct KStat {
@@ -162,6 +163,7 @@ void launch_aref(pint_ctx* c, const double* in, double* out, int count);
 // pin: EPI_UZAWA_P input p;  aux: EPI_SCALE_DOT partner vector; acc_slot: d_acc index
 void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
             double scale, const double* pin, const double* aux, int acc_slot);
+void mg_compute_shapes(MgSet& set, const double* tables);
 
 // sine transforms (dst.cu)
 void dst_plan_build(DstPlan& d, int N);
