@@ -111,11 +111,41 @@ __device__ __forceinline__ BandView band_view(const double* buf, long long pb, i
 }
 
 // ============================================================================
+// shared helpers for the padded work tiles
+// ============================================================================
+// Row sum on a zero-padded tile (pitch m+2, zero columns 0 and m+1, zero rows
+// outside the plane): no boundary predicates.  rm/r0/rp point at column 0 of
+// the padded rows y-1, y, y+1; x is the padded column (1..m).
+template <int SH>
+__device__ __forceinline__ double row_sum_pad(const double* c, const double* rm,
+                                              const double* r0, const double* rp, int x) {
+    double s = 0.0;
+    bool first = true;
+#define PINT_TERM(K, V)                      \
+    if (used<SH>(K)) {                       \
+        const double t_ = c[K] * (V);        \
+        s = first ? t_ : s + t_;             \
+        first = false;                       \
+    }
+    PINT_TERM(0, rm[x - 1])
+    PINT_TERM(1, rm[x])
+    PINT_TERM(2, rm[x + 1])
+    PINT_TERM(3, r0[x - 1])
+    PINT_TERM(4, r0[x])
+    PINT_TERM(5, r0[x + 1])
+    PINT_TERM(6, rp[x - 1])
+    PINT_TERM(7, rp[x])
+    PINT_TERM(8, rp[x + 1])
+#undef PINT_TERM
+    return s;
+}
+
+// ============================================================================
 // pre-smoothing + residual + restriction, level (m -> mc)
 // ============================================================================
 struct PreParams {
     int m, mc, B, Hc, nbands;
-    int words_b, words_x, words_r;  // smem words: stage b, x0, residual
+    int words_b, words_x, words_r;  // smem words: stage b, padded x0 tile, residual
     const double* b;
     double* bc;
     const double* tab;  // level table [n_sets][10]
@@ -126,17 +156,19 @@ template <int SH>
 __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t bars[NSTAGE];
-    const int m = P.m, mc = P.mc;
+    const int m = P.m, mc = P.mc, mp = m + 2;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
     double* stage[NSTAGE];
     for (int s = 0; s < NSTAGE; ++s) stage[s] = smem + s * P.words_b;
-    double* sx = smem + NSTAGE * P.words_b;
-    double* sr = sx + P.words_x;
+    double* sx = smem + NSTAGE * P.words_b;  // (2Hc+3) x (m+2), zero-padded
+    double* sr = sx + P.words_x;             // (2Hc+1) x m
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
-    const int TX = min(256, ((m + 31) / 32) * 32);
-    const int TY = BT / TX;
+    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
     const int tx = tid % TX, ty = tid / TX;
+    const int TXC = min(BT, ((mc + 31) / 32) * 32), TYC = BT / TXC;
+    const int txc = tid % TXC, tyc = tid / TXC;
+    for (int i = tid; i < P.words_x; i += BT) sx[i] = 0.0;
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
@@ -177,38 +209,33 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
         mbar_wait(&bars[s], (k / NSTAGE) & 1);
         const BandView vb = band_view(stage[s], pb, m, first, lo);
         const int nrow_b = 2 * (Y1 - Y0) + 3;
-        // x0 = dinv * b on the staged rows (rows outside the plane stay unused)
+        // x0 = dinv * b into the padded tile (rows outside the plane = 0)
         for (int r = ty; r < nrow_b; r += TY) {
             const int gy = first + r;
-            if (gy < 0 || gy >= m) continue;
+            const bool in = gy >= 0 && gy < m;
             const double* br = vb.row(r, m);
-            double* xr = sx + r * m;
-            for (int x = tx; x < m; x += TX) xr[x] = d * br[x];
+            double* xr = sx + r * mp + 1;
+            for (int x = tx; x < m; x += TX) xr[x] = in ? d * br[x] : 0.0;
         }
         __syncthreads();
         // residual r = b - A x0 on fine rows 2*Y0 .. 2*Y1
         const int nrow_r = 2 * (Y1 - Y0) + 1;
         for (int r = ty; r < nrow_r; r += TY) {
-            const int gy = 2 * Y0 + r;  // slot r+1 of the staged rows
-            const bool hs = gy > 0, hn = gy < m - 1;
-            const double* xm = sx + r * m;
-            const double* x0 = xm + m;
-            const double* xp = x0 + m;
+            const double* xm = sx + r * mp;
             const double* br = vb.row(r + 1, m);
             double* rr = sr + r * m;
             for (int x = tx; x < m; x += TX)
-                rr[x] = br[x] - row_sum<SH>(ca, xm, x0, xp, x, hs, hn, x > 0, x < m - 1);
+                rr[x] = br[x] - row_sum_pad<SH>(ca, xm, xm + mp, xm + 2 * mp, x + 1);
         }
         __syncthreads();
         // restriction: P^T r, ascending fine index (csc_matvec order)
         const int ncr = Y1 - Y0;
-        const int TXC = TX, TYC = TY;
-        for (int r = ty; r < ncr; r += TYC) {
+        for (int r = tyc; r < ncr; r += TYC) {
             const double* r0 = sr + (2 * r) * m;
             const double* r1 = r0 + m;
             const double* r2 = r1 + m;
             double* out = P.bc + plane * nc + (long long)(Y0 + r) * mc;
-            for (int X = tx; X < mc; X += TXC) {
+            for (int X = txc; X < mc; X += TXC) {
                 const int f = 2 * X;
                 double v = 0.25 * r0[f];
                 v = v + 0.5 * r0[f + 1];
@@ -231,8 +258,7 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
 // ============================================================================
 struct PostBandParams {
     int m, mc, B, H, nbands;
-    int words_b, words_e, words_q, words_x;  // stage: b, e, pin|aux ; work: x
-    int nq;                                  // staged epilogue inputs (0 or 1)
+    int words_b, words_e, words_q, words_x;  // stage: b, e, pin|aux ; work: padded x
     const double* b;
     const double* ec;
     const double* tab;
@@ -250,19 +276,23 @@ template <int SH, int EPI>
 __global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t bars[NSTAGE];
-    const int m = P.m, mc = P.mc;
+    const int m = P.m, mc = P.mc, mp = m + 2;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
     const int wstage = P.words_b + P.words_e + P.words_q;
-    double* sx = smem + NSTAGE * wstage;
+    double* sx = smem + NSTAGE * wstage;  // (H+2) x (m+2) zero-padded
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
-    const int TX = min(256, ((m + 31) / 32) * 32);
-    const int TY = BT / TX;
+    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
     const int tx = tid % TX, ty = tid / TX;
+    // prolongation: thread owns coarse column pair (t-1, t) -> fine columns 2t, 2t+1
+    const int TXP = min(BT, ((mc + 1 + 31) / 32) * 32), TYP = BT / TXP;
+    const int txp = tid % TXP, typ = tid / TXP;
     constexpr bool HAS_Q = EPI == EPI_UZAWA_P || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
     constexpr bool HAS_DOT =
         EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
+    constexpr bool HAS_TAU = EPI == EPI_DIV_TAU || EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU;
     const double* qsrc = EPI == EPI_UZAWA_P ? P.pin : P.aux;
+    for (int i = tid; i < P.words_x; i += BT) sx[i] = 0.0;
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
@@ -311,98 +341,87 @@ __global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
         mbar_wait(&bars[s], (k / NSTAGE) & 1);
         const BandView vb = band_view(sb(s), pb, m, fb, lob);
         const BandView ve = band_view(se(s), pc, mc, fe, loe);
-        // x = dinv*b + P e on rows y0-1 .. y1 (slots 0 .. y1-y0+1)
+        // x = dinv*b + P e on rows y0-1 .. y1 (tile rows 0 .. y1-y0+1)
         const int nrx = y1 - y0 + 2;
-        for (int r = ty; r < nrx; r += TY) {
+        for (int r = typ; r < nrx; r += TYP) {
             const int gy = fb + r;
-            double* xr = sx + r * m;
+            double* xr = sx + r * mp + 1;
             if (gy < 0 || gy >= m) {
-                for (int x = tx; x < m; x += TX) xr[x] = 0.0;
+                for (int t = txp; t <= mc; t += TXP) {
+                    xr[2 * t] = 0.0;
+                    if (t < mc) xr[2 * t + 1] = 0.0;
+                }
                 continue;
             }
             const double* br = vb.row(r, m);
-            // coarse rows contributing to fine row gy (ascending)
-            int ja, jb;
-            double wa, wb;
-            if (gy & 1) {
-                ja = (gy - 1) >> 1;
-                wa = 1.0;
-                jb = -1;
-                wb = 0.0;
-            } else {
-                ja = (gy >> 1) - 1;
-                wa = 0.5;
-                jb = gy >> 1;
-                wb = 0.5;
-            }
-            const bool va = ja >= 0 && ja < mc, vbb = jb >= 0 && jb < mc;
-            const double* ea = ve.row(va ? ja - fe : 0, mc);
-            const double* eb = ve.row(vbb ? jb - fe : 0, mc);
-            for (int x = tx; x < m; x += TX) {
-                int ia, ib;
-                double ua, ub;
-                if (x & 1) {
-                    ia = (x - 1) >> 1;
-                    ua = 1.0;
-                    ib = -1;
-                    ub = 0.0;
-                } else {
-                    ia = (x >> 1) - 1;
-                    ua = 0.5;
-                    ib = x >> 1;
-                    ub = 0.5;
+            if (gy & 1) {  // one coarse row J, weight 1
+                const double* ea = ve.row(((gy - 1) >> 1) - fe, mc);
+                for (int t = txp; t <= mc; t += TXP) {
+                    const bool l = t >= 1, rr = t < mc;
+                    const double e0 = l ? ea[t - 1] : 0.0, e1 = rr ? ea[t] : 0.0;
+                    // even column 2t: (J, t-1) w .5, (J, t) w .5
+                    double pe;
+                    if (l && rr) pe = (1.0 * 0.5) * e0 + (1.0 * 0.5) * e1;
+                    else pe = l ? (1.0 * 0.5) * e0 : (1.0 * 0.5) * e1;
+                    xr[2 * t] = d * br[2 * t] + pe;
+                    if (rr) xr[2 * t + 1] = d * br[2 * t + 1] + (1.0 * 1.0) * e1;
                 }
-                const bool ha = ia >= 0, hb = ib >= 0 && ib < mc;
-                // csr_matvec over ascending coarse index: (ja,ia),(ja,ib),(jb,ia),(jb,ib)
-                double pe = 0.0;
-                bool first = true;
-                auto add = [&](bool ok, double w, double e) {
-                    if (!ok) return;
-                    const double t = w * e;
-                    pe = first ? t : pe + t;
-                    first = false;
-                };
-                add(va && ha, wa * ua, ea[ia]);
-                add(va && hb, wa * ub, ea[ib]);
-                add(vbb && ha, wb * ua, eb[ia]);
-                add(vbb && hb, wb * ub, eb[ib]);
-                xr[x] = d * br[x] + pe;
+            } else {  // coarse rows ja = gy/2-1, jb = gy/2, weights .5
+                const int ja = (gy >> 1) - 1, jb = gy >> 1;
+                const bool va = ja >= 0, vbb = jb < mc;
+                const double* ea = ve.row(va ? ja - fe : 0, mc);
+                const double* eb = ve.row(vbb ? jb - fe : 0, mc);
+                for (int t = txp; t <= mc; t += TXP) {
+                    const bool l = t >= 1, rr = t < mc;
+                    const double a0 = (va && l) ? ea[t - 1] : 0.0;
+                    const double a1 = (va && rr) ? ea[t] : 0.0;
+                    const double b0 = (vbb && l) ? eb[t - 1] : 0.0;
+                    const double b1 = (vbb && rr) ? eb[t] : 0.0;
+                    // even column 2t: (ja,t-1),(ja,t),(jb,t-1),(jb,t), w .25 each;
+                    // absent terms contribute +0 (exact)
+                    double pe = (0.5 * 0.5) * a0;
+                    pe = pe + (0.5 * 0.5) * a1;
+                    pe = pe + (0.5 * 0.5) * b0;
+                    pe = pe + (0.5 * 0.5) * b1;
+                    xr[2 * t] = d * br[2 * t] + pe;
+                    if (rr) {  // odd column 2t+1: (ja,t),(jb,t), w .5
+                        double po = (0.5 * 1.0) * a1;
+                        po = po + (0.5 * 1.0) * b1;
+                        xr[2 * t + 1] = d * br[2 * t + 1] + po;
+                    }
+                }
             }
         }
         __syncthreads();
         // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
         const BandView vq = band_view(sq(s), pb, m, y0, y0);
+        const double tau = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
         for (int r = ty; r < y1 - y0; r += TY) {
             const int gy = y0 + r;
-            const bool hs = gy > 0, hn = gy < m - 1;
-            const double* xm = sx + r * m;
-            const double* x0 = xm + m;
-            const double* xp = x0 + m;
+            const double* xm = sx + r * mp;
+            const double* x0 = xm + mp;
             const double* br = vb.row(r + 1, m);
             const double* qr = vq.row(r, m);
-            const long long gbase = pb + (long long)gy * m;
-            const double tau = (EPI == EPI_DIV_TAU || EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU)
-                                   ? __ldg(P.steps + plane)
-                                   : 1.0;
+            double* orow = P.out + pb + (long long)gy * m;
             for (int x = tx; x < m; x += TX) {
                 const double bv = br[x];
                 const double xn =
-                    x0[x] + d * (bv - row_sum<SH>(ca, xm, x0, xp, x, hs, hn, x > 0, x < m - 1));
+                    x0[x + 1] + d * (bv - row_sum_pad<SH>(ca, xm, x0, x0 + mp, x + 1));
                 if (EPI == EPI_PLAIN) {
-                    P.out[gbase + x] = xn;
+                    orow[x] = xn;
                 } else if (EPI == EPI_DIV_TAU) {
-                    P.out[gbase + x] = xn / tau;
+                    orow[x] = xn / tau;
                 } else if (EPI == EPI_UZAWA_P) {
                     const double dp = xn / tau;
-                    P.out[gbase + x] = qr[x] + dp;
+                    orow[x] = qr[x] + dp;
                     acc += bv * dp;
                 } else if (EPI == EPI_DOT_TAU) {
                     acc += bv * (xn / tau);
                 } else if (EPI == EPI_SCALE) {
-                    P.out[gbase + x] = P.scale * xn;
+                    orow[x] = P.scale * xn;
                 } else if (EPI == EPI_SCALE_DOT) {
                     const double w = P.scale * xn;
-                    P.out[gbase + x] = w;
+                    orow[x] = w;
                     acc += qr[x] * w;
                 } else if (EPI == EPI_SCALE_DOTONLY) {
                     acc += qr[x] * (P.scale * xn);
@@ -688,7 +707,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.Hc = P.m > 300 ? 2 : 4;
         P.nbands = (P.mc + P.Hc - 1) / P.Hc;
         P.words_b = band_words(2 * P.Hc + 3, P.m);
-        P.words_x = (2 * P.Hc + 3) * P.m;
+        P.words_x = (2 * P.Hc + 3) * (P.m + 2);
         P.words_r = (2 * P.Hc + 1) * P.m;
         P.b = bl;
         P.bc = c->lev_b[l + 1];
@@ -773,7 +792,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_b = band_words(P.H + 2, P.m);
         P.words_e = band_words(P.H / 2 + 2, P.mc);
         P.words_q = has_q ? band_words(P.H, P.m) : 0;
-        P.words_x = (P.H + 2) * P.m;
+        P.words_x = (P.H + 2) * (P.m + 2);
         P.b = top ? b : c->lev_b[l];
         P.ec = c->lev_x[l + 1];
         P.tab = lvl_tab(l);
