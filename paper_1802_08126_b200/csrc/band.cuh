@@ -60,6 +60,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barrier 1 over the NT consumer threads (the producer warp is excluded)
+template <int NT>
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+// deterministic sum over the NT consumer threads; valid in consumer thread 0
+template <int NT>
+__device__ __forceinline__ double consumer_sum(double v, double* scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int tid = threadIdx.x;
+    if ((tid & 31) == 0) scratch[tid >> 5] = v;
+    consumer_sync<NT>();
+    double s = 0.0;
+    if (tid == 0)
+        for (int w = 0; w < NT / 32; ++w) s += scratch[w];
+    return s;
+}
+
 // Contiguous element range [e0, e1) of a slab, widened to 16-byte alignment.
 struct Span {
     long long g0;      // first copied element (even)

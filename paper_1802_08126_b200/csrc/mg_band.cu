@@ -34,7 +34,6 @@ namespace pint {
 
 constexpr int BT = 256;       // threads of the band kernels
 constexpr int TT = 512;       // threads of the tail kernel
-constexpr int NSTAGE = 2;
 
 // stencil shapes: which of the 9 CSR positions can be non-zero
 enum Shape : int { SH_FULL = 0, SH_SEVEN = 1, SH_FIVE = 2 };
@@ -143,8 +142,14 @@ __device__ __forceinline__ double row_sum_pad(const double* c, const double* rm,
 // ============================================================================
 // pre-smoothing + residual + restriction, level (m -> mc)
 // ============================================================================
+// Warp-specialised: the last warp of the CTA is the TMA producer (full/empty
+// mbarrier ring of P.stages stages), the first BT threads compute.  A producer
+// that also computed would serialise the copies with the compute phases
+// (tools/tma_stream_micro.cu measured 2x lower streaming rates).
+constexpr int MAXSTAGE = 4;
+
 struct PreParams {
-    int m, mc, B, Hc, nbands;
+    int m, mc, B, Hc, nbands, stages;
     int words_b, words_x, words_r;  // smem words: stage b, padded x0 tile, residual
     const double* b;
     double* bc;
@@ -153,49 +158,55 @@ struct PreParams {
 };
 
 template <int SH>
-__global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
+__global__ void __launch_bounds__(BT + 32) k_band_pre(PreParams P) {
     extern __shared__ __align__(16) double smem[];
-    __shared__ __align__(8) uint64_t bars[NSTAGE];
-    const int m = P.m, mc = P.mc, mp = m + 2;
+    __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
+    const int m = P.m, mc = P.mc, mp = m + 2, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
-    double* stage[NSTAGE];
-    for (int s = 0; s < NSTAGE; ++s) stage[s] = smem + s * P.words_b;
-    double* sx = smem + NSTAGE * P.words_b;  // (2Hc+3) x (m+2), zero-padded
-    double* sr = sx + P.words_x;             // (2Hc+1) x m
+    double* sx = smem + S * P.words_b;  // (2Hc+3) x (m+2), zero-padded
+    double* sr = sx + P.words_x;        // (2Hc+1) x m
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
-    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
-    const int tx = tid % TX, ty = tid / TX;
-    const int TXC = min(BT, ((mc + 31) / 32) * 32), TYC = BT / TXC;
-    const int txc = tid % TXC, tyc = tid / TXC;
-    for (int i = tid; i < P.words_x; i += BT) sx[i] = 0.0;
-    if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
     auto unit_rows = [&](int u, int& plane, int& Y0, int& Y1) {
         plane = u / P.nbands;
         const int j = u - plane * P.nbands;
         Y0 = j * P.Hc;
         Y1 = min(mc, Y0 + P.Hc);
     };
-    auto issue = [&](int u, int s) {
-        int plane, Y0, Y1;
-        unit_rows(u, plane, Y0, Y1);
-        const long long pb = plane * n;
-        const int first = 2 * Y0 - 1;
-        const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
-        fence_proxy_async();
-        mbar_expect_tx(&bars[s], band_bytes(pb, m, lo, hi));
-        band_issue(stage[s], P.b, pb, m, first, lo, hi, &bars[s]);
-    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    for (int i = tid; i < P.words_x; i += BT + 32) sx[i] = 0.0;
+    __syncthreads();
+    if (tid >= BT) {  // ---- producer warp ----
+        if (tid == BT) {
+            int k = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+                const int s = k % S;
+                if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                int plane, Y0, Y1;
+                unit_rows(u, plane, Y0, Y1);
+                const long long pb = plane * n;
+                const int first = 2 * Y0 - 1;
+                const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
+                mbar_expect_tx(&full[s], band_bytes(pb, m, lo, hi));
+                band_issue(smem + s * P.words_b, P.b, pb, m, first, lo, hi, &full[s]);
+            }
+        }
+        return;
+    }
+    // ---- consumers ----
+    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
+    const int tx = tid % TX, ty = tid / TX;
+    const int TXC = min(BT, ((mc + 31) / 32) * 32), TYC = BT / TXC;
+    const int txc = tid % TXC, tyc = tid / TXC;
     int k = 0;
-    const int u0 = blockIdx.x;
-    if (tid == 0 && u0 < units) issue(u0, 0);
-    for (int u = u0; u < units; u += gridDim.x, ++k) {
-        const int s = k % NSTAGE;
-        if (tid == 0 && u + (int)gridDim.x < units) issue(u + gridDim.x, (k + 1) % NSTAGE);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % S;
         int plane, Y0, Y1;
         unit_rows(u, plane, Y0, Y1);
         const long long pb = plane * n;
@@ -206,8 +217,8 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
         const double d = __ldg(tb + 9);
         const int first = 2 * Y0 - 1;
         const int lo = max(0, first);
-        mbar_wait(&bars[s], (k / NSTAGE) & 1);
-        const BandView vb = band_view(stage[s], pb, m, first, lo);
+        mbar_wait(&full[s], (k / S) & 1);
+        const BandView vb = band_view(smem + s * P.words_b, pb, m, first, lo);
         const int nrow_b = 2 * (Y1 - Y0) + 3;
         // x0 = dinv * b into the padded tile (rows outside the plane = 0)
         for (int r = ty; r < nrow_b; r += TY) {
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
             double* xr = sx + r * mp + 1;
             for (int x = tx; x < m; x += TX) xr[x] = in ? d * br[x] : 0.0;
         }
-        __syncthreads();
+        consumer_sync<BT>();
         // residual r = b - A x0 on fine rows 2*Y0 .. 2*Y1
         const int nrow_r = 2 * (Y1 - Y0) + 1;
         for (int r = ty; r < nrow_r; r += TY) {
@@ -227,7 +238,8 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
             for (int x = tx; x < m; x += TX)
                 rr[x] = br[x] - row_sum_pad<SH>(ca, xm, xm + mp, xm + 2 * mp, x + 1);
         }
-        __syncthreads();
+        consumer_sync<BT>();
+        if (tid == 0) mbar_arrive(&empty[s]);  // stage s fully consumed
         // restriction: P^T r, ascending fine index (csc_matvec order)
         const int ncr = Y1 - Y0;
         for (int r = tyc; r < ncr; r += TYC) {
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
                 out[X] = v;
             }
         }
-        __syncthreads();
+        consumer_sync<BT>();
     }
 }
 
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(BT) k_band_pre(PreParams P) {
 // prolongation + post-smoothing (+ finest-level epilogue), level (mc -> m)
 // ============================================================================
 struct PostBandParams {
-    int m, mc, B, H, nbands;
+    int m, mc, B, H, nbands, stages;
     int words_b, words_e, words_q, words_x;  // stage: b, e, pin|aux ; work: padded x
     const double* b;
     const double* ec;
@@ -273,31 +285,20 @@ struct PostBandParams {
 };
 
 template <int SH, int EPI>
-__global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
+__global__ void __launch_bounds__(BT + 32) k_band_post(PostBandParams P) {
     extern __shared__ __align__(16) double smem[];
-    __shared__ __align__(8) uint64_t bars[NSTAGE];
-    const int m = P.m, mc = P.mc, mp = m + 2;
+    __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
+    __shared__ double red[BT / 32];
+    const int m = P.m, mc = P.mc, mp = m + 2, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
     const int wstage = P.words_b + P.words_e + P.words_q;
-    double* sx = smem + NSTAGE * wstage;  // (H+2) x (m+2) zero-padded
+    double* sx = smem + S * wstage;  // (H+2) x (m+2) zero-padded
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
-    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
-    const int tx = tid % TX, ty = tid / TX;
-    // prolongation: thread owns coarse column pair (t-1, t) -> fine columns 2t, 2t+1
-    const int TXP = min(BT, ((mc + 1 + 31) / 32) * 32), TYP = BT / TXP;
-    const int txp = tid % TXP, typ = tid / TXP;
     constexpr bool HAS_Q = EPI == EPI_UZAWA_P || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
     constexpr bool HAS_DOT =
         EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
     constexpr bool HAS_TAU = EPI == EPI_DIV_TAU || EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU;
-    const double* qsrc = EPI == EPI_UZAWA_P ? P.pin : P.aux;
-    for (int i = tid; i < P.words_x; i += BT) sx[i] = 0.0;
-    if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
     auto sb = [&](int s) { return smem + s * wstage; };
     auto se = [&](int s) { return smem + s * wstage + P.words_b; };
     auto sq = [&](int s) { return smem + s * wstage + P.words_b + P.words_e; };
@@ -307,27 +308,47 @@ __global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
         y0 = j * P.H;
         y1 = min(m, y0 + P.H);
     };
-    auto issue = [&](int u, int s) {
-        int plane, y0, y1;
-        unit_rows(u, plane, y0, y1);
-        const long long pb = plane * n, pc = plane * nc;
-        const int fb = y0 - 1, lob = max(0, fb), hib = min(m, y1 + 1);
-        const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
-        uint32_t tx_bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
-        if (HAS_Q) tx_bytes += band_bytes(pb, m, y0, y1);
-        fence_proxy_async();
-        mbar_expect_tx(&bars[s], tx_bytes);
-        band_issue(sb(s), P.b, pb, m, fb, lob, hib, &bars[s]);
-        band_issue(se(s), P.ec, pc, mc, fe, loe, hie, &bars[s]);
-        if (HAS_Q) band_issue(sq(s), qsrc, pb, m, y0, y0, y1, &bars[s]);
-    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    for (int i = tid; i < P.words_x; i += BT + 32) sx[i] = 0.0;
+    __syncthreads();
+    if (tid >= BT) {  // ---- producer warp ----
+        if (tid == BT) {
+            const double* qsrc = EPI == EPI_UZAWA_P ? P.pin : P.aux;
+            int k = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+                const int s = k % S;
+                if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                int plane, y0, y1;
+                unit_rows(u, plane, y0, y1);
+                const long long pb = plane * n, pc = plane * nc;
+                const int fb = y0 - 1, lob = max(0, fb), hib = min(m, y1 + 1);
+                const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
+                uint32_t bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
+                if (HAS_Q) bytes += band_bytes(pb, m, y0, y1);
+                mbar_expect_tx(&full[s], bytes);
+                band_issue(sb(s), P.b, pb, m, fb, lob, hib, &full[s]);
+                band_issue(se(s), P.ec, pc, mc, fe, loe, hie, &full[s]);
+                if (HAS_Q) band_issue(sq(s), qsrc, pb, m, y0, y0, y1, &full[s]);
+            }
+        }
+        return;
+    }
+    // ---- consumers ----
+    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
+    const int tx = tid % TX, ty = tid / TX;
+    // prolongation: thread owns coarse column pair (t-1, t) -> fine columns 2t, 2t+1
+    const int TXP = min(BT, ((mc + 1 + 31) / 32) * 32), TYP = BT / TXP;
+    const int txp = tid % TXP, typ = tid / TXP;
     double acc = 0.0;
     int k = 0;
-    const int u0 = blockIdx.x;
-    if (tid == 0 && u0 < units) issue(u0, 0);
-    for (int u = u0; u < units; u += gridDim.x, ++k) {
-        const int s = k % NSTAGE;
-        if (tid == 0 && u + (int)gridDim.x < units) issue(u + gridDim.x, (k + 1) % NSTAGE);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % S;
         int plane, y0, y1;
         unit_rows(u, plane, y0, y1);
         const long long pb = plane * n, pc = plane * nc;
@@ -338,7 +359,7 @@ __global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
         const double d = __ldg(tb + 9);
         const int fb = y0 - 1, lob = max(0, fb);
         const int fe = y0 / 2 - 1, loe = max(0, fe);
-        mbar_wait(&bars[s], (k / NSTAGE) & 1);
+        mbar_wait(&full[s], (k / S) & 1);
         const BandView vb = band_view(sb(s), pb, m, fb, lob);
         const BandView ve = band_view(se(s), pc, mc, fe, loe);
         // x = dinv*b + P e on rows y0-1 .. y1 (tile rows 0 .. y1-y0+1)
@@ -392,7 +413,7 @@ __global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
                 }
             }
         }
-        __syncthreads();
+        consumer_sync<BT>();
         // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
         const BandView vq = band_view(sq(s), pb, m, y0, y0);
         const double tau = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
@@ -428,10 +449,11 @@ __global__ void __launch_bounds__(BT) k_band_post(PostBandParams P) {
                 }
             }
         }
-        __syncthreads();
+        consumer_sync<BT>();
+        if (tid == 0) mbar_arrive(&empty[s]);
     }
     if (HAS_DOT) {
-        const double s = block_sum<BT>(acc);
+        const double s = consumer_sum<BT>(acc, red);
         if (tid == 0) P.part[blockIdx.x] = s;
     }
 }
@@ -651,7 +673,7 @@ static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    k_band_pre<SH><<<grid, BT, smem, c->stream>>>(P);
+    k_band_pre<SH><<<grid, BT + 32, smem, c->stream>>>(P);
 }
 
 template <int SH, int EPI>
@@ -662,7 +684,7 @@ static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, i
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    k_band_post<SH, EPI><<<grid, BT, smem, c->stream>>>(P);
+    k_band_post<SH, EPI><<<grid, BT + 32, smem, c->stream>>>(P);
 }
 
 template <int SH>
@@ -677,6 +699,14 @@ static void launch_post_sh(pint_ctx* c, const PostBandParams& P, size_t smem, in
         case EPI_SCALE_DOTONLY: launch_post_epi<SH, EPI_SCALE_DOTONLY>(c, P, smem, grid); break;
         default: pint_throw(PINT_INPUT, "unknown epilogue");
     }
+}
+
+// stages of the TMA ring: 3 when two CTAs per SM still fit, else 2
+static int pick_stages(int words_stage, int words_work) {
+    const size_t budget = 110 * 1024;
+    for (int st = 3; st >= 2; --st)
+        if (sizeof(double) * ((size_t)st * words_stage + words_work) <= budget) return st;
+    return 2;
 }
 
 static int blocks_per_sm(size_t smem) {
@@ -709,11 +739,12 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_b = band_words(2 * P.Hc + 3, P.m);
         P.words_x = (2 * P.Hc + 3) * (P.m + 2);
         P.words_r = (2 * P.Hc + 1) * P.m;
+        P.stages = pick_stages(P.words_b, P.words_x + P.words_r);
         P.b = bl;
         P.bc = c->lev_b[l + 1];
         P.tab = lvl_tab(l);
         P.sid = s.sid;
-        const size_t smem = sizeof(double) * (NSTAGE * P.words_b + P.words_x + P.words_r);
+        const size_t smem = sizeof(double) * (P.stages * P.words_b + P.words_x + P.words_r);
         const int units = P.B * P.nbands;
         const int grid = std::min(units, sms * blocks_per_sm(smem));
         ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
@@ -793,6 +824,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_e = band_words(P.H / 2 + 2, P.mc);
         P.words_q = has_q ? band_words(P.H, P.m) : 0;
         P.words_x = (P.H + 2) * (P.m + 2);
+        P.stages = pick_stages(P.words_b + P.words_e + P.words_q, P.words_x);
         P.b = top ? b : c->lev_b[l];
         P.ec = c->lev_x[l + 1];
         P.tab = lvl_tab(l);
@@ -803,7 +835,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.pin = pin;
         P.aux = aux;
         const size_t smem =
-            sizeof(double) * (NSTAGE * (P.words_b + P.words_e + P.words_q) + P.words_x);
+            sizeof(double) * (P.stages * (P.words_b + P.words_e + P.words_q) + P.words_x);
         const int units = P.B * P.nbands;
         const int grid = std::min(units, sms * blocks_per_sm(smem));
         const bool dl = top && dot;
