@@ -389,6 +389,9 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
         c->tau_ref = tau_ref;
         c->n_a = n_a;
         c->h_steps.assign(steps, steps + N);
+        c->h_mass.assign(mass, mass + PINT_S2);
+        c->h_ast.assign(a_st, a_st + (size_t)n_a * PINT_S2);
+        c->h_aref.assign(aref, aref + PINT_S2);
         c->d_steps = upload(c, steps, N);
         c->d_mass = upload(c, mass, PINT_S2);
         c->d_ast = upload(c, a_st, (size_t)n_a * PINT_S2);

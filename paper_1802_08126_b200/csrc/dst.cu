@@ -104,16 +104,19 @@ struct DstArgs {
 
 // KIND 0: out = S^T in (dst.py:67-73);  KIND 1: out = S in (dst.py:86-93)
 template <int KIND>
-__global__ void __launch_bounds__(DST_THREADS) k_dst_fft(DstArgs a) {
+__global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
     extern __shared__ double2 buf[];
     const int N = a.N, n = a.n, P = a.P, W = 2 * P;
     const int c0 = blockIdx.x * W;
     const int ncol = min(W, n - c0);
     const int tid = threadIdx.x;
     // ---- load (+ pre-processing) ----
-    for (int idx = tid; idx < N * W; idx += DST_THREADS) {
+    // batches of LB independent loads per thread keep LB requests in flight
+    // (a load-store-load loop would expose the full HBM latency per element)
+    constexpr int LB = 16;
+    const int total = N * W;
+    auto place = [&](int idx, double v) {
         const int j = idx / W, cc = idx - j * W;
-        double v = (cc < ncol) ? __ldg(a.in + (size_t)j * n + c0 + cc) : 0.0;
         if (j == N - 1) v *= a.in_last;
         int pos;
         if (KIND == 0) {
@@ -128,6 +131,20 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst_fft(DstArgs a) {
         }
         double* dst = reinterpret_cast<double*>(buf + (size_t)(cc >> 1) * N + pos) + (cc & 1);
         *dst = v;
+    };
+    for (int base = tid; base < total; base += DST_THREADS * LB) {
+        double v[LB];
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+            const int idx = base + i * DST_THREADS;
+            const int j = idx / W, cc = idx - j * W;
+            v[i] = (idx < total && cc < ncol) ? __ldg(a.in + (size_t)j * n + c0 + cc) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+            const int idx = base + i * DST_THREADS;
+            if (idx < total) place(idx, v[i]);
+        }
     }
     __syncthreads();
     if (KIND == 1) {
@@ -150,9 +167,8 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst_fft(DstArgs a) {
     }
     fft_dif(buf, N, P, a.r2first, a.tw);
     // ---- post-processing + store ----
-    for (int idx = tid; idx < N * W; idx += DST_THREADS) {
+    auto value = [&](int idx) -> double {
         const int j = idx / W, cc = idx - j * W;
-        if (cc >= ncol) continue;
         const double2* col = buf + (size_t)(cc >> 1) * N;
         double v;
         if (KIND == 0) {
@@ -172,8 +188,26 @@ __global__ void __launch_bounds__(DST_THREADS) k_dst_fft(DstArgs a) {
         }
         v = a.alpha * v;
         if (j == N - 1) v *= a.out_last;
-        const size_t gi = (size_t)j * n + c0 + cc;
-        a.out[gi] = a.base ? __ldg(a.base + gi) + v : v;
+        return v;
+    };
+    for (int base = tid; base < total; base += DST_THREADS * LB) {
+        double bv[LB];
+        if (a.base) {
+#pragma unroll
+            for (int i = 0; i < LB; ++i) {
+                const int idx = base + i * DST_THREADS;
+                const int j = idx / W, cc = idx - j * W;
+                bv[i] = (idx < total && cc < ncol) ? __ldg(a.base + (size_t)j * n + c0 + cc) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+            const int idx = base + i * DST_THREADS;
+            const int j = idx / W, cc = idx - j * W;
+            if (idx >= total || cc >= ncol) continue;
+            const double v = value(idx);
+            a.out[(size_t)j * n + c0 + cc] = a.base ? bv[i] + v : v;
+        }
     }
 }
 

@@ -25,6 +25,7 @@
 // four diagonal entries of the stiffness) are skipped, which adds +-0 and so
 // cannot change a non-zero sum.
 #include <algorithm>
+#include <cstdlib>
 
 #include "band.cuh"
 #include "pint_device.cuh"
@@ -143,35 +144,63 @@ __device__ __forceinline__ double row_sum_pad(const double* c, const double* rm,
 // pre-smoothing + residual + restriction, level (m -> mc)
 // ============================================================================
 // Warp-specialised: the last warp of the CTA is the TMA producer (full/empty
-// mbarrier ring of P.stages stages), the first BT threads compute.  A producer
-// that also computed would serialise the copies with the compute phases
-// (tools/tma_stream_micro.cu measured 2x lower streaming rates).
+// mbarrier ring of P.stages stages), the first NT threads compute.  Each
+// consumer thread owns CPT fine columns and marches down the band's rows with
+// a 3x3 register window, so a stencil costs 3 shared loads per point and the
+// loop structure is fully unrolled (HC compile-time).
 constexpr int MAXSTAGE = 4;
 
 struct PreParams {
     int m, mc, B, Hc, nbands, stages;
-    int words_b, words_x, words_r;  // smem words: stage b, padded x0 tile, residual
+    int words_b, words_r;  // smem words: stage b, residual rows
     const double* b;
     double* bc;
     const double* tab;  // level table [n_sets][10]
     const int* sid;
 };
 
+// CSR-ordered 9-point row sum from a register window (rows a = y-1, b = y, c = y+1;
+// columns 0 = x-1, 1 = x, 2 = x+1)
 template <int SH>
-__global__ void __launch_bounds__(BT + 32) k_band_pre(PreParams P) {
+__device__ __forceinline__ double win_sum(const double* ca, double a0, double a1, double a2,
+                                          double b0, double b1, double b2, double c0, double c1,
+                                          double c2) {
+    double s = 0.0;
+    bool first = true;
+#define PINT_W(K, V)                  \
+    if (used<SH>(K)) {                \
+        const double t_ = ca[K] * (V); \
+        s = first ? t_ : s + t_;      \
+        first = false;                \
+    }
+    PINT_W(0, a0)
+    PINT_W(1, a1)
+    PINT_W(2, a2)
+    PINT_W(3, b0)
+    PINT_W(4, b1)
+    PINT_W(5, b2)
+    PINT_W(6, c0)
+    PINT_W(7, c1)
+    PINT_W(8, c2)
+#undef PINT_W
+    return s;
+}
+
+template <int SH, int NT, int CPT, int HC>
+__global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
-    const int m = P.m, mc = P.mc, mp = m + 2, S = P.stages;
+    constexpr int RR = 2 * HC + 1;  // residual rows per unit
+    const int m = P.m, mc = P.mc, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
-    double* sx = smem + S * P.words_b;  // (2Hc+3) x (m+2), zero-padded
-    double* sr = sx + P.words_x;        // (2Hc+1) x m
+    double* sr = smem + S * P.words_b;  // RR x m
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
     auto unit_rows = [&](int u, int& plane, int& Y0, int& Y1) {
         plane = u / P.nbands;
         const int j = u - plane * P.nbands;
-        Y0 = j * P.Hc;
-        Y1 = min(mc, Y0 + P.Hc);
+        Y0 = j * HC;
+        Y1 = min(mc, Y0 + HC);
     };
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -180,10 +209,9 @@ __global__ void __launch_bounds__(BT + 32) k_band_pre(PreParams P) {
         }
         fence_barrier_init();
     }
-    for (int i = tid; i < P.words_x; i += BT + 32) sx[i] = 0.0;
     __syncthreads();
-    if (tid >= BT) {  // ---- producer warp ----
-        if (tid == BT) {
+    if (tid >= NT) {  // ---- producer warp ----
+        if (tid == NT) {
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
@@ -199,11 +227,6 @@ __global__ void __launch_bounds__(BT + 32) k_band_pre(PreParams P) {
         }
         return;
     }
-    // ---- consumers ----
-    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
-    const int tx = tid % TX, ty = tid / TX;
-    const int TXC = min(BT, ((mc + 31) / 32) * 32), TYC = BT / TXC;
-    const int txc = tid % TXC, tyc = tid / TXC;
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
         const int s = k % S;
@@ -217,51 +240,73 @@ __global__ void __launch_bounds__(BT + 32) k_band_pre(PreParams P) {
         const double d = __ldg(tb + 9);
         const int first = 2 * Y0 - 1;
         const int lo = max(0, first);
+        const int nr = 2 * (Y1 - Y0) + 1;
         mbar_wait(&full[s], (k / S) & 1);
         const BandView vb = band_view(smem + s * P.words_b, pb, m, first, lo);
-        const int nrow_b = 2 * (Y1 - Y0) + 3;
-        // x0 = dinv * b into the padded tile (rows outside the plane = 0)
-        for (int r = ty; r < nrow_b; r += TY) {
-            const int gy = first + r;
-            const bool in = gy >= 0 && gy < m;
-            const double* br = vb.row(r, m);
-            double* xr = sx + r * mp + 1;
-            for (int x = tx; x < m; x += TX) xr[x] = in ? d * br[x] : 0.0;
+        // residual r = b - A(dinv*b) on fine rows 2*Y0 .. 2*Y1 (slots 1 .. nr)
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int x = tid + j * NT;
+            if (x >= m) continue;
+            const bool w = x > 0, e = x < m - 1;
+            double a0, a1, a2, b0, b1, b2, bb, braw_b;
+            auto ld = [&](int slot, double& l, double& c, double& r, double& raw) {
+                const int gy = first + slot;
+                const bool in = gy >= 0 && gy < m;
+                const double* row = vb.row(slot, m);
+                raw = in ? row[x] : 0.0;
+                l = (in && w) ? d * row[x - 1] : 0.0;
+                c = d * raw;
+                r = (in && e) ? d * row[x + 1] : 0.0;
+            };
+            ld(0, a0, a1, a2, bb);
+            ld(1, b0, b1, b2, braw_b);
+#pragma unroll
+            for (int rho = 0; rho < RR; ++rho) {
+                if (rho < nr) {
+                    double c0, c1, c2, braw_c;
+                    ld(rho + 2, c0, c1, c2, braw_c);
+                    sr[rho * m + x] =
+                        braw_b - win_sum<SH>(ca, a0, a1, a2, b0, b1, b2, c0, c1, c2);
+                    a0 = b0; a1 = b1; a2 = b2;
+                    b0 = c0; b1 = c1; b2 = c2;
+                    braw_b = braw_c;
+                }
+            }
         }
-        consumer_sync<BT>();
-        // residual r = b - A x0 on fine rows 2*Y0 .. 2*Y1
-        const int nrow_r = 2 * (Y1 - Y0) + 1;
-        for (int r = ty; r < nrow_r; r += TY) {
-            const double* xm = sx + r * mp;
-            const double* br = vb.row(r + 1, m);
-            double* rr = sr + r * m;
-            for (int x = tx; x < m; x += TX)
-                rr[x] = br[x] - row_sum_pad<SH>(ca, xm, xm + mp, xm + 2 * mp, x + 1);
-        }
-        consumer_sync<BT>();
+        consumer_sync<NT>();
         if (tid == 0) mbar_arrive(&empty[s]);  // stage s fully consumed
         // restriction: P^T r, ascending fine index (csc_matvec order)
         const int ncr = Y1 - Y0;
-        for (int r = tyc; r < ncr; r += TYC) {
-            const double* r0 = sr + (2 * r) * m;
-            const double* r1 = r0 + m;
-            const double* r2 = r1 + m;
-            double* out = P.bc + plane * nc + (long long)(Y0 + r) * mc;
-            for (int X = txc; X < mc; X += TXC) {
-                const int f = 2 * X;
-                double v = 0.25 * r0[f];
-                v = v + 0.5 * r0[f + 1];
-                v = v + 0.25 * r0[f + 2];
-                v = v + 0.5 * r1[f];
-                v = v + 1.0 * r1[f + 1];
-                v = v + 0.5 * r1[f + 2];
-                v = v + 0.25 * r2[f];
-                v = v + 0.5 * r2[f + 1];
-                v = v + 0.25 * r2[f + 2];
-                out[X] = v;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int X = tid + j * NT;
+            if (X >= mc) continue;
+            const int f = 2 * X;
+            double p0 = sr[f], p1 = sr[f + 1], p2 = sr[f + 2];
+            double* out = P.bc + plane * nc + (long long)Y0 * mc + X;
+#pragma unroll
+            for (int r = 0; r < HC; ++r) {
+                if (r < ncr) {
+                    const double* r1 = sr + (2 * r + 1) * m + f;
+                    const double* r2 = r1 + m;
+                    const double q0 = r1[0], q1 = r1[1], q2 = r1[2];
+                    const double t0 = r2[0], t1 = r2[1], t2 = r2[2];
+                    double v = 0.25 * p0;
+                    v = v + 0.5 * p1;
+                    v = v + 0.25 * p2;
+                    v = v + 0.5 * q0;
+                    v = v + 1.0 * q1;
+                    v = v + 0.5 * q2;
+                    v = v + 0.25 * t0;
+                    v = v + 0.5 * t1;
+                    v = v + 0.25 * t2;
+                    out[(long long)r * mc] = v;
+                    p0 = t0; p1 = t1; p2 = t2;
+                }
             }
         }
-        consumer_sync<BT>();
+        consumer_sync<NT>();
     }
 }
 
@@ -284,11 +329,11 @@ struct PostBandParams {
     double* part;
 };
 
-template <int SH, int EPI>
-__global__ void __launch_bounds__(BT + 32) k_band_post(PostBandParams P) {
+template <int SH, int EPI, int NT, int CPT, int H>
+__global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
-    __shared__ double red[BT / 32];
+    __shared__ double red[NT / 32];
     const int m = P.m, mc = P.mc, mp = m + 2, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
     const int wstage = P.words_b + P.words_e + P.words_q;
@@ -305,8 +350,8 @@ __global__ void __launch_bounds__(BT + 32) k_band_post(PostBandParams P) {
     auto unit_rows = [&](int u, int& plane, int& y0, int& y1) {
         plane = u / P.nbands;
         const int j = u - plane * P.nbands;
-        y0 = j * P.H;
-        y1 = min(m, y0 + P.H);
+        y0 = j * H;
+        y1 = min(m, y0 + H);
     };
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -315,10 +360,10 @@ __global__ void __launch_bounds__(BT + 32) k_band_post(PostBandParams P) {
         }
         fence_barrier_init();
     }
-    for (int i = tid; i < P.words_x; i += BT + 32) sx[i] = 0.0;
+    for (int i = tid; i < P.words_x; i += NT + 32) sx[i] = 0.0;
     __syncthreads();
-    if (tid >= BT) {  // ---- producer warp ----
-        if (tid == BT) {
+    if (tid >= NT) {  // ---- producer warp ----
+        if (tid == NT) {
             const double* qsrc = EPI == EPI_UZAWA_P ? P.pin : P.aux;
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
@@ -339,12 +384,6 @@ __global__ void __launch_bounds__(BT + 32) k_band_post(PostBandParams P) {
         }
         return;
     }
-    // ---- consumers ----
-    const int TX = min(BT, ((m + 31) / 32) * 32), TY = BT / TX;
-    const int tx = tid % TX, ty = tid / TX;
-    // prolongation: thread owns coarse column pair (t-1, t) -> fine columns 2t, 2t+1
-    const int TXP = min(BT, ((mc + 1 + 31) / 32) * 32), TYP = BT / TXP;
-    const int txp = tid % TXP, typ = tid / TXP;
     double acc = 0.0;
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
@@ -359,102 +398,111 @@ __global__ void __launch_bounds__(BT + 32) k_band_post(PostBandParams P) {
         const double d = __ldg(tb + 9);
         const int fb = y0 - 1, lob = max(0, fb);
         const int fe = y0 / 2 - 1, loe = max(0, fe);
+        const int nrow = y1 - y0;
         mbar_wait(&full[s], (k / S) & 1);
         const BandView vb = band_view(sb(s), pb, m, fb, lob);
         const BandView ve = band_view(se(s), pc, mc, fe, loe);
-        // x = dinv*b + P e on rows y0-1 .. y1 (tile rows 0 .. y1-y0+1)
-        const int nrx = y1 - y0 + 2;
-        for (int r = typ; r < nrx; r += TYP) {
-            const int gy = fb + r;
-            double* xr = sx + r * mp + 1;
-            if (gy < 0 || gy >= m) {
-                for (int t = txp; t <= mc; t += TXP) {
-                    xr[2 * t] = 0.0;
-                    if (t < mc) xr[2 * t + 1] = 0.0;
-                }
-                continue;
-            }
-            const double* br = vb.row(r, m);
-            if (gy & 1) {  // one coarse row J, weight 1
-                const double* ea = ve.row(((gy - 1) >> 1) - fe, mc);
-                for (int t = txp; t <= mc; t += TXP) {
-                    const bool l = t >= 1, rr = t < mc;
-                    const double e0 = l ? ea[t - 1] : 0.0, e1 = rr ? ea[t] : 0.0;
-                    // even column 2t: (J, t-1) w .5, (J, t) w .5
+        // x = dinv*b + P e on rows y0-1 .. y1 (tile rows 0 .. nrow+1)
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int x = tid + j * NT;
+            if (x >= m) continue;
+            const bool xodd = x & 1;
+            const int c0 = xodd ? (x - 1) >> 1 : (x >> 1) - 1;  // odd: the one coarse column
+            const int c1 = x >> 1;
+            const bool h0 = xodd || x >= 2, h1 = !xodd && c1 < mc;
+#pragma unroll
+            for (int r = 0; r < H + 2; ++r) {
+                if (r > nrow + 1) continue;
+                const int gy = fb + r;
+                double xv = 0.0;
+                if (gy >= 0 && gy < m) {
+                    const double bv = vb.row(r, m)[x];
                     double pe;
-                    if (l && rr) pe = (1.0 * 0.5) * e0 + (1.0 * 0.5) * e1;
-                    else pe = l ? (1.0 * 0.5) * e0 : (1.0 * 0.5) * e1;
-                    xr[2 * t] = d * br[2 * t] + pe;
-                    if (rr) xr[2 * t + 1] = d * br[2 * t + 1] + (1.0 * 1.0) * e1;
-                }
-            } else {  // coarse rows ja = gy/2-1, jb = gy/2, weights .5
-                const int ja = (gy >> 1) - 1, jb = gy >> 1;
-                const bool va = ja >= 0, vbb = jb < mc;
-                const double* ea = ve.row(va ? ja - fe : 0, mc);
-                const double* eb = ve.row(vbb ? jb - fe : 0, mc);
-                for (int t = txp; t <= mc; t += TXP) {
-                    const bool l = t >= 1, rr = t < mc;
-                    const double a0 = (va && l) ? ea[t - 1] : 0.0;
-                    const double a1 = (va && rr) ? ea[t] : 0.0;
-                    const double b0 = (vbb && l) ? eb[t - 1] : 0.0;
-                    const double b1 = (vbb && rr) ? eb[t] : 0.0;
-                    // even column 2t: (ja,t-1),(ja,t),(jb,t-1),(jb,t), w .25 each;
-                    // absent terms contribute +0 (exact)
-                    double pe = (0.5 * 0.5) * a0;
-                    pe = pe + (0.5 * 0.5) * a1;
-                    pe = pe + (0.5 * 0.5) * b0;
-                    pe = pe + (0.5 * 0.5) * b1;
-                    xr[2 * t] = d * br[2 * t] + pe;
-                    if (rr) {  // odd column 2t+1: (ja,t),(jb,t), w .5
-                        double po = (0.5 * 1.0) * a1;
-                        po = po + (0.5 * 1.0) * b1;
-                        xr[2 * t + 1] = d * br[2 * t + 1] + po;
+                    if (gy & 1) {
+                        const double* ea = ve.row(((gy - 1) >> 1) - fe, mc);
+                        if (xodd) {
+                            pe = (1.0 * 1.0) * ea[c0];
+                        } else {
+                            if (h0 && h1) pe = (1.0 * 0.5) * ea[c0] + (1.0 * 0.5) * ea[c1];
+                            else pe = h0 ? (1.0 * 0.5) * ea[c0] : (1.0 * 0.5) * ea[c1];
+                        }
+                    } else {
+                        const int ja = (gy >> 1) - 1, jb = gy >> 1;
+                        const bool va = ja >= 0, vbb = jb < mc;
+                        const double* ea = ve.row(va ? ja - fe : 0, mc);
+                        const double* eb = ve.row(vbb ? jb - fe : 0, mc);
+                        if (xodd) {
+                            const double a = va ? ea[c0] : 0.0, bq = vbb ? eb[c0] : 0.0;
+                            pe = (0.5 * 1.0) * a;
+                            pe = pe + (0.5 * 1.0) * bq;
+                        } else {
+                            const double a0 = (va && h0) ? ea[c0] : 0.0;
+                            const double a1 = (va && h1) ? ea[c1] : 0.0;
+                            const double b0 = (vbb && h0) ? eb[c0] : 0.0;
+                            const double b1 = (vbb && h1) ? eb[c1] : 0.0;
+                            pe = (0.5 * 0.5) * a0;
+                            pe = pe + (0.5 * 0.5) * a1;
+                            pe = pe + (0.5 * 0.5) * b0;
+                            pe = pe + (0.5 * 0.5) * b1;
+                        }
                     }
+                    xv = d * bv + pe;
                 }
+                sx[r * mp + x + 1] = xv;
             }
         }
-        consumer_sync<BT>();
+        consumer_sync<NT>();
         // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
         const BandView vq = band_view(sq(s), pb, m, y0, y0);
         const double tau = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
-        for (int r = ty; r < y1 - y0; r += TY) {
-            const int gy = y0 + r;
-            const double* xm = sx + r * mp;
-            const double* x0 = xm + mp;
-            const double* br = vb.row(r + 1, m);
-            const double* qr = vq.row(r, m);
-            double* orow = P.out + pb + (long long)gy * m;
-            for (int x = tx; x < m; x += TX) {
-                const double bv = br[x];
-                const double xn =
-                    x0[x + 1] + d * (bv - row_sum_pad<SH>(ca, xm, x0, x0 + mp, x + 1));
-                if (EPI == EPI_PLAIN) {
-                    orow[x] = xn;
-                } else if (EPI == EPI_DIV_TAU) {
-                    orow[x] = xn / tau;
-                } else if (EPI == EPI_UZAWA_P) {
-                    const double dp = xn / tau;
-                    orow[x] = qr[x] + dp;
-                    acc += bv * dp;
-                } else if (EPI == EPI_DOT_TAU) {
-                    acc += bv * (xn / tau);
-                } else if (EPI == EPI_SCALE) {
-                    orow[x] = P.scale * xn;
-                } else if (EPI == EPI_SCALE_DOT) {
-                    const double w = P.scale * xn;
-                    orow[x] = w;
-                    acc += qr[x] * w;
-                } else if (EPI == EPI_SCALE_DOTONLY) {
-                    acc += qr[x] * (P.scale * xn);
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const int x = tid + j * NT;
+            if (x >= m) continue;
+            const double* col = sx + x;  // padded columns x, x+1, x+2 = fine x-1, x, x+1
+            double a0 = col[0], a1 = col[1], a2 = col[2];
+            double b0 = col[mp], b1 = col[mp + 1], b2 = col[mp + 2];
+            double* orow = P.out + pb + (long long)y0 * m + x;
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+                if (r < nrow) {
+                    const double* cr = col + (r + 2) * mp;
+                    const double c0 = cr[0], c1 = cr[1], c2 = cr[2];
+                    const double bv = vb.row(r + 1, m)[x];
+                    const double xn =
+                        b1 + d * (bv - win_sum<SH>(ca, a0, a1, a2, b0, b1, b2, c0, c1, c2));
+                    double* o = orow + (long long)r * m;
+                    if (EPI == EPI_PLAIN) {
+                        *o = xn;
+                    } else if (EPI == EPI_DIV_TAU) {
+                        *o = xn / tau;
+                    } else if (EPI == EPI_UZAWA_P) {
+                        const double dp = xn / tau;
+                        *o = vq.row(r, m)[x] + dp;
+                        acc += bv * dp;
+                    } else if (EPI == EPI_DOT_TAU) {
+                        acc += bv * (xn / tau);
+                    } else if (EPI == EPI_SCALE) {
+                        *o = P.scale * xn;
+                    } else if (EPI == EPI_SCALE_DOT) {
+                        const double wv = P.scale * xn;
+                        *o = wv;
+                        acc += vq.row(r, m)[x] * wv;
+                    } else if (EPI == EPI_SCALE_DOTONLY) {
+                        acc += vq.row(r, m)[x] * (P.scale * xn);
+                    }
+                    a0 = b0; a1 = b1; a2 = b2;
+                    b0 = c0; b1 = c1; b2 = c2;
                 }
             }
         }
-        consumer_sync<BT>();
+        consumer_sync<NT>();
         if (tid == 0) mbar_arrive(&empty[s]);
     }
     if (HAS_DOT) {
-        const double s = consumer_sum<BT>(acc, red);
-        if (tid == 0) P.part[blockIdx.x] = s;
+        const double sum = consumer_sum<NT>(acc, red);
+        if (tid == 0) P.part[blockIdx.x] = sum;
     }
 }
 
@@ -665,26 +713,48 @@ void mg_compute_shapes(MgSet& set, const double* tab) {
     }
 }
 
-template <int SH>
-static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+template <int SH, int NT, int CPT>
+static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
     static bool attr = false;
+    auto* kern = P.Hc == 2 ? k_band_pre<SH, NT, CPT, 2> : k_band_pre<SH, NT, CPT, 4>;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH, NT, CPT, 2>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH, NT, CPT, 4>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    k_band_pre<SH><<<grid, BT + 32, smem, c->stream>>>(P);
+    kern<<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int SH>
+static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+    if (P.m <= 128) launch_pre_cfg<SH, 128, 1>(c, P, smem, grid);
+    else if (P.m <= 256) launch_pre_cfg<SH, 256, 1>(c, P, smem, grid);
+    else if (P.m <= 512) launch_pre_cfg<SH, 256, 2>(c, P, smem, grid);
+    else pint_throw(PINT_INPUT, "grid wider than 511 points is not supported");
+}
+
+template <int SH, int EPI, int NT, int CPT>
+static void launch_post_cfg(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    static bool attr = false;
+    auto* kern = P.H == 4 ? k_band_post<SH, EPI, NT, CPT, 4> : k_band_post<SH, EPI, NT, CPT, 8>;
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI, NT, CPT, 4>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI, NT, CPT, 8>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    kern<<<grid, NT + 32, smem, c->stream>>>(P);
 }
 
 template <int SH, int EPI>
 static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
-    static bool attr = false;
-    if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
-    k_band_post<SH, EPI><<<grid, BT + 32, smem, c->stream>>>(P);
+    if (P.m <= 128) launch_post_cfg<SH, EPI, 128, 1>(c, P, smem, grid);
+    else if (P.m <= 256) launch_post_cfg<SH, EPI, 256, 1>(c, P, smem, grid);
+    else if (P.m <= 512) launch_post_cfg<SH, EPI, 256, 2>(c, P, smem, grid);
+    else pint_throw(PINT_INPUT, "grid wider than 511 points is not supported");
 }
 
 template <int SH>
@@ -701,12 +771,18 @@ static void launch_post_sh(pint_ctx* c, const PostBandParams& P, size_t smem, in
     }
 }
 
-// stages of the TMA ring: 3 when two CTAs per SM still fit, else 2
+// Stages of the TMA ring.  Measured on B200 (tools/sweep_mg.py): two stages
+// and as many CTAs per SM as fit beat deeper rings, so keep two.
 static int pick_stages(int words_stage, int words_work) {
-    const size_t budget = 110 * 1024;
-    for (int st = 3; st >= 2; --st)
-        if (sizeof(double) * ((size_t)st * words_stage + words_work) <= budget) return st;
+    (void)words_stage;
+    (void)words_work;
     return 2;
+}
+
+// tuning overrides (diagnostic sweeps only): PINT_STAGES, PINT_BAND, PINT_CTAS
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
 }
 
 static int blocks_per_sm(size_t smem) {
@@ -714,6 +790,8 @@ static int blocks_per_sm(size_t smem) {
     int k = (int)(per_sm / (smem + 1024));
     if (k < 1) k = 1;
     if (k > 4) k = 4;
+    const int cap = env_int("PINT_CTAS", 0);
+    if (cap > 0 && cap < k) k = cap;
     return k;
 }
 
@@ -734,17 +812,16 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.m = s.m[l];
         P.mc = s.m[l + 1];
         P.B = count;
-        P.Hc = P.m > 300 ? 2 : 4;
+        P.Hc = env_int("PINT_BAND", 8) / 2 == 2 ? 2 : 4;  // 4 coarse rows = 8 fine rows
         P.nbands = (P.mc + P.Hc - 1) / P.Hc;
         P.words_b = band_words(2 * P.Hc + 3, P.m);
-        P.words_x = (2 * P.Hc + 3) * (P.m + 2);
-        P.words_r = (2 * P.Hc + 1) * P.m;
-        P.stages = pick_stages(P.words_b, P.words_x + P.words_r);
+        P.words_r = ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
+        P.stages = env_int("PINT_STAGES", pick_stages(P.words_b, P.words_r));
         P.b = bl;
         P.bc = c->lev_b[l + 1];
         P.tab = lvl_tab(l);
         P.sid = s.sid;
-        const size_t smem = sizeof(double) * (P.stages * P.words_b + P.words_x + P.words_r);
+        const size_t smem = sizeof(double) * (P.stages * P.words_b + P.words_r);
         const int units = P.B * P.nbands;
         const int grid = std::min(units, sms * blocks_per_sm(smem));
         ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
@@ -814,7 +891,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.m = s.m[l];
         P.mc = s.m[l + 1];
         P.B = count;
-        P.H = P.m > 300 ? 4 : 8;
+        P.H = env_int("PINT_BAND", P.m > 300 ? 4 : 8) == 4 ? 4 : 8;
         P.nbands = (P.m + P.H - 1) / P.H;
         const bool top = l == 0;
         P.epi = top ? epi : EPI_PLAIN;
@@ -824,7 +901,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_e = band_words(P.H / 2 + 2, P.mc);
         P.words_q = has_q ? band_words(P.H, P.m) : 0;
         P.words_x = (P.H + 2) * (P.m + 2);
-        P.stages = pick_stages(P.words_b + P.words_e + P.words_q, P.words_x);
+        P.stages = env_int("PINT_STAGES", pick_stages(P.words_b + P.words_e + P.words_q, P.words_x));
         P.b = top ? b : c->lev_b[l];
         P.ec = c->lev_x[l + 1];
         P.tab = lvl_tab(l);

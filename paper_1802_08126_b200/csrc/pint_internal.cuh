@@ -94,7 +94,7 @@ struct pint_ctx {
     int dims = 0, m = 0, n = 0, N = 0;
     double tau_ref = 0.0;
     int n_a = 0;
-    std::vector<double> h_steps;
+    std::vector<double> h_steps, h_mass, h_ast, h_aref;
     double* d_steps = nullptr;   // [N]
     double* d_mass = nullptr;    // [9]
     double* d_ast = nullptr;     // [n_a][9]
@@ -157,6 +157,12 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
                    double* out);
 void launch_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f);
 void launch_aref(pint_ctx* c, const double* in, double* out, int count);
+// TMA band versions (timeop_band.cu), used for 64 <= m <= 512
+bool band_timeop_supported(const pint_ctx* c);
+void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,
+                        double* out);
+void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host, const double* in,
+                       double* out, int count);
 
 // multigrid (mg.cu)
 // V-cycle over planes [0,count) of set `which`; finest post kernel uses `epi`.

@@ -12,6 +12,8 @@
 // planes, carrying the mass-stencil products M u_{n-1}, M u_n, M u_{n+1}
 // (and M p_n, M p_{n+1}) in registers so every input plane is read from HBM
 // once (the neighbouring-plane halo is a register carry, not a re-read).
+#include <cstdlib>
+
 #include "pint_device.cuh"
 #include "pint_internal.cuh"
 
@@ -156,6 +158,10 @@ static dim3 plane_grid(int m, int planes) {
 
 void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                    double* out) {
+    if ((op == OP_R1 || op == OP_Z) && band_timeop_supported(c) && !getenv("PINT_NO_BAND_TIMEOP")) {
+        launch_band_timeop(c, op, u, p, f, out);
+        return;
+    }
     const dim3 g = plane_grid(c->m, c->N), b(TX, TY);
     static const int kid[] = {K_TIMEOP_K, K_TIMEOP_KT, K_TIMEOP_ABD, K_TIMEOP_R1, K_TIMEOP_Z};
     static const int passes[] = {2, 2, 2, 4, 4};
@@ -181,6 +187,10 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
 }
 
 void launch_aref(pint_ctx* c, const double* in, double* out, int count) {
+    if (band_timeop_supported(c)) {
+        launch_band_apply(c, c->d_aref, c->h_aref.data(), in, out, count);
+        return;
+    }
     ProfScope prof(c, K_AREF, 16.0 * (double)count * c->n);
     k_aref<<<plane_grid(c->m, count), dim3(TX, TY), 0, c->stream>>>(c->m, count, c->d_aref, in,
                                                                      out);
