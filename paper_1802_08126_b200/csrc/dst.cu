@@ -41,30 +41,47 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
     return make_double2(a.x - b.x, a.y - b.y);
 }
 
+// Output position of DFT index k after the DIF stages (radix-2 first when
+// log2 N is odd, then radix-4): base-4 digit reversal = bit reversal with
+// the two bits of every digit swapped back.
+__device__ __forceinline__ int dif_pos(int k, int lgN) {
+    if (lgN == 0) return 0;
+    if (lgN & 1) {
+        const int lg4 = lgN - 1;
+        int t = lg4 ? (int)(__brev((unsigned)(k >> 1)) >> (32 - lg4)) : 0;
+        t = ((t & 0x55555555) << 1) | ((t >> 1) & 0x55555555);
+        return ((k & 1) << (lgN - 1)) | t;
+    }
+    int t = (int)(__brev((unsigned)k) >> (32 - lgN));
+    return ((t & 0x55555555) << 1) | ((t >> 1) & 0x55555555);
+}
+
 // in-place DIF FFT (forward, e^{-2 pi i jk/N}) of P columns of length N in smem
-__device__ void fft_dif(double2* buf, int N, int P, int r2first, const double2* __restrict__ tw) {
+template <int P>
+__device__ __forceinline__ void fft_dif(double2* buf, int lgN, const double2* __restrict__ tw) {
     const int tid = threadIdx.x;
-    int L = N;
-    if (r2first) {
-        const int s = N >> 1;
+    const int N = 1 << lgN;
+    int lgL = lgN;
+    if (lgN & 1) {
+        const int lgs = lgN - 1, s = 1 << lgs;
         for (int item = tid; item < P * s; item += DST_THREADS) {
-            const int pr = item / s, j = item - pr * s;
-            double2* p = buf + (size_t)pr * N + j;
+            const int pr = item >> lgs, j = item & (s - 1);
+            double2* p = buf + ((size_t)pr << lgN) + j;
             const double2 a = p[0], b = p[s];
             p[0] = cadd(a, b);
             p[s] = cmul(csub(a, b), __ldg(tw + j));
         }
         __syncthreads();
-        L = s;
+        lgL = lgs;
     }
-    const int quarter = N >> 2;
-    while (L >= 4) {
-        const int s = L >> 2;
-        const int stride = N / L;
-        for (int item = tid; item < P * quarter; item += DST_THREADS) {
-            const int pr = item / quarter, t = item - pr * quarter;
-            const int blk = t / s, j = t - blk * s;
-            double2* p = buf + (size_t)pr * N + blk * L + j;
+    const int lgq = lgN - 2;  // quarter = N/4 butterflies per column
+    while (lgL >= 2) {
+        const int lgs = lgL - 2, s = 1 << lgs;
+        const int lgstride = lgN - lgL;
+        for (int item = tid; item < (P << lgq); item += DST_THREADS) {
+            const int pr = item >> lgq, t = item & ((1 << lgq) - 1);
+            const int blk = t >> lgs, j = t & (s - 1);
+            double2* p = buf + ((size_t)pr << lgN) + (blk << lgL) + j;
             const double2 x0 = p[0], x1 = p[s], x2 = p[2 * s], x3 = p[3 * s];
             const double2 a0 = cadd(x0, x2), a1 = csub(x0, x2);
             const double2 b0 = cadd(x1, x3), b1 = csub(x1, x3);
@@ -79,21 +96,22 @@ __device__ void fft_dif(double2* buf, int N, int P, int r2first, const double2* 
                 p[2 * s] = y2;
                 p[3 * s] = y3;
             } else {
-                p[s] = cmul(y1, __ldg(tw + j * stride));
-                p[2 * s] = cmul(y2, __ldg(tw + 2 * j * stride));
-                p[3 * s] = cmul(y3, __ldg(tw + 3 * j * stride));
+                const int js = j << lgstride;
+                p[s] = cmul(y1, __ldg(tw + js));
+                p[2 * s] = cmul(y2, __ldg(tw + 2 * js));
+                p[3 * s] = cmul(y3, __ldg(tw + 3 * js));
             }
         }
         __syncthreads();
-        L = s;
+        lgL = lgs;
     }
+    (void)N;
 }
 
 struct DstArgs {
-    int N, n, P, r2first;
+    int N, lgN, n;
     const double2* tw;
     const double2* tq;
-    const int* rev;
     const double* in;
     double* out;
     const double* base;   // out = base + alpha*T(in) when non-null
@@ -102,110 +120,105 @@ struct DstArgs {
     double out_last;      // factor on output row N-1
 };
 
-// KIND 0: out = S^T in (dst.py:67-73);  KIND 1: out = S in (dst.py:86-93)
-template <int KIND>
+// KIND 0: out = S^T in (dst.py:67-73);  KIND 1: out = S in (dst.py:86-93).
+// P column pairs (W = 2P spatial columns) per CTA; all index math is shifts.
+template <int KIND, int P>
 __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
     extern __shared__ double2 buf[];
-    const int N = a.N, n = a.n, P = a.P, W = 2 * P;
+    constexpr int W = 2 * P;
+    constexpr int lgW = P == 1 ? 1 : P == 2 ? 2 : P == 4 ? 3 : P == 8 ? 4 : 5;
+    const int lgN = a.lgN, N = 1 << lgN, n = a.n;
     const int c0 = blockIdx.x * W;
     const int ncol = min(W, n - c0);
     const int tid = threadIdx.x;
     // ---- load (+ pre-processing) ----
     // batches of LB independent loads per thread keep LB requests in flight
-    // (a load-store-load loop would expose the full HBM latency per element)
-    constexpr int LB = 16;
-    const int total = N * W;
-    auto place = [&](int idx, double v) {
-        const int j = idx / W, cc = idx - j * W;
-        if (j == N - 1) v *= a.in_last;
-        int pos;
-        if (KIND == 0) {
-            if (j & 1) {
-                v = -v;
-                pos = N - 1 - (j >> 1);
-            } else {
-                pos = j >> 1;
-            }
-        } else {
-            pos = N - 1 - j;
-        }
-        double* dst = reinterpret_cast<double*>(buf + (size_t)(cc >> 1) * N + pos) + (cc & 1);
-        *dst = v;
-    };
+    constexpr int LB = 8;
+    const int total = N << lgW;
     for (int base = tid; base < total; base += DST_THREADS * LB) {
         double v[LB];
 #pragma unroll
         for (int i = 0; i < LB; ++i) {
             const int idx = base + i * DST_THREADS;
-            const int j = idx / W, cc = idx - j * W;
+            const int j = idx >> lgW, cc = idx & (W - 1);
             v[i] = (idx < total && cc < ncol) ? __ldg(a.in + (size_t)j * n + c0 + cc) : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < LB; ++i) {
             const int idx = base + i * DST_THREADS;
-            if (idx < total) place(idx, v[i]);
+            if (idx >= total) continue;
+            const int j = idx >> lgW, cc = idx & (W - 1);
+            double x = v[i];
+            if (j == N - 1) x *= a.in_last;
+            int pos;
+            if (KIND == 0) {
+                if (j & 1) {
+                    x = -x;
+                    pos = N - 1 - (j >> 1);
+                } else {
+                    pos = j >> 1;
+                }
+            } else {
+                pos = N - 1 - j;
+            }
+            reinterpret_cast<double*>(buf + ((size_t)(cc >> 1) << lgN) + pos)[cc & 1] = x;
         }
     }
     __syncthreads();
     if (KIND == 1) {
         // Q_k = (t_k Z_k + conj(t_k') Z_k') / 2,  k' = (N - k) mod N,  t_k = e^{-i pi k / 2N}
-        const int half = N / 2 + 1;
-        for (int item = tid; item < P * half; item += DST_THREADS) {
-            const int pr = item / half, k = item - pr * half;
-            const int kp = (N - k) & (N - 1);
-            double2* col = buf + (size_t)pr * N;
-            const double2 zk = col[k], zp = col[kp];
-            const double2 q = __ldg(a.tq + k), qp = __ldg(a.tq + kp);
-            const double2 tk = make_double2(q.x, -q.y), tp = make_double2(qp.x, -qp.y);
-            const double2 ctk = q, ctp = qp;  // conjugates
-            const double2 u1 = cadd(cmul(tk, zk), cmul(ctp, zp));
-            const double2 u2 = cadd(cmul(tp, zp), cmul(ctk, zk));
-            col[k] = make_double2(0.5 * u1.x, 0.5 * u1.y);
-            if (kp != k) col[kp] = make_double2(0.5 * u2.x, 0.5 * u2.y);
+#pragma unroll
+        for (int pr = 0; pr < P; ++pr) {
+            double2* col = buf + ((size_t)pr << lgN);
+            for (int k = tid; k <= (N >> 1); k += DST_THREADS) {
+                const int kp = (N - k) & (N - 1);
+                const double2 zk = col[k], zp = col[kp];
+                const double2 q = __ldg(a.tq + k), qp = __ldg(a.tq + kp);
+                const double2 tk = make_double2(q.x, -q.y), tp = make_double2(qp.x, -qp.y);
+                const double2 u1 = cadd(cmul(tk, zk), cmul(qp, zp));
+                const double2 u2 = cadd(cmul(tp, zp), cmul(q, zk));
+                col[k] = make_double2(0.5 * u1.x, 0.5 * u1.y);
+                if (kp != k) col[kp] = make_double2(0.5 * u2.x, 0.5 * u2.y);
+            }
         }
         __syncthreads();
     }
-    fft_dif(buf, N, P, a.r2first, a.tw);
+    fft_dif<P>(buf, lgN, a.tw);
     // ---- post-processing + store ----
-    auto value = [&](int idx) -> double {
-        const int j = idx / W, cc = idx - j * W;
-        const double2* col = buf + (size_t)(cc >> 1) * N;
-        double v;
-        if (KIND == 0) {
-            const int mm = N - 1 - j;  // out_{N-1-m} = X_m
-            const double2 C = col[__ldg(a.rev + mm)];
-            const double2 D = col[__ldg(a.rev + ((N - mm) & (N - 1)))];
-            const double2 q = __ldg(a.tq + mm);
-            if ((cc & 1) == 0)
-                v = 0.5 * (q.x * (C.x + D.x) + q.y * (C.y - D.y));
-            else
-                v = 0.5 * (q.x * (C.y + D.y) - q.y * (C.x - D.x));
-        } else {
-            const int pos = (j & 1) ? N - 1 - (j >> 1) : (j >> 1);
-            const double2 Dv = col[__ldg(a.rev + pos)];
-            v = (cc & 1) ? Dv.y : Dv.x;
-            if (j & 1) v = -v;
-        }
-        v = a.alpha * v;
-        if (j == N - 1) v *= a.out_last;
-        return v;
-    };
     for (int base = tid; base < total; base += DST_THREADS * LB) {
         double bv[LB];
         if (a.base) {
 #pragma unroll
             for (int i = 0; i < LB; ++i) {
                 const int idx = base + i * DST_THREADS;
-                const int j = idx / W, cc = idx - j * W;
+                const int j = idx >> lgW, cc = idx & (W - 1);
                 bv[i] = (idx < total && cc < ncol) ? __ldg(a.base + (size_t)j * n + c0 + cc) : 0.0;
             }
         }
 #pragma unroll
         for (int i = 0; i < LB; ++i) {
             const int idx = base + i * DST_THREADS;
-            const int j = idx / W, cc = idx - j * W;
+            const int j = idx >> lgW, cc = idx & (W - 1);
             if (idx >= total || cc >= ncol) continue;
-            const double v = value(idx);
+            const double2* col = buf + ((size_t)(cc >> 1) << lgN);
+            double v;
+            if (KIND == 0) {
+                const int mm = N - 1 - j;  // out_{N-1-m} = X_m
+                const double2 C = col[dif_pos(mm, lgN)];
+                const double2 D = col[dif_pos((N - mm) & (N - 1), lgN)];
+                const double2 q = __ldg(a.tq + mm);
+                if ((cc & 1) == 0)
+                    v = 0.5 * (q.x * (C.x + D.x) + q.y * (C.y - D.y));
+                else
+                    v = 0.5 * (q.x * (C.y + D.y) - q.y * (C.x - D.x));
+            } else {
+                const int pos = (j & 1) ? N - 1 - (j >> 1) : (j >> 1);
+                const double2 Dv = col[dif_pos(pos, lgN)];
+                v = (cc & 1) ? Dv.y : Dv.x;
+                if (j & 1) v = -v;
+            }
+            v = a.alpha * v;
+            if (j == N - 1) v *= a.out_last;
             a.out[(size_t)j * n + c0 + cc] = a.base ? bv[i] + v : v;
         }
     }
@@ -283,17 +296,18 @@ void dst_plan_build(DstPlan& d, int N) {
         PINT_CUDA_CHECK(cudaMemcpy(d.rev, rev.data(), N * sizeof(int), cudaMemcpyHostToDevice));
         int P = 65536 / (16 * N);
         if (P < 1) P = 1;
-        if (P > 16) P = 16;
+        if (P > 8) P = 8;
         if ((size_t)P * N * 16 > 200 * 1024)
             pint_throw(PINT_INPUT, "time axis too long for the single-CTA sine transform");
         d.pairs = P;
         // the attribute is per function, shared by every plan in the process:
         // allow the largest plan once instead of the current one
         static const int kMaxSmem = 200 * 1024;
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<0>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+#define PINT_DSTATTR(K, PP) \
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_dst_fft<K, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        PINT_DSTATTR(0, 1) PINT_DSTATTR(0, 2) PINT_DSTATTR(0, 4) PINT_DSTATTR(0, 8)
+        PINT_DSTATTR(1, 1) PINT_DSTATTR(1, 2) PINT_DSTATTR(1, 4) PINT_DSTATTR(1, 8)
+#undef PINT_DSTATTR
     } else {
         std::vector<double> kern((size_t)N * N);
         for (int k = 0; k < N; ++k)
@@ -317,12 +331,14 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
     if (ncols > 0x7fffffffLL) pint_throw(PINT_INPUT, "too many columns");
     DstArgs a{};
     a.N = d.N;
+    {
+        int lg = 0;
+        while ((1 << lg) < d.N) ++lg;
+        a.lgN = lg;
+    }
     a.n = (int)ncols;
-    a.P = d.pairs;
-    a.r2first = d.radix2_first;
     a.tw = d.tw;
     a.tq = d.tq;
-    a.rev = d.rev;
     a.in = in;
     a.out = out;
     a.base = base;
@@ -343,10 +359,23 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
         const int W = 2 * d.pairs;
         const dim3 g((unsigned)((ncols + W - 1) / W));
         const size_t smem = (size_t)d.pairs * d.N * 16;
-        if (K == 0)
-            k_dst_fft<0><<<g, DST_THREADS, smem, c->stream>>>(a);
-        else
-            k_dst_fft<1><<<g, DST_THREADS, smem, c->stream>>>(a);
+#define PINT_DSTL(K, PP) k_dst_fft<K, PP><<<g, DST_THREADS, smem, c->stream>>>(a)
+        if (K == 0) {
+            switch (d.pairs) {
+                case 1: PINT_DSTL(0, 1); break;
+                case 2: PINT_DSTL(0, 2); break;
+                case 4: PINT_DSTL(0, 4); break;
+                default: PINT_DSTL(0, 8); break;
+            }
+        } else {
+            switch (d.pairs) {
+                case 1: PINT_DSTL(1, 1); break;
+                case 2: PINT_DSTL(1, 2); break;
+                case 4: PINT_DSTL(1, 4); break;
+                default: PINT_DSTL(1, 8); break;
+            }
+        }
+#undef PINT_DSTL
     } else {
         const dim3 g((unsigned)((ncols + 255) / 256), d.N);
         if (K == 0)

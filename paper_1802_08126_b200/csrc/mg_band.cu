@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
-                if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                 int plane, Y0, Y1;
                 unit_rows(u, plane, Y0, Y1);
                 const long long pb = plane * n;
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
-                if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                 int plane, y0, y1;
                 unit_rows(u, plane, y0, y1);
                 const long long pb = plane * n, pc = plane * nc;

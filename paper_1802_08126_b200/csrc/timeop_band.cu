@@ -25,7 +25,7 @@ namespace pint {
 
 namespace {
 
-constexpr int TB_MAXSTAGE = 2;
+constexpr int TB_MAXSTAGE = 4;
 constexpr int TB_NT = 256;
 
 enum TShape : int { TS_FULL = 0, TS_SEVEN = 1, TS_FIVE = 2 };
@@ -75,7 +75,8 @@ __device__ __forceinline__ void tb_issue(double* buf, const double* slab, long l
 
 struct TopParams {
     int m, N, G, nchunks, nbands, H, stages;
-    int words;  // one array band (H+2 rows) per stage
+    int words;   // one halo band (H+2 rows) of u or p
+    int wordsf;  // one band (H rows) of f
     const double* mass;
     const double* ast;
     const int* asid;
@@ -116,8 +117,10 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
         qs = max(0, n0 - 1);
         qe = OP == 0 ? n1 : min(N, n1 + 1);
     };
-    auto ustage = [&](int s) { return smem + (2 * s) * P.words; };
-    auto pstage = [&](int s) { return smem + (2 * s + 1) * P.words; };
+    const int wst = 2 * P.words + P.wordsf;
+    auto ustage = [&](int s) { return smem + s * wst; };
+    auto pstage = [&](int s) { return smem + s * wst + P.words; };
+    auto fstage = [&](int s) { return smem + s * wst + 2 * P.words; };
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -136,13 +139,20 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                 const int first = y0 - 1, lo = max(0, first), hi = min(m, y1 + 1);
                 for (int q = qs; q < qe; ++q, ++k) {
                     const int s = k % S;
-                    if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                    if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                     const long long pb = q * n;
                     const Span sp = span_of(pb + (long long)lo * m, pb + (long long)hi * m);
                     const bool need_p = OP == 1 || q >= n0;
-                    mbar_expect_tx(&full[s], need_p ? 2 * sp.bytes : sp.bytes);
+                    // f of the output plane: r1 -> q, z -> q-1
+                    const int t = OP == 0 ? q : q - 1;
+                    const bool need_f = t >= n0 && t < n1;
+                    const long long tb = (long long)t * n;
+                    const uint32_t fbytes =
+                        need_f ? span_of(tb + (long long)y0 * m, tb + (long long)y1 * m).bytes : 0;
+                    mbar_expect_tx(&full[s], (need_p ? 2 * sp.bytes : sp.bytes) + fbytes);
                     tb_issue(ustage(s), P.u, pb, m, first, lo, hi, &full[s]);
                     if (need_p) tb_issue(pstage(s), P.p, pb, m, first, lo, hi, &full[s]);
+                    if (need_f) tb_issue(fstage(s), P.f, tb, m, y0, y0, y1, &full[s]);
                 }
             }
         }
@@ -177,21 +187,10 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
             // z output plane t = q-1, r1 output plane t = q
             const int t = OP == 0 ? q : q - 1;
             const bool emit = t >= n0 && t < n1;
-            double fv[CPT][H];
-            if (emit) {
-#pragma unroll
-                for (int j = 0; j < CPT; ++j) {
-                    const int x = tid + j * TB_NT;
-#pragma unroll
-                    for (int r = 0; r < H; ++r)
-                        fv[j][r] = (x < m && r < nrow)
-                                       ? __ldg(P.f + t * n + (long long)(y0 + r) * m + x)
-                                       : 0.0;
-                }
-            }
             if (staged) mbar_wait(&full[s], (k / S) & 1);
             const double* us = ustage(s) + tb_shift(pb, m, first, lo);
             const double* ps = pstage(s) + tb_shift(pb, m, first, lo);
+            const double* fs = fstage(s) + tb_shift((long long)t * n, m, y0, y0);
 #pragma unroll
             for (int j = 0; j < CPT; ++j) {
                 const int x = tid + j * TB_NT;
@@ -225,7 +224,7 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                     if (OP == 0) {
                         if (emit) {
                             const double ku = t > 0 ? mu - mu_prev[j][r] : mu;
-                            *o = (ku - ap) - fv[j][r];
+                            *o = (ku - ap) - fs[r * m + x];
                         }
                         mu_prev[j][r] = mu;
                     } else {
@@ -234,7 +233,10 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                             const double ktp = has_next ? mp_cur[j][r] - mp : mp_cur[j][r];
                             const double ku = t > 0 ? mu_cur[j][r] - mu_prev[j][r] : mu_cur[j][r];
                             const double ktu = has_next ? mu_cur[j][r] - mu : mu_cur[j][r];
-                            *o = (fv[j][r] - ktp) - ((ku + ktu) + au_cur[j][r]);
+                            // the virtual step q = N has no stage: f_{N-1} straight from HBM
+                            const double fval =
+                                staged ? fs[r * m + x] : __ldg(P.f + t * n + (long long)gy * m + x);
+                            *o = (fval - ktp) - ((ku + ktu) + au_cur[j][r]);
                         }
                         mu_prev[j][r] = mu_cur[j][r];
                         mu_cur[j][r] = mu;
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(TB_NT + 32) k_band_apply(ApplyParams P) {
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
-                if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                 int plane, y0, y1;
                 unit(u, plane, y0, y1);
                 const long long pb = plane * n;
@@ -385,7 +387,7 @@ void launch_timeop_cfg(pint_ctx* c, const TopParams& P, size_t smem, int grid) {
 template <int OP, int CPT>
 void launch_timeop_shapes(pint_ctx* c, const TopParams& P, size_t smem, int grid, int shm,
                           int sha) {
-    constexpr int H = OP == 0 ? 8 : 4;  // z carries 4 planes of state per row: keep it in registers
+    constexpr int H = 4;  // z carries 4 planes of state per row: keep it in registers
     if (shm == TS_SEVEN && sha == TS_FIVE) launch_timeop_cfg<OP, CPT, H, TS_SEVEN, TS_FIVE>(c, P, smem, grid);
     else if (shm == TS_SEVEN) launch_timeop_cfg<OP, CPT, H, TS_SEVEN, TS_FULL>(c, P, smem, grid);
     else launch_timeop_cfg<OP, CPT, H, TS_FULL, TS_FULL>(c, P, smem, grid);
@@ -400,12 +402,20 @@ void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, c
     TopParams P{};
     P.m = c->m;
     P.N = c->N;
-    P.H = op == OP_R1 ? 8 : 4;
+    P.H = 4;
     P.G = 8;
     P.nbands = (P.m + P.H - 1) / P.H;
     P.nchunks = (P.N + P.G - 1) / P.G;
-    P.stages = 2;
     P.words = band_words(P.H + 2, P.m);
+    P.wordsf = band_words(P.H, P.m);
+    {
+        // deepest ring that keeps two CTAs per SM
+        const size_t wst = sizeof(double) * (2 * (size_t)P.words + P.wordsf);
+        int st = (int)((110 * 1024) / wst);
+        P.stages = std::max(2, std::min(TB_MAXSTAGE, st));
+        const char* e = getenv("PINT_STAGES");
+        if (e) P.stages = std::max(2, std::min(TB_MAXSTAGE, atoi(e)));
+    }
     P.mass = c->d_mass;
     P.ast = c->d_ast;
     P.asid = c->d_asid;
@@ -414,7 +424,7 @@ void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, c
     P.p = p;
     P.f = f;
     P.out = out;
-    const size_t smem = sizeof(double) * (size_t)P.stages * 2 * P.words;
+    const size_t smem = sizeof(double) * (size_t)P.stages * (2 * P.words + P.wordsf);
     const int grid = grid_for(smem, P.nbands * P.nchunks);
     const int shm = shape_of(c->h_mass.data());
     int sha = TS_FIVE;
