@@ -190,6 +190,7 @@ template <int SH, int NT, int CPT, int HC>
 __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
+    __shared__ double meta[MAXSTAGE][PINT_TW];  // per-stage stencil + dinv, written by the producer
     constexpr int RR = 2 * HC + 1;  // residual rows per unit
     const int m = P.m, mc = P.mc, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
@@ -221,7 +222,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
                 const long long pb = plane * n;
                 const int first = 2 * Y0 - 1;
                 const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
-                mbar_expect_tx(&full[s], band_bytes(pb, m, lo, hi));
+                const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+#pragma unroll
+                for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
+                mbar_expect_tx(&full[s], band_bytes(pb, m, lo, hi));  // release: meta visible
                 band_issue(smem + s * P.words_b, P.b, pb, m, first, lo, hi, &full[s]);
             }
         }
@@ -233,15 +237,14 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
         int plane, Y0, Y1;
         unit_rows(u, plane, Y0, Y1);
         const long long pb = plane * n;
-        const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
-        double ca[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) ca[q] = __ldg(tb + q);
-        const double d = __ldg(tb + 9);
         const int first = 2 * Y0 - 1;
         const int lo = max(0, first);
         const int nr = 2 * (Y1 - Y0) + 1;
         mbar_wait(&full[s], (k / S) & 1);
+        double ca[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
+        const double d = meta[s][9];
         const BandView vb = band_view(smem + s * P.words_b, pb, m, first, lo);
         // residual r = b - A(dinv*b) on fine rows 2*Y0 .. 2*Y1 (slots 1 .. nr)
 #pragma unroll
@@ -333,6 +336,7 @@ template <int SH, int EPI, int NT, int CPT, int H>
 __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
+    __shared__ double meta[MAXSTAGE][PINT_TW + 1];  // stencil, dinv, tau (producer-written)
     __shared__ double red[NT / 32];
     const int m = P.m, mc = P.mc, mp = m + 2, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
@@ -376,6 +380,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
                 const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
                 uint32_t bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
                 if (HAS_Q) bytes += band_bytes(pb, m, y0, y1);
+                const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+#pragma unroll
+                for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
+                meta[s][PINT_TW] = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
                 mbar_expect_tx(&full[s], bytes);
                 band_issue(sb(s), P.b, pb, m, fb, lob, hib, &full[s]);
                 band_issue(se(s), P.ec, pc, mc, fe, loe, hie, &full[s]);
@@ -391,15 +399,14 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
         int plane, y0, y1;
         unit_rows(u, plane, y0, y1);
         const long long pb = plane * n, pc = plane * nc;
-        const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
-        double ca[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) ca[q] = __ldg(tb + q);
-        const double d = __ldg(tb + 9);
         const int fb = y0 - 1, lob = max(0, fb);
         const int fe = y0 / 2 - 1, loe = max(0, fe);
         const int nrow = y1 - y0;
         mbar_wait(&full[s], (k / S) & 1);
+        double ca[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
+        const double d = meta[s][9];
         const BandView vb = band_view(sb(s), pb, m, fb, lob);
         const BandView ve = band_view(se(s), pc, mc, fe, loe);
         // x = dinv*b + P e on rows y0-1 .. y1 (tile rows 0 .. nrow+1)
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
         consumer_sync<NT>();
         // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
         const BandView vq = band_view(sq(s), pb, m, y0, y0);
-        const double tau = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
+        const double tau = meta[s][PINT_TW];
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
             const int x = tid + j * NT;

@@ -77,6 +77,8 @@ struct TopParams {
     int m, N, G, nchunks, nbands, H, stages;
     int words;   // one halo band (H+2 rows) of u or p
     int wordsf;  // one band (H rows) of f
+    int one_a;   // every step uses stencil a0 (the proportional / constant case)
+    double cmass[9], a0[9];  // by value: kernel-parameter (constant bank) operands
     const double* mass;
     const double* ast;
     const int* asid;
@@ -96,10 +98,11 @@ __device__ __forceinline__ void wrow(const double* row, bool in, int x, bool w, 
 }
 
 // OP 0: r1 (needs u, p);  OP 1: z (needs u, p, look-ahead)
-template <int OP, int CPT, int H, int SHM, int SHA>
+template <int OP, int CPT, int H, int SHM, int SHA, int ONEA>
 __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[TB_MAXSTAGE], empty[TB_MAXSTAGE];
+    __shared__ double meta[TB_MAXSTAGE][10];  // A_q stencil + scale, producer-written
     const int m = P.m, N = P.N, S = P.stages;
     const long long n = (long long)m * m;
     const int units = P.nbands * P.nchunks;
@@ -149,6 +152,12 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                     const long long tb = (long long)t * n;
                     const uint32_t fbytes =
                         need_f ? span_of(tb + (long long)y0 * m, tb + (long long)y1 * m).bytes : 0;
+                    {
+                        const double* a = P.ast + 9 * __ldg(P.asid + q);
+#pragma unroll
+                        for (int t2 = 0; t2 < 9; ++t2) meta[s][t2] = __ldg(a + t2);
+                        meta[s][9] = __ldg(P.ascale + q);
+                    }
                     mbar_expect_tx(&full[s], (need_p ? 2 * sp.bytes : sp.bytes) + fbytes);
                     tb_issue(ustage(s), P.u, pb, m, first, lo, hi, &full[s]);
                     if (need_p) tb_issue(pstage(s), P.p, pb, m, first, lo, hi, &full[s]);
@@ -159,9 +168,7 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
         return;
     }
     // ---- consumers ----
-    double cm[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) cm[q] = __ldg(P.mass + q);
+    const double* cm = P.cmass;
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int y0, y1, n0, n1, qs, qe;
@@ -178,16 +185,17 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
             const long long pb = q * n;
             double ca[9];
             double sc = 0.0;
-            if (staged) {
-                const double* a = P.ast + 9 * __ldg(P.asid + q);
-#pragma unroll
-                for (int t = 0; t < 9; ++t) ca[t] = __ldg(a + t);
-                sc = __ldg(P.ascale + q);
-            }
             // z output plane t = q-1, r1 output plane t = q
             const int t = OP == 0 ? q : q - 1;
             const bool emit = t >= n0 && t < n1;
-            if (staged) mbar_wait(&full[s], (k / S) & 1);
+            if (staged) {
+                mbar_wait(&full[s], (k / S) & 1);
+                if (!ONEA) {
+#pragma unroll
+                    for (int t2 = 0; t2 < 9; ++t2) ca[t2] = meta[s][t2];
+                }
+                sc = meta[s][9];
+            }
             const double* us = ustage(s) + tb_shift(pb, m, first, lo);
             const double* ps = pstage(s) + tb_shift(pb, m, first, lo);
             const double* fs = fstage(s) + tb_shift((long long)t * n, m, y0, y0);
@@ -213,11 +221,11 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                     if (staged) {
                         wrow(us + (r + 2) * m, gy + 1 < m, x, w, e, uc);
                         mu = wsum<SHM>(cm, ua, ub, uc);
-                        if (OP == 1) au = sc * wsum<SHA>(ca, ua, ub, uc);
+                        if (OP == 1) au = sc * wsum<SHA>(ONEA ? P.a0 : ca, ua, ub, uc);
                         if (OP == 1 || q >= n0) {
                             wrow(ps + (r + 2) * m, gy + 1 < m, x, w, e, pc);
                             if (OP == 1) mp = wsum<SHM>(cm, pa, pbv, pc);
-                            else ap = sc * wsum<SHA>(ca, pa, pbv, pc);
+                            else ap = sc * wsum<SHA>(ONEA ? P.a0 : ca, pa, pbv, pc);
                         }
                     }
                     double* o = P.out + t * n + (long long)gy * m + x;
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
 // out_plane = A stencil (one stencil for all planes) * in_plane, planes [0, count)
 struct ApplyParams {
     int m, count, nbands, H, stages, words;
+    double cst[9];
     const double* st;
     const double* in;
     double* out;
@@ -310,9 +319,7 @@ __global__ void __launch_bounds__(TB_NT + 32) k_band_apply(ApplyParams P) {
         }
         return;
     }
-    double ca[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) ca[q] = __ldg(P.st + q);
+    const double* ca = P.cst;
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
         const int s = k % S;
@@ -370,6 +377,7 @@ int shape_of(const double* st9_host) {
 int grid_for(size_t smem, int units) {
     int per = (int)((227 * 1024) / (smem + 1024));
     per = std::max(1, std::min(per, 4));
+    if (const char* e = getenv("PINT_CTAS")) per = std::max(1, std::min(per, atoi(e)));
     return std::max(1, std::min(units, sms_count() * per));
 }
 
@@ -377,11 +385,16 @@ template <int OP, int CPT, int H, int SHM, int SHA>
 void launch_timeop_cfg(pint_ctx* c, const TopParams& P, size_t smem, int grid) {
     static bool attr = false;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_timeop<OP, CPT, H, SHM, SHA>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_timeop<OP, CPT, H, SHM, SHA, 0>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_timeop<OP, CPT, H, SHM, SHA, 1>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    k_band_timeop<OP, CPT, H, SHM, SHA><<<grid, TB_NT + 32, smem, c->stream>>>(P);
+    if (P.one_a)
+        k_band_timeop<OP, CPT, H, SHM, SHA, 1><<<grid, TB_NT + 32, smem, c->stream>>>(P);
+    else
+        k_band_timeop<OP, CPT, H, SHM, SHA, 0><<<grid, TB_NT + 32, smem, c->stream>>>(P);
 }
 
 template <int OP, int CPT>
@@ -417,6 +430,9 @@ void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, c
         if (e) P.stages = std::max(2, std::min(TB_MAXSTAGE, atoi(e)));
     }
     P.mass = c->d_mass;
+    for (int q = 0; q < 9; ++q) P.cmass[q] = c->h_mass[q];
+    P.one_a = c->n_a == 1;
+    for (int q = 0; q < 9; ++q) P.a0[q] = c->h_ast[q];
     P.ast = c->d_ast;
     P.asid = c->d_asid;
     P.ascale = c->d_ascale;
@@ -453,6 +469,7 @@ void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host,
     P.nbands = (P.m + H - 1) / H;
     P.words = band_words(H + 2, P.m);
     P.st = st_dev;
+    for (int q = 0; q < 9; ++q) P.cst[q] = st_host[q];
     P.in = in;
     P.out = out;
     const size_t smem = sizeof(double) * (size_t)P.stages * P.words;
