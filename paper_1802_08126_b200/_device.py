@@ -45,15 +45,16 @@ def proportional_scales(spec):
     return s * spec.grid.steps
 
 
-class GpuProblem:
-    """Device copy of one ProblemSpec: stencils, steps, scales, MG sets."""
+class HostProblem:
+    """Host-side arrays of one ProblemSpec that the C ABI consumes: stencils,
+    step sizes, stiffness scales and the multigrid tables.  Pure numpy/scipy
+    (setup); accepts the reference's ProblemSpec as well as ours."""
 
-    def __init__(self, spec, device=None):
+    def __init__(self, spec):
         self.spec = spec
         self.m = _grid_side(spec)
         self.N = spec.N
         self.n = spec.dim
-        self.ctx = Context(device)
         m = self.m
         self.steps = np.ascontiguousarray(spec.grid.steps, dtype=np.float64)
         self.mass_st = grid_stencil(spec.mass, m)
@@ -62,33 +63,25 @@ class GpuProblem:
             a_st = grid_stencil(spec.stiffness[0], m)[None, :]
             a_sid = np.zeros(self.N, dtype=np.int32)
             a_scale = scales
-            self.a_sets = [spec.stiffness[0]]
         else:
             ids: dict[int, int] = {}
-            self.a_sets = []
+            sets = []
             a_sid = np.empty(self.N, dtype=np.int32)
             for k, a in enumerate(spec.stiffness):
                 if id(a) not in ids:
-                    ids[id(a)] = len(self.a_sets)
-                    self.a_sets.append(a)
+                    ids[id(a)] = len(sets)
+                    sets.append(a)
                 a_sid[k] = ids[id(a)]
-            a_st = np.stack([grid_stencil(a, m) for a in self.a_sets])
+            a_st = np.stack([grid_stencil(a, m) for a in sets])
             a_scale = self.steps.copy()
         self.scales = scales
         self.a_st = np.ascontiguousarray(a_st)
         self.a_sid = a_sid
         self.a_scale = np.ascontiguousarray(a_scale, dtype=np.float64)
         self.aref_st = grid_stencil(spec.a_ref, m)
-        self.ctx.call("pint_problem_set", 2, m, self.N, self.steps.ctypes.data,
-                      self.mass_st.ctypes.data, self.a_st.shape[0], self.a_st.ctypes.data,
-                      self.a_sid.ctypes.data, self.a_scale.ctypes.data,
-                      self.aref_st.ctypes.data, float(spec.tau_ref))
-        self.atilde_ready = False
-        self.htilde_ready = False
 
-    # ---- multigrid sets -------------------------------------------------
-    def set_atilde(self, hierarchy: MgHierarchy, damping: float):
-        """Per-step hierarchies; one per distinct A_n object (solvers.py:134-140)."""
+    def atilde_tables(self, hierarchy: MgHierarchy, damping: float):
+        """Per-step hierarchies, one per distinct A_n object (solvers.py:134-140)."""
         ids: dict[int, int] = {}
         ops = []
         sid = np.empty(self.N, dtype=np.int32)
@@ -98,17 +91,38 @@ class GpuProblem:
                 ops.append(a)
             sid[k] = ids[id(a)]
         st = np.stack([grid_stencil(a, self.m) for a in ops])
-        self._upload_set(MG_ATILDE, hierarchy, galerkin_tables(st, hierarchy, damping), sid)
-        self.atilde_ready = True
+        return galerkin_tables(st, hierarchy, damping), sid
 
-    def set_htilde(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray):
+    def htilde_tables(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray):
         """H_k = mu_k M + tau_ref A_ref (schur.py:41-47): the coefficient of
         add_matrices(mu_k, M, 1.0, A_ref.scaled(tau_ref)) at every stencil
         position is fl(mu_k m) + fl(1.0 * fl(tau_ref a))."""
         ta = 1.0 * (float(self.spec.tau_ref) * self.aref_st)
         st = mu[:, None] * self.mass_st[None, :] + ta[None, :]
-        sid = np.arange(self.N, dtype=np.int32)
-        self._upload_set(MG_HTILDE, hierarchy, galerkin_tables(st, hierarchy, damping), sid)
+        return galerkin_tables(st, hierarchy, damping), np.arange(self.N, dtype=np.int32)
+
+
+class GpuProblem(HostProblem):
+    """Device copy of one ProblemSpec: stencils, steps, scales, MG sets."""
+
+    def __init__(self, spec, device=None):
+        super().__init__(spec)
+        self.ctx = Context(device)
+        self.ctx.call("pint_problem_set", 2, self.m, self.N, self.steps.ctypes.data,
+                      self.mass_st.ctypes.data, self.a_st.shape[0], self.a_st.ctypes.data,
+                      self.a_sid.ctypes.data, self.a_scale.ctypes.data,
+                      self.aref_st.ctypes.data, float(spec.tau_ref))
+        self.atilde_ready = False
+        self.htilde_ready = False
+
+    def set_atilde(self, hierarchy: MgHierarchy, damping: float):
+        tab, sid = self.atilde_tables(hierarchy, damping)
+        self._upload_set(MG_ATILDE, hierarchy, tab, sid)
+        self.atilde_ready = True
+
+    def set_htilde(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray):
+        tab, sid = self.htilde_tables(hierarchy, damping, mu)
+        self._upload_set(MG_HTILDE, hierarchy, tab, sid)
         self.htilde_ready = True
 
     def _upload_set(self, which, hierarchy, tables, sid):

@@ -154,3 +154,47 @@ def test_product_does_not_import_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present (GPU box)")
+def test_reference_problemspec_is_accepted_bitwise():
+    """A ProblemSpec built by the unmodified reference yields exactly the same
+    device-upload arrays (stencils, scales, multigrid tables) as ours."""
+    import importlib
+    import sys
+
+    sys.path.insert(0, REF_SRC)
+    try:
+        ps = importlib.import_module("pintsolve")
+    finally:
+        sys.path.remove(REF_SRC)
+    from paper_1802_08126_b200._device import HostProblem
+
+    for coeff in (None, lambda t: 0.8 + 0.6 * t):
+        rgrid = ps.build_time_grid("perturbed", 16, 1.3, perturbation=0.3, seed=3)
+        rspec = ps.make_heat_problem("2d", 16, rgrid, coeff=coeff, data="random", seed=11)
+        ogrid = pg.build_time_grid("perturbed", 16, 1.3, perturbation=0.3, seed=3)
+        ospec = pg.make_heat_problem("2d", 16, ogrid, coeff=coeff, data="random", seed=11)
+        hr, ho = HostProblem(rspec), HostProblem(ospec)
+        for name in ("steps", "mass_st", "a_st", "a_sid", "a_scale", "aref_st"):
+            np.testing.assert_array_equal(getattr(hr, name), getattr(ho, name), err_msg=name)
+        hier = pg.build_mg_hierarchy("2d", 16)
+        for t_r, t_o in zip(hr.atilde_tables(hier, 0.8), ho.atilde_tables(hier, 0.8)):
+            np.testing.assert_array_equal(t_r, t_o)
+        mu = pg.frequency_weights(16)
+        for t_r, t_o in zip(hr.htilde_tables(hier, 0.8, mu), ho.htilde_tables(hier, 0.8, mu)):
+            np.testing.assert_array_equal(t_r, t_o)
+        # and the tables reproduce the reference's own multigrid operators
+        rsch = ps.build_schur_preconditioner(rspec, "mg", vcycles=1)
+        tab, _ = hr.htilde_tables(hier, 0.8, mu)
+        for k in (0, 9, 15):
+            for lvl, op in enumerate(rsch.solvers[k]._ops):
+                ml = hier.cells[lvl] - 1
+                if ml >= 3:
+                    diff = (op - stencil_matrix_2d(tab[lvl, k, :9], ml)).tocoo()
+                    assert not np.any(diff.data)
+                np.testing.assert_array_equal(rsch.solvers[k]._dinv[lvl],
+                                              np.full(ml * ml, tab[lvl, k, 9]))
