@@ -149,6 +149,31 @@ int pint_uzawa(pint_ctx* ctx, const double* f, double* p, double* u, double omeg
                double tol, int max_iter, int use_initial, double* res_hist, int* iters,
                int* converged, double* phase_ms);
 
+/* ---------------------------------------------------------------------------
+ * Time-partitioned building blocks (one context per rank).  The
+ * driver (paper_1802_08126_b200/distributed.py) moves ghost planes and
+ * transposes with torch.distributed; these calls do the arithmetic.  All
+ * pointers must be device pointers.
+ *
+ * pint_set_partition: this context's N steps are global steps [n0, n0+N) of
+ *   N_global.  With has_prev / has_next the u and p slabs passed to the
+ *   residual calls carry the neighbours' boundary planes at local plane -1 / N
+ *   (the pointer still addresses local plane 0).
+ * pint_residual_r1 / _z: r1 = K u - A p - f, z = f - K^T p - (K u + K^T u + A u)
+ *   over the local steps (solvers.py:224, 227-229).
+ * pint_atilde_update: p += A~^{-1} r1, *dot = sum r1.dp over the local steps
+ *   (solvers.py:225-226, 233); p == NULL: only *dot = sum r1.(A~^{-1} r1).
+ * pint_htilde_modes: for this rank's DST modes zh, w = (2 tau_ref/N_global)
+ *   V_H(A_ref V_H(zh)) and *dot = sum zh.w (schur.py:69-75); w == NULL: dot only.
+ * pint_axpy: u = u + omega*y on `count` values (solvers.py:231).
+ * ------------------------------------------------------------------------- */
+int pint_set_partition(pint_ctx* ctx, int n0, int N_global, int has_prev, int has_next);
+int pint_residual_r1(pint_ctx* ctx, const double* u, const double* p, const double* f, double* r1);
+int pint_residual_z(pint_ctx* ctx, const double* u, const double* p, const double* f, double* z);
+int pint_atilde_update(pint_ctx* ctx, const double* r1, double* p, double* dot);
+int pint_htilde_modes(pint_ctx* ctx, const double* zh, double* w, double* dot);
+int pint_axpy(pint_ctx* ctx, double* u, const double* y, double omega, long long count);
+
 /* Enable per-phase CUDA-event timing of pint_uzawa_step (on != 0) and read
  * the cumulative device milliseconds {dst, multigrid, other} since begin()
  * (the fft_seconds / spatial_seconds columns of ConvergenceHistory,

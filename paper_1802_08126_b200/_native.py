@@ -60,6 +60,12 @@ _SIGNATURES = {
     "pint_kernel_stat": (_I, [_P, _I, ctypes.POINTER(ctypes.c_char_p), _DP,
                               ctypes.POINTER(ctypes.c_longlong), _DP]),
     "pint_uzawa_run": (_I, [_P, _D, _I, _P, _DP]),
+    "pint_set_partition": (_I, [_P, _I, _I, _I, _I]),
+    "pint_residual_r1": (_I, [_P, _P, _P, _P, _P]),
+    "pint_residual_z": (_I, [_P, _P, _P, _P, _P]),
+    "pint_atilde_update": (_I, [_P, _P, _P, _DP]),
+    "pint_htilde_modes": (_I, [_P, _P, _P, _DP]),
+    "pint_axpy": (_I, [_P, _P, _P, _D, ctypes.c_longlong]),
     "pint_launch_count": (ctypes.c_longlong, [_P]),
 }
 

@@ -388,6 +388,9 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
         c->N = N;
         c->tau_ref = tau_ref;
         c->n_a = n_a;
+        c->n0 = 0;
+        c->N_global = N;
+        c->has_prev = c->has_next = false;
         c->h_steps.assign(steps, steps + N);
         c->h_mass.assign(mass, mass + PINT_S2);
         c->h_ast.assign(a_st, a_st + (size_t)n_a * PINT_S2);
@@ -555,6 +558,102 @@ int pint_dst_raw(pint_ctx* c, int kind, int N, long long ncols, const double* in
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         dfree(tmp_in);
         dfree(tmp_out);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// time-partitioned building blocks (driven by paper_1802_08126_b200/distributed.py)
+// ---------------------------------------------------------------------------
+static void require_device(const void* p, const char* what) {
+    if (p == nullptr || !is_device_ptr(p))
+        pint_throw(PINT_INPUT, std::string(what) + " must be a device pointer");
+}
+
+int pint_set_partition(pint_ctx* c, int n0, int N_global, int has_prev, int has_next) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (n0 < 0 || N_global < n0 + c->N)
+            pint_throw(PINT_DIMENSION, "partition does not contain the local steps");
+        if ((has_prev != 0) != (n0 > 0) || (has_next != 0) != (n0 + c->N < N_global))
+            pint_throw(PINT_INPUT, "ghost flags disagree with the partition");
+        c->n0 = n0;
+        c->N_global = N_global;
+        c->has_prev = has_prev != 0;
+        c->has_next = has_next != 0;
+    });
+}
+
+int pint_residual_r1(pint_ctx* c, const double* u, const double* p, const double* f, double* r1) {
+    return guarded(c, [&] {
+        require_problem(c);
+        require_device(u, "u");
+        require_device(p, "p");
+        require_device(f, "f");
+        require_device(r1, "r1");
+        pint::launch_timeop(c, pint::OP_R1, u, p, f, r1);
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        pint_prof_drain(c);
+    });
+}
+
+int pint_residual_z(pint_ctx* c, const double* u, const double* p, const double* f, double* z) {
+    return guarded(c, [&] {
+        require_problem(c);
+        require_device(u, "u");
+        require_device(p, "p");
+        require_device(f, "f");
+        require_device(z, "z");
+        pint::launch_timeop(c, pint::OP_Z, u, p, f, z);
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        pint_prof_drain(c);
+    });
+}
+
+static double read_acc(pint_ctx* c, int slot) {
+    PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc, c->d_acc + slot, sizeof(double),
+                                    cudaMemcpyDeviceToHost, c->stream));
+    PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    pint_prof_drain(c);
+    return c->h_acc[0];
+}
+
+int pint_atilde_update(pint_ctx* c, const double* r1, double* p, double* dot) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (!c->mg[PINT_MG_ATILDE].ready) pint_throw(PINT_INPUT, "A~ multigrid set not configured");
+        require_device(r1, "r1");
+        if (p) require_device(p, "p");
+        pint::vcycle(c, PINT_MG_ATILDE, c->N, r1, p, p ? EPI_UZAWA_P : EPI_DOT_TAU, 1.0, p,
+                     nullptr, 0);
+        const double v = read_acc(c, 0);
+        if (dot) *dot = v;
+    });
+}
+
+int pint_htilde_modes(pint_ctx* c, const double* zh, double* w, double* dot) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (!c->mg[PINT_MG_HTILDE].ready) pint_throw(PINT_INPUT, "H~ multigrid set not configured");
+        require_device(zh, "zh");
+        if (w) require_device(w, "w");
+        ensure_uzawa_buffers(c);
+        const int Ng = c->N_global > 0 ? c->N_global : c->N;
+        const double s = 2.0 * c->tau_ref / Ng;  // schur.py:67 with the global N
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, zh, c->d_w2, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
+        pint::launch_aref(c, c->d_w2, c->d_z, c->N);
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_z, w, w ? EPI_SCALE_DOT : EPI_SCALE_DOTONLY, s,
+                     nullptr, zh, 1);
+        const double v = read_acc(c, 1);
+        if (dot) *dot = v;
+    });
+}
+
+int pint_axpy(pint_ctx* c, double* u, const double* y, double omega, long long count) {
+    return guarded(c, [&] {
+        require_device(u, "u");
+        require_device(y, "y");
+        pint::launch_axpy(c, u, y, omega, count);
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -92,6 +92,11 @@ struct pint_ctx {
 
     // problem
     int dims = 0, m = 0, n = 0, N = 0;
+    // time partition (pint_set_partition): this context owns global steps
+    // [n0, n0 + N) of N_global; neighbouring ranks' ghost planes sit at local
+    // plane -1 / N of the u and p slabs passed to the residual kernels
+    int n0 = 0, N_global = 0;
+    bool has_prev = false, has_next = false;
     double tau_ref = 0.0;
     int n_a = 0;
     std::vector<double> h_steps, h_mass, h_ast, h_aref;
@@ -157,6 +162,7 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
                    double* out);
 void launch_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f);
 void launch_aref(pint_ctx* c, const double* in, double* out, int count);
+void launch_axpy(pint_ctx* c, double* u, const double* y, double omega, long long count);
 // TMA band versions (timeop_band.cu), used for 64 <= m <= 512
 bool band_timeop_supported(const pint_ctx* c);
 void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,

@@ -12,6 +12,7 @@
 // planes, carrying the mass-stencil products M u_{n-1}, M u_n, M u_{n+1}
 // (and M p_n, M p_{n+1}) in registers so every input plane is read from HBM
 // once (the neighbouring-plane halo is a register carry, not a re-read).
+#include <algorithm>
 #include <cstdlib>
 
 #include "pint_device.cuh"
@@ -23,7 +24,8 @@ constexpr int TX = 32, TY = 8, GT = 8;  // 32x8 spatial tile, 8 planes per CTA
 
 template <int OP>
 __global__ void __launch_bounds__(TX* TY)
-    k_timeop(int m, int N, const double* __restrict__ mass, const double* __restrict__ ast,
+    k_timeop(int m, int N, int qmin, int qmax, const double* __restrict__ mass,
+             const double* __restrict__ ast,
              const int* __restrict__ asid, const double* __restrict__ ascale,
              const double* __restrict__ u, const double* __restrict__ p,
              const double* __restrict__ f, double* __restrict__ out) {
@@ -49,10 +51,14 @@ __global__ void __launch_bounds__(TX* TY)
         return;
     }
     if (OP == OP_K || OP == OP_R1) {
-        double mprev = (n0 > 0) ? stencil9_global(cm, u + (n0 - 1) * n, m, x, y) : 0.0;
+        // planes [qmin, qmax] are addressable (qmin = -1 / qmax = N: ghost planes of the
+        // neighbouring ranks when the time axis is partitioned)
+        double mprev = (n0 - 1 >= qmin)
+                           ? stencil9_global(cm, u + (long long)(n0 - 1) * (long long)n, m, x, y)
+                           : 0.0;
         for (int t = n0; t < n1; ++t) {
             const double mcur = stencil9_global(cm, u + t * n, m, x, y);
-            const double ku = (t > 0) ? mcur - mprev : mcur;
+            const double ku = (t - 1 >= qmin) ? mcur - mprev : mcur;
             if (OP == OP_K) {
                 out[t * n + i] = ku;
             } else {
@@ -70,22 +76,24 @@ __global__ void __launch_bounds__(TX* TY)
     if (OP == OP_KT) {
         double mcur = stencil9_global(cm, u + n0 * n, m, x, y);
         for (int t = n0; t < n1; ++t) {
-            const double mnext = (t + 1 < N) ? stencil9_global(cm, u + (t + 1) * n, m, x, y) : 0.0;
-            out[t * n + i] = (t + 1 < N) ? mcur - mnext : mcur;
+            const double mnext = (t + 1 <= qmax) ? stencil9_global(cm, u + (t + 1) * n, m, x, y) : 0.0;
+            out[t * n + i] = (t + 1 <= qmax) ? mcur - mnext : mcur;
             mcur = mnext;
         }
         return;
     }
     if (OP == OP_Z) {
-        double muprev = (n0 > 0) ? stencil9_global(cm, u + (n0 - 1) * n, m, x, y) : 0.0;
+        double muprev = (n0 - 1 >= qmin)
+                            ? stencil9_global(cm, u + (long long)(n0 - 1) * (long long)n, m, x, y)
+                            : 0.0;
         double mucur = stencil9_global(cm, u + n0 * n, m, x, y);
         double mpcur = stencil9_global(cm, p + n0 * n, m, x, y);
         for (int t = n0; t < n1; ++t) {
-            const bool has_next = t + 1 < N;
+            const bool has_next = t + 1 <= qmax;
             const double munext = has_next ? stencil9_global(cm, u + (t + 1) * n, m, x, y) : 0.0;
             const double mpnext = has_next ? stencil9_global(cm, p + (t + 1) * n, m, x, y) : 0.0;
             const double ktp = has_next ? mpcur - mpnext : mpcur;
-            const double ku = (t > 0) ? mucur - muprev : mucur;
+            const double ku = (t - 1 >= qmin) ? mucur - muprev : mucur;
             const double ktu = has_next ? mucur - munext : mucur;
             const double* a = ast + 9 * __ldg(asid + t);
             double ca[9];
@@ -142,6 +150,20 @@ __global__ void __launch_bounds__(TX* TY)
     }
 }
 
+// u = u + omega * y   (solvers.py:231, time-partitioned driver)
+__global__ void __launch_bounds__(256) k_axpy(double* __restrict__ u, const double* __restrict__ y,
+                                              double omega, long long count) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < count; i += (long long)gridDim.x * 256)
+        u[i] = u[i] + omega * y[i];
+}
+
+void launch_axpy(pint_ctx* c, double* u, const double* y, double omega, long long count) {
+    const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 16);
+    k_axpy<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, c->stream>>>(u, y, omega, count);
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
 // Deterministic final reduction of per-CTA partial sums into d_acc[slot].
 __global__ void __launch_bounds__(1024) k_reduce_partials(const double* __restrict__ part,
                                                           int nparts, double* __restrict__ acc,
@@ -170,8 +192,9 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
     switch (op) {
 #define PINT_OP(OPV)                                                                         \
     case OPV:                                                                                \
-        k_timeop<OPV><<<g, b, 0, c->stream>>>(c->m, c->N, c->d_mass, c->d_ast, c->d_asid, \
-                                              c->d_ascale, u, p, f, out);               \
+        k_timeop<OPV><<<g, b, 0, c->stream>>>(c->m, c->N, c->has_prev ? -1 : 0,             \
+                                              c->has_next ? c->N : c->N - 1, c->d_mass,     \
+                                              c->d_ast, c->d_asid, c->d_ascale, u, p, f, out); \
         break;
         PINT_OP(OP_K)
         PINT_OP(OP_KT)

@@ -78,6 +78,7 @@ struct TopParams {
     int words;   // one halo band (H+2 rows) of u or p
     int wordsf;  // one band (H rows) of f
     int one_a;   // every step uses stencil a0 (the proportional / constant case)
+    int qmin, qmax;  // planes addressable through u/p: -1 / N when a neighbour rank's ghost plane is present
     double cmass[9], a0[9];  // by value: kernel-parameter (constant bank) operands
     const double* mass;
     const double* ast;
@@ -117,8 +118,8 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
     };
     // staged planes of a unit: r1: q in [max(0,n0-1), n1);  z: q in [max(0,n0-1), min(N, n1+1))
     auto qrange = [&](int n0, int n1, int& qs, int& qe) {
-        qs = max(0, n0 - 1);
-        qe = OP == 0 ? n1 : min(N, n1 + 1);
+        qs = max(P.qmin, n0 - 1);
+        qe = OP == 0 ? n1 : min(P.qmax + 1, n1 + 1);
     };
     const int wst = 2 * P.words + P.wordsf;
     auto ustage = [&](int s) { return smem + s * wst; };
@@ -231,15 +232,16 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                     double* o = P.out + t * n + (long long)gy * m + x;
                     if (OP == 0) {
                         if (emit) {
-                            const double ku = t > 0 ? mu - mu_prev[j][r] : mu;
+                            const double ku = t - 1 >= P.qmin ? mu - mu_prev[j][r] : mu;
                             *o = (ku - ap) - fs[r * m + x];
                         }
                         mu_prev[j][r] = mu;
                     } else {
                         if (emit) {
-                            const bool has_next = t + 1 < N;
+                            const bool has_next = t + 1 <= P.qmax;
                             const double ktp = has_next ? mp_cur[j][r] - mp : mp_cur[j][r];
-                            const double ku = t > 0 ? mu_cur[j][r] - mu_prev[j][r] : mu_cur[j][r];
+                            const double ku =
+                                t - 1 >= P.qmin ? mu_cur[j][r] - mu_prev[j][r] : mu_cur[j][r];
                             const double ktu = has_next ? mu_cur[j][r] - mu : mu_cur[j][r];
                             // the virtual step q = N has no stage: f_{N-1} straight from HBM
                             const double fval =
@@ -429,6 +431,8 @@ void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, c
         const char* e = getenv("PINT_STAGES");
         if (e) P.stages = std::max(2, std::min(TB_MAXSTAGE, atoi(e)));
     }
+    P.qmin = c->has_prev ? -1 : 0;
+    P.qmax = c->has_next ? c->N : c->N - 1;
     P.mass = c->d_mass;
     for (int q = 0; q < 9; ++q) P.cmass[q] = c->h_mass[q];
     P.one_a = c->n_a == 1;

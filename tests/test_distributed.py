@@ -1,0 +1,270 @@
+"""Time-partitioned Uzawa (paper_1802_08126_b200/distributed.py) on CPU ranks
+with the gloo backend: ghost-plane exchanges, the time<->column<->mode
+transposes around the sine transforms, and the residual all-reduce.
+
+The rank-local arithmetic is plugged in from the CPU oracle (numpy/scipy,
+test infrastructure), so the test checks the partitioning and communication
+logic: world sizes 2 and 3 (uneven split) must reproduce the single-process
+oracle's residual history and solution."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem(cells=8, N=12, T=0.5, seed=4):
+    import oracle as orc
+
+    n = (cells - 1) ** 2
+    rng = np.random.default_rng(seed)
+    load = rng.standard_normal((N, n))
+    u0 = rng.standard_normal(n)
+    nodes = orc.time_nodes("perturbed", N, T, 0.2, seed)
+    pb = orc.heat_problem("2d", cells, nodes, coeff=lambda t: 1.0 + t, load=load, u_init=u0)
+    return pb
+
+
+class OracleLocalOps:
+    """Rank-local arithmetic from the CPU oracle, same operation order."""
+
+    def __init__(self, pb, part, rank):
+        import oracle as orc
+        from paper_1802_08126_b200.schur import frequency_weights
+
+        self.orc, self.pb = orc, pb
+        self.sl = part.slice(rank)
+        self.nl = part.count(rank)
+        self.n0 = part.start(rank)
+        self.N = pb.N
+        self.prev = self.n0 > 0
+        self.next = self.n0 + self.nl < self.N
+        lev = orc.mg_levels("2d", pb.cells)
+        self.scales = orc.stiffness_scales(pb)
+        self.steps = pb.steps
+        self.A0 = pb.stiffness[0]
+        at = orc.BlockInv(pb, lev)
+        self.vA = at.solvers[self.sl]
+        ht = orc.SchurInv(pb, lev)
+        self.vH = ht.solvers[self.sl]
+        self.aref = pb.a_ref
+        self.scale_h = 2.0 * pb.tau_ref / pb.N
+        self.mu = frequency_weights(pb.N)
+
+    def _M(self, x):
+        return self.pb.mass.dot(x.T).T
+
+    def _A(self, x, idx):
+        # scales_n * (A_0 x_n), operators.py:92-99 (proportional case)
+        return self.scales[idx][:, None] * self.A0.dot(x.T).T
+
+    def r1(self, u_ext, p_ext, f):
+        u = u_ext.numpy()
+        mu = self._M(u)  # planes -1 .. nl
+        loc = mu[1:self.nl + 1]
+        ku = loc.copy()
+        if self.prev:
+            ku[0:] = loc - mu[0:self.nl]
+        else:
+            ku[1:] = loc[1:] - loc[:-1]
+        idx = np.arange(self.n0, self.n0 + self.nl)
+        ap = self._A(p_ext.numpy()[1:self.nl + 1], idx)
+        return torch.from_numpy((ku - ap) - f.numpy())
+
+    def z(self, u_ext, p_ext, f):
+        u, p = u_ext.numpy(), p_ext.numpy()
+        mu, mp = self._M(u), self._M(p)
+        nl = self.nl
+        loc_u, loc_p = mu[1:nl + 1], mp[1:nl + 1]
+        ku = loc_u.copy()
+        if self.prev:
+            ku = loc_u - mu[0:nl]
+        else:
+            ku[1:] = loc_u[1:] - loc_u[:-1]
+        ktu, ktp = loc_u.copy(), loc_p.copy()
+        if self.next:
+            ktu = loc_u - mu[2:nl + 2]
+            ktp = loc_p - mp[2:nl + 2]
+        else:
+            ktu[:-1] = loc_u[:-1] - loc_u[1:]
+            ktp[:-1] = loc_p[:-1] - loc_p[1:]
+        idx = np.arange(self.n0, self.n0 + nl)
+        au = self._A(u[1:nl + 1], idx)
+        return torch.from_numpy((f.numpy() - ktp) - ((ku + ktu) + au))
+
+    def atilde_update(self, r1, p_ext):
+        r = r1.numpy()
+        dp = np.stack([v.apply(r[k]) / self.steps[self.n0 + k] for k, v in enumerate(self.vA)])
+        if p_ext is not None:
+            p = p_ext.numpy()
+            p[1:self.nl + 1] = p[1:self.nl + 1] + dp
+        return float(np.sum(r * dp))
+
+    def dst_cols(self, kind, x):
+        fn = self.orc.dst_inverse_T if kind == 1 else self.orc.dst_inverse
+        return torch.from_numpy(np.ascontiguousarray(fn(x.numpy())))
+
+    def htilde_modes(self, zh, want_w=True):
+        z = zh.numpy()
+        w = np.empty_like(z)
+        for k, v in enumerate(self.vH):
+            y = v.apply(z[k])
+            y = self.aref.dot(y)
+            w[k] = self.scale_h * v.apply(y)
+        return (torch.from_numpy(w) if want_w else None), float(np.sum(z * w))
+
+    def axpy(self, u_local, y, omega):
+        u_local.copy_(u_local + omega * y)
+
+
+def _worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as orc
+        from paper_1802_08126_b200.distributed import Comm, Partition, dist_uzawa_solve
+        from paper_1802_08126_b200.solvers import UzawaConfig
+
+        pb = _problem()
+        part = Partition(pb.N, world)
+        ops = OracleLocalOps(pb, part, rank)
+        f = torch.from_numpy(np.ascontiguousarray(orc.fold_rhs(pb)[part.slice(rank)]))
+        p, u, hist = dist_uzawa_solve(ops, Comm(), pb.N, pb.dim, f,
+                                      UzawaConfig(omega=0.9, tol=1e-10, max_iter=300))
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), p=p.numpy(), u=u.numpy(),
+                 res=np.array(hist.residual), conv=hist.converged)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_time_partitioned_uzawa_matches_single_process(world, tmp_path):
+    import oracle as orc
+    from paper_1802_08126_b200.distributed import Partition
+
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    pb = _problem()
+    lev = orc.mg_levels("2d", pb.cells)
+    ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), 0.9, 1e-10, 300)
+    part = Partition(pb.N, world)
+    outs = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
+    for o in outs:  # every rank holds the same history
+        np.testing.assert_allclose(o["res"], outs[0]["res"], rtol=0, atol=0)
+    res = outs[0]["res"]
+    assert len(res) == len(ref.residual) and bool(outs[0]["conv"]) == ref.converged
+    np.testing.assert_allclose(res, ref.residual, rtol=1e-11)
+    u = np.concatenate([o["u"] for o in outs])
+    p = np.concatenate([o["p"] for o in outs])
+    np.testing.assert_allclose(u, ref.u, rtol=0, atol=1e-12 * np.abs(ref.u).max())
+    np.testing.assert_allclose(p, ref.p, rtol=0, atol=1e-12 * np.abs(ref.p).max())
+    assert sum(part.count(r) for r in range(world)) == pb.N
+
+
+def test_partition_balanced():
+    from paper_1802_08126_b200.distributed import Partition
+
+    p = Partition(10, 3)
+    assert [p.count(r) for r in range(3)] == [4, 3, 3]
+    assert [p.start(r) for r in range(3)] == [0, 4, 7]
+    assert p.slice(2) == slice(7, 10)
+
+
+class LoopbackComm:
+    """W thread-ranks in one process exchanging tensors through a shared
+    mailbox (no kernel waits on another: all waiting is host-side barriers)."""
+
+    def __init__(self, rank, world, shared):
+        self.rank, self.world, self.sh = rank, world, shared
+
+    def _sync(self):
+        self.sh["barrier"].wait()
+
+    def exchange(self, send, recv):
+        self.sh["box"][self.rank] = [s.clone() for s in send]
+        self._sync()
+        for q in range(self.world):
+            recv[q].copy_(self.sh["box"][q][self.rank])
+        self._sync()
+
+    def halo(self, ext, nl, prev, nxt):
+        self.sh["box"][self.rank] = (ext[1].clone(), ext[nl].clone())
+        self._sync()
+        r = self.rank
+        if prev and r > 0:
+            ext[0].copy_(self.sh["box"][r - 1][1])
+        if nxt and r + 1 < self.world:
+            ext[nl + 1].copy_(self.sh["box"][r + 1][0])
+        self._sync()
+
+    def allreduce(self, vals, device):
+        self.sh["box"][self.rank] = list(vals)
+        self._sync()
+        out = [sum(self.sh["box"][q][i] for q in range(self.world)) for i in range(len(vals))]
+        self._sync()
+        return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cells,N,world", [(32, 16, 2), (128, 12, 3)])
+def test_gpu_local_ops_partitioned(cells, N, world):
+    """GpuLocalOps (libpint building blocks with ghost planes, column DSTs,
+    per-rank mode sets) driven by dist_uzawa_solve for `world` ranks on one
+    GPU (threads + loopback transport): same history as the oracle."""
+    import threading
+
+    import oracle as orc
+    import paper_1802_08126_b200 as pg
+    from paper_1802_08126_b200.distributed import GpuLocalOps, Partition, dist_uzawa_solve
+
+    n = (cells - 1) ** 2
+    rng = np.random.default_rng(cells)
+    load = rng.standard_normal((N, n))
+    nodes = orc.time_nodes("uniform", N, 0.25)
+    pb = orc.heat_problem("2d", cells, nodes, load=load, u_init=np.zeros(n))
+    spec = pg.problem_from_arrays("2d", cells, pg.TimeGrid(nodes), load, np.zeros(n))
+    f_all = orc.fold_rhs(pb)
+    hier = pg.build_mg_hierarchy("2d", cells)
+    part = Partition(N, world)
+    shared = {"barrier": threading.Barrier(world), "box": [None] * world}
+    results = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            ops = GpuLocalOps(spec, hier, part, rank)
+            f = torch.from_numpy(np.ascontiguousarray(f_all[part.slice(rank)])).to(ops.dev)
+            results[rank] = dist_uzawa_solve(ops, LoopbackComm(rank, world, shared), N, n, f,
+                                             pg.UzawaConfig(omega=0.9, tol=1e-300, max_iter=8))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+            shared["barrier"].abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    lev = orc.mg_levels("2d", cells)
+    ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), 0.9, 1e-300, 8)
+    res = np.array(results[0][2].residual)
+    np.testing.assert_allclose(res, ref.residual, rtol=1e-10)
+    u = np.concatenate([r[1].cpu().numpy() for r in results])
+    assert np.max(np.abs(u - ref.u)) <= 1e-10 * np.max(np.abs(ref.u))
