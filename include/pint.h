@@ -61,6 +61,9 @@ int pint_ctx_destroy(pint_ctx* ctx);
 const char* pint_last_error(const pint_ctx* ctx);
 /* Synchronise the context stream. */
 int pint_sync(pint_ctx* ctx);
+/* Order all further work on a caller-owned cudaStream_t (e.g. the current
+ * torch stream); NULL restores the context's own stream. */
+int pint_set_stream(pint_ctx* ctx, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Problem: the spatial stencils, step sizes and stiffness scales of one

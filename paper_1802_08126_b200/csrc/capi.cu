@@ -272,7 +272,8 @@ int pint_ctx_create(int device, int rank, int world, const void* nccl_id, pint_c
     c->rank = rank;
     c->world = world;
     const int st = guarded(c, [&] {
-        PINT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        PINT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
         PINT_CUDA_CHECK(cudaMalloc(&c->d_acc, 8 * sizeof(double)));
         PINT_CUDA_CHECK(cudaMallocHost(&c->h_acc, 8 * sizeof(double)));
         for (auto& e : c->ev) PINT_CUDA_CHECK(cudaEventCreate(&e));
@@ -297,7 +298,7 @@ int pint_ctx_destroy(pint_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->prof_pool) cudaEventDestroy(e);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return PINT_OK;
 }
@@ -309,6 +310,13 @@ int pint_sync(pint_ctx* c) {
 }
 
 long long pint_launch_count(const pint_ctx* c) { return c ? c->launches : 0; }
+
+int pint_set_stream(pint_ctx* c, void* stream) {
+    return guarded(c, [&] {
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    });
+}
 
 int pint_profile(pint_ctx* c, int on) {
     return guarded(c, [&] {

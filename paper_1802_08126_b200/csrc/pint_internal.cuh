@@ -87,6 +87,7 @@ struct ProfRec {
 struct pint_ctx {
     int dev = 0, rank = 0, world = 1;
     cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;  // created by the context; `stream` may be a caller's
     std::string err;
     long long launches = 0;
 

@@ -157,52 +157,68 @@ class LocalOps:
         raise NotImplementedError
 
 
-def dist_uzawa_solve(ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.Tensor,
-                     cfg: UzawaConfig, initial=None):
-    """Damped two-stage inexact Uzawa (solvers.py:177-264) on a time-partitioned
-    problem.  Returns (p_local, u_local, ConvergenceHistory) on every rank."""
-    if cfg.diagnostics or cfg.stopping == "s_norm_error":
-        raise InputError("diagnostic stopping is not available on the partitioned path")
-    dev = f_local.device
-    tr = Transposer(comm, N, n, dev)
-    nl = tr.nl
-    if f_local.shape != (nl, n):
-        raise InputError(f"local rhs has shape {tuple(f_local.shape)}, expected {(nl, n)}")
-    prev, nxt = comm.rank > 0, comm.rank + 1 < comm.world
-    u_ext = torch.zeros((nl + 2, n), dtype=torch.float64, device=dev)
-    p_ext = torch.zeros((nl + 2, n), dtype=torch.float64, device=dev)
-    if initial is not None:
-        p_ext[1:nl + 1].copy_(initial[0])
-        u_ext[1:nl + 1].copy_(initial[1])
-    u, p = u_ext[1:nl + 1], p_ext[1:nl + 1]
+class DistUzawa:
+    """Time-partitioned damped two-stage inexact Uzawa (solvers.py:177-264).
 
-    def htilde_dot_only(x):
-        xc = tr.rows_to_cols(x)
-        xh = tr.cols_to_rows(ops.dst_cols(1, xc))
-        return ops.htilde_modes(xh, want_w=False)[1]
+    ``begin()`` computes the reference norm (solvers.py:212-217); each
+    ``step()`` is one iteration (solvers.py:224-233) and returns the residual
+    numerator sqrt(max(sum r1.dp + sum z.y, 0)), identical on every rank."""
 
-    a = ops.atilde_update(f_local, None)
-    h = htilde_dot_only(f_local)
-    tot = comm.allreduce([a, h], dev)
-    ref = float(np.sqrt(max(tot[0] + tot[1], 0.0)))
-    hist = ConvergenceHistory()
-    if ref == 0.0:
-        hist.converged = True
-        return p.clone(), u.clone(), hist
-    first = None
-    t0 = time.perf_counter()
-    for _ in range(cfg.max_iter):
-        comm.halo(u_ext, nl, prev=True, nxt=True)
-        r1 = ops.r1(u_ext, p_ext, f_local)
-        d1 = ops.atilde_update(r1, p_ext)
-        comm.halo(p_ext, nl, prev=False, nxt=True)
-        z = ops.z(u_ext, p_ext, f_local)
+    def __init__(self, ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.Tensor,
+                 initial=None):
+        self.ops, self.comm = ops, comm
+        self.dev = f_local.device
+        self.tr = tr = Transposer(comm, N, n, self.dev)
+        nl = self.nl = tr.nl
+        if f_local.shape != (nl, n):
+            raise InputError(f"local rhs has shape {tuple(f_local.shape)}, expected {(nl, n)}")
+        self.f = f_local
+        self.u_ext = torch.zeros((nl + 2, n), dtype=torch.float64, device=self.dev)
+        self.p_ext = torch.zeros((nl + 2, n), dtype=torch.float64, device=self.dev)
+        if initial is not None:
+            self.p_ext[1:nl + 1].copy_(initial[0])
+            self.u_ext[1:nl + 1].copy_(initial[1])
+        self.u, self.p = self.u_ext[1:nl + 1], self.p_ext[1:nl + 1]
+
+    def begin(self) -> float:
+        ops, tr = self.ops, self.tr
+        a = ops.atilde_update(self.f, None)
+        fh = tr.cols_to_rows(ops.dst_cols(1, tr.rows_to_cols(self.f)))
+        h = ops.htilde_modes(fh, want_w=False)[1]
+        tot = self.comm.allreduce([a, h], self.dev)
+        return float(np.sqrt(max(tot[0] + tot[1], 0.0)))
+
+    def step(self, omega: float) -> float:
+        ops, tr, comm, nl = self.ops, self.tr, self.comm, self.nl
+        comm.halo(self.u_ext, nl, prev=True, nxt=True)
+        r1 = ops.r1(self.u_ext, self.p_ext, self.f)
+        d1 = ops.atilde_update(r1, self.p_ext)
+        comm.halo(self.p_ext, nl, prev=False, nxt=True)
+        z = ops.z(self.u_ext, self.p_ext, self.f)
         zh = tr.cols_to_rows(ops.dst_cols(1, tr.rows_to_cols(z)))  # mode-sharded S z
         w, d2 = ops.htilde_modes(zh, want_w=True)
         y = tr.cols_to_rows(ops.dst_cols(0, tr.rows_to_cols(w)))  # time-sharded S^T w
-        ops.axpy(u, y, cfg.omega)
-        s = comm.allreduce([d1, d2], dev)
-        res = float(np.sqrt(max(s[0] + s[1], 0.0))) / ref
+        ops.axpy(self.u, y, omega)
+        s = comm.allreduce([d1, d2], self.dev)
+        return float(np.sqrt(max(s[0] + s[1], 0.0)))
+
+
+def dist_uzawa_solve(ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.Tensor,
+                     cfg: UzawaConfig, initial=None):
+    """uzawa_solve (solvers.py:177-264) on a time-partitioned problem.
+    Returns (p_local, u_local, ConvergenceHistory) on every rank."""
+    if cfg.diagnostics or cfg.stopping == "s_norm_error":
+        raise InputError("diagnostic stopping is not available on the partitioned path")
+    it = DistUzawa(ops, comm, N, n, f_local, initial)
+    ref = it.begin()
+    hist = ConvergenceHistory()
+    if ref == 0.0:
+        hist.converged = True
+        return it.p.clone(), it.u.clone(), hist
+    first = None
+    t0 = time.perf_counter()
+    for _ in range(cfg.max_iter):
+        res = it.step(cfg.omega) / ref
         if first is None:
             first = max(res, 1e-300)
         hist.append(res, None, None, time.perf_counter() - t0, 0.0, 0.0)
@@ -211,7 +227,7 @@ def dist_uzawa_solve(ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.T
         if res < cfg.tol:
             hist.converged = True
             break
-    return p.clone(), u.clone(), hist
+    return it.p.clone(), it.u.clone(), hist
 
 
 class GpuLocalOps(LocalOps):
@@ -229,6 +245,10 @@ class GpuLocalOps(LocalOps):
         self.n0 = part.start(rank)
         self.ctx = ctx = Context(device)
         self.dev = torch.device("cuda", ctx.device)
+        # launch on the torch stream so the transposes (torch copies, NCCL)
+        # and the kernels are ordered without host synchronisation
+        with torch.cuda.device(self.dev):
+            ctx.call("pint_set_stream", torch.cuda.current_stream().cuda_stream)
         steps = np.ascontiguousarray(hp.steps[sl])
         a_sid = np.ascontiguousarray(hp.a_sid[sl])
         used = np.unique(a_sid)
