@@ -197,6 +197,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
     double* sr = smem + S * P.words_b;  // RR x m
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
+    // element offsets are taken from a 16-byte aligned virtual base so that the
+    // bulk-copy alignment does not depend on where the caller's slab starts
+    const int bob = (int)((reinterpret_cast<uintptr_t>(P.b) >> 3) & 1);
+    const double* gb = P.b - bob;
     auto unit_rows = [&](int u, int& plane, int& Y0, int& Y1) {
         plane = u / P.nbands;
         const int j = u - plane * P.nbands;
@@ -219,14 +223,14 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
                 if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                 int plane, Y0, Y1;
                 unit_rows(u, plane, Y0, Y1);
-                const long long pb = plane * n;
+                const long long pb = plane * n + bob;
                 const int first = 2 * Y0 - 1;
                 const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
                 const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
 #pragma unroll
                 for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
                 mbar_expect_tx(&full[s], band_bytes(pb, m, lo, hi));  // release: meta visible
-                band_issue(smem + s * P.words_b, P.b, pb, m, first, lo, hi, &full[s]);
+                band_issue(smem + s * P.words_b, gb, pb, m, first, lo, hi, &full[s]);
             }
         }
         return;
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
         const int s = k % S;
         int plane, Y0, Y1;
         unit_rows(u, plane, Y0, Y1);
-        const long long pb = plane * n;
+        const long long pb = plane * n + bob;
         const int first = 2 * Y0 - 1;
         const int lo = max(0, first);
         const int nr = 2 * (Y1 - Y0) + 1;
@@ -344,6 +348,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
     double* sx = smem + S * wstage;  // (H+2) x (m+2) zero-padded
     const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
+    const double* qsrc0 = EPI == EPI_UZAWA_P ? P.pin : P.aux;
+    const int bob = (int)((reinterpret_cast<uintptr_t>(P.b) >> 3) & 1);
+    const int boe = (int)((reinterpret_cast<uintptr_t>(P.ec) >> 3) & 1);
+    const int boq = (int)((reinterpret_cast<uintptr_t>(qsrc0) >> 3) & 1);
     constexpr bool HAS_Q = EPI == EPI_UZAWA_P || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
     constexpr bool HAS_DOT =
         EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
@@ -368,26 +376,25 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
     __syncthreads();
     if (tid >= NT) {  // ---- producer warp ----
         if (tid == NT) {
-            const double* qsrc = EPI == EPI_UZAWA_P ? P.pin : P.aux;
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
                 if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                 int plane, y0, y1;
                 unit_rows(u, plane, y0, y1);
-                const long long pb = plane * n, pc = plane * nc;
+                const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
                 const int fb = y0 - 1, lob = max(0, fb), hib = min(m, y1 + 1);
                 const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
                 uint32_t bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
-                if (HAS_Q) bytes += band_bytes(pb, m, y0, y1);
+                if (HAS_Q) bytes += band_bytes(pq, m, y0, y1);
                 const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
 #pragma unroll
                 for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
                 meta[s][PINT_TW] = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
                 mbar_expect_tx(&full[s], bytes);
-                band_issue(sb(s), P.b, pb, m, fb, lob, hib, &full[s]);
-                band_issue(se(s), P.ec, pc, mc, fe, loe, hie, &full[s]);
-                if (HAS_Q) band_issue(sq(s), qsrc, pb, m, y0, y0, y1, &full[s]);
+                band_issue(sb(s), P.b - bob, pb, m, fb, lob, hib, &full[s]);
+                band_issue(se(s), P.ec - boe, pc, mc, fe, loe, hie, &full[s]);
+                if (HAS_Q) band_issue(sq(s), qsrc0 - boq, pq, m, y0, y0, y1, &full[s]);
             }
         }
         return;
@@ -398,7 +405,8 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
         const int s = k % S;
         int plane, y0, y1;
         unit_rows(u, plane, y0, y1);
-        const long long pb = plane * n, pc = plane * nc;
+        const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
+        const long long po = plane * n;  // output plane (plain stores, no alignment needs)
         const int fb = y0 - 1, lob = max(0, fb);
         const int fe = y0 / 2 - 1, loe = max(0, fe);
         const int nrow = y1 - y0;
@@ -461,7 +469,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
         }
         consumer_sync<NT>();
         // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
-        const BandView vq = band_view(sq(s), pb, m, y0, y0);
+        const BandView vq = band_view(sq(s), pq, m, y0, y0);
         const double tau = meta[s][PINT_TW];
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
             const double* col = sx + x;  // padded columns x, x+1, x+2 = fine x-1, x, x+1
             double a0 = col[0], a1 = col[1], a2 = col[2];
             double b0 = col[mp], b1 = col[mp + 1], b2 = col[mp + 2];
-            double* orow = P.out + pb + (long long)y0 * m + x;
+            double* orow = P.out + po + (long long)y0 * m + x;
 #pragma unroll
             for (int r = 0; r < H; ++r) {
                 if (r < nrow) {

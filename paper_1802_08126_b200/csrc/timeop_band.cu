@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
     const long long n = (long long)m * m;
     const int units = P.nbands * P.nchunks;
     const int tid = threadIdx.x;
+    // alignment parity of each slab's base (see span_of): offsets relative to 16-B aligned bases
+    const int bou = (int)((reinterpret_cast<uintptr_t>(P.u) >> 3) & 1);
+    const int bop = (int)((reinterpret_cast<uintptr_t>(P.p) >> 3) & 1);
+    const int bof = (int)((reinterpret_cast<uintptr_t>(P.f) >> 3) & 1);
     // unit u -> band j (fast), chunk c
     auto unit = [&](int u, int& y0, int& y1, int& n0, int& n1) {
         const int c = u / P.nbands, j = u - c * P.nbands;
@@ -145,24 +149,26 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                     const int s = k % S;
                     if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                     const long long pb = q * n;
-                    const Span sp = span_of(pb + (long long)lo * m, pb + (long long)hi * m);
+                    const Span sp = span_of(pb + bou + (long long)lo * m, pb + bou + (long long)hi * m);
+                    const Span spp = span_of(pb + bop + (long long)lo * m, pb + bop + (long long)hi * m);
                     const bool need_p = OP == 1 || q >= n0;
                     // f of the output plane: r1 -> q, z -> q-1
                     const int t = OP == 0 ? q : q - 1;
                     const bool need_f = t >= n0 && t < n1;
                     const long long tb = (long long)t * n;
                     const uint32_t fbytes =
-                        need_f ? span_of(tb + (long long)y0 * m, tb + (long long)y1 * m).bytes : 0;
+                        need_f ? span_of(tb + bof + (long long)y0 * m, tb + bof + (long long)y1 * m).bytes
+                               : 0;
                     {
                         const double* a = P.ast + 9 * __ldg(P.asid + q);
 #pragma unroll
                         for (int t2 = 0; t2 < 9; ++t2) meta[s][t2] = __ldg(a + t2);
                         meta[s][9] = __ldg(P.ascale + q);
                     }
-                    mbar_expect_tx(&full[s], (need_p ? 2 * sp.bytes : sp.bytes) + fbytes);
-                    tb_issue(ustage(s), P.u, pb, m, first, lo, hi, &full[s]);
-                    if (need_p) tb_issue(pstage(s), P.p, pb, m, first, lo, hi, &full[s]);
-                    if (need_f) tb_issue(fstage(s), P.f, tb, m, y0, y0, y1, &full[s]);
+                    mbar_expect_tx(&full[s], sp.bytes + (need_p ? spp.bytes : 0) + fbytes);
+                    tb_issue(ustage(s), P.u - bou, pb + bou, m, first, lo, hi, &full[s]);
+                    if (need_p) tb_issue(pstage(s), P.p - bop, pb + bop, m, first, lo, hi, &full[s]);
+                    if (need_f) tb_issue(fstage(s), P.f - bof, tb + bof, m, y0, y0, y1, &full[s]);
                 }
             }
         }
@@ -197,9 +203,9 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
                 }
                 sc = meta[s][9];
             }
-            const double* us = ustage(s) + tb_shift(pb, m, first, lo);
-            const double* ps = pstage(s) + tb_shift(pb, m, first, lo);
-            const double* fs = fstage(s) + tb_shift((long long)t * n, m, y0, y0);
+            const double* us = ustage(s) + tb_shift(pb + bou, m, first, lo);
+            const double* ps = pstage(s) + tb_shift(pb + bop, m, first, lo);
+            const double* fs = fstage(s) + tb_shift((long long)t * n + bof, m, y0, y0);
 #pragma unroll
             for (int j = 0; j < CPT; ++j) {
                 const int x = tid + j * TB_NT;
@@ -290,6 +296,7 @@ __global__ void __launch_bounds__(TB_NT + 32) k_band_apply(ApplyParams P) {
     const long long n = (long long)m * m;
     const int units = P.nbands * P.count;
     const int tid = threadIdx.x;
+    const int boi = (int)((reinterpret_cast<uintptr_t>(P.in) >> 3) & 1);
     auto unit = [&](int u, int& plane, int& y0, int& y1) {
         plane = u / P.nbands;
         const int j = u - plane * P.nbands;
@@ -312,11 +319,11 @@ __global__ void __launch_bounds__(TB_NT + 32) k_band_apply(ApplyParams P) {
                 if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
                 int plane, y0, y1;
                 unit(u, plane, y0, y1);
-                const long long pb = plane * n;
+                const long long pb = plane * n + boi;
                 const int first = y0 - 1, lo = max(0, first), hi = min(m, y1 + 1);
                 const Span sp = span_of(pb + (long long)lo * m, pb + (long long)hi * m);
                 mbar_expect_tx(&full[s], sp.bytes);
-                tb_issue(smem + s * P.words, P.in, pb, m, first, lo, hi, &full[s]);
+                tb_issue(smem + s * P.words, P.in - boi, pb, m, first, lo, hi, &full[s]);
             }
         }
         return;
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(TB_NT + 32) k_band_apply(ApplyParams P) {
         const int first = y0 - 1, lo = max(0, first);
         const int nrow = y1 - y0;
         mbar_wait(&full[s], (k / S) & 1);
-        const double* vs = smem + s * P.words + tb_shift(pb, m, first, lo);
+        const double* vs = smem + s * P.words + tb_shift(pb + boi, m, first, lo);
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
             const int x = tid + j * TB_NT;
