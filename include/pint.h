@@ -62,8 +62,9 @@ const char* pint_last_error(const pint_ctx* ctx);
 /* Synchronise the context stream. */
 int pint_sync(pint_ctx* ctx);
 /* Order all further work on a caller-owned cudaStream_t (e.g. the current
- * torch stream); NULL restores the context's own stream. */
-int pint_set_stream(pint_ctx* ctx, void* stream);
+ * torch stream; 0 = the legacy default stream); own != 0 restores the
+ * context's own stream. */
+int pint_set_stream(pint_ctx* ctx, void* stream, int own);
 
 /* ---------------------------------------------------------------------------
  * Problem: the spatial stencils, step sizes and stiffness scales of one

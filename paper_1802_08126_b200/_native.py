@@ -38,7 +38,7 @@ _SIGNATURES = {
     "pint_ctx_destroy": (_I, [_P]),
     "pint_last_error": (ctypes.c_char_p, [_P]),
     "pint_sync": (_I, [_P]),
-    "pint_set_stream": (_I, [_P, _P]),
+    "pint_set_stream": (_I, [_P, _P, _I]),
     "pint_problem_set": (_I, [_P, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _D]),
     "pint_fold_rhs": (_I, [_P, _P, _P, _P]),
     "pint_apply_K": (_I, [_P, _P, _P]),

@@ -311,10 +311,11 @@ int pint_sync(pint_ctx* c) {
 
 long long pint_launch_count(const pint_ctx* c) { return c ? c->launches : 0; }
 
-int pint_set_stream(pint_ctx* c, void* stream) {
+int pint_set_stream(pint_ctx* c, void* stream, int own) {
     return guarded(c, [&] {
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+        // stream 0 is the legacy default stream (torch's default): a valid choice
+        c->stream = own ? c->own_stream : static_cast<cudaStream_t>(stream);
     });
 }
 

@@ -248,7 +248,7 @@ class GpuLocalOps(LocalOps):
         # launch on the torch stream so the transposes (torch copies, NCCL)
         # and the kernels are ordered without host synchronisation
         with torch.cuda.device(self.dev):
-            ctx.call("pint_set_stream", torch.cuda.current_stream().cuda_stream)
+            ctx.call("pint_set_stream", torch.cuda.current_stream().cuda_stream, 0)
         steps = np.ascontiguousarray(hp.steps[sl])
         a_sid = np.ascontiguousarray(hp.a_sid[sl])
         used = np.unique(a_sid)
