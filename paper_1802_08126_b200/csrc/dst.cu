@@ -23,6 +23,7 @@
 // relative), not bitwise; the parity tests bound it at the reference's own
 // 1e-13 (tests/test_dst.py:28-41 of the reference).
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "pint_internal.cuh"
@@ -78,6 +79,7 @@ __device__ __forceinline__ void fft_dif(double2* buf, int lgN, const double2* __
     while (lgL >= 2) {
         const int lgs = lgL - 2, s = 1 << lgs;
         const int lgstride = lgN - lgL;
+#pragma unroll 4
         for (int item = tid; item < (P << lgq); item += DST_THREADS) {
             const int pr = item >> lgq, t = item & ((1 << lgq) - 1);
             const int blk = t >> lgs, j = t & (s - 1);
@@ -110,6 +112,7 @@ __device__ __forceinline__ void fft_dif(double2* buf, int lgN, const double2* __
 
 struct DstArgs {
     int N, lgN, n;
+    int debug;  // diagnostic: 1 skip FFT, 2 skip FFT and fold
     const double2* tw;
     const double2* tq;
     const double* in;
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
         }
     }
     __syncthreads();
-    if (KIND == 1) {
+    if (KIND == 1 && a.debug < 2) {
         // Q_k = (t_k Z_k + conj(t_k') Z_k') / 2,  k' = (N - k) mod N,  t_k = e^{-i pi k / 2N}
 #pragma unroll
         for (int pr = 0; pr < P; ++pr) {
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
         }
         __syncthreads();
     }
-    fft_dif<P>(buf, lgN, a.tw);
+    if (a.debug == 0) fft_dif<P>(buf, lgN, a.tw);
     // ---- post-processing + store ----
     for (int base = tid; base < total; base += DST_THREADS * LB) {
         double bv[LB];
@@ -345,6 +348,7 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
     a.alpha = alpha;
     a.in_last = 1.0;
     a.out_last = 1.0;
+    a.debug = getenv("PINT_DST_DEBUG") ? atoi(getenv("PINT_DST_DEBUG")) : 0;
     int K;
     switch (kind) {
         case 0: K = 0; break;

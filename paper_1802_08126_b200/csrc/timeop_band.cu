@@ -425,7 +425,13 @@ void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, c
     P.m = c->m;
     P.N = c->N;
     P.H = 4;
-    P.G = 8;
+    // long time chunks amortise the extra (halo) planes; keep >= 4 units per CTA slot
+    P.G = 32;
+    {
+        const int nb = (P.m + P.H - 1) / P.H;
+        while (P.G > 4 && (long long)nb * ((P.N + P.G - 1) / P.G) < 4LL * 2 * sms_count()) P.G /= 2;
+    }
+    if (const char* e = getenv("PINT_TOP_G")) P.G = std::max(1, atoi(e));
     P.nbands = (P.m + P.H - 1) / P.H;
     P.nchunks = (P.N + P.G - 1) / P.G;
     P.words = band_words(P.H + 2, P.m);
