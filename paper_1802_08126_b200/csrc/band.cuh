@@ -63,7 +63,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
             : "r"(smem_u32(bar)), "r"(phase)
             : "memory");
         if (ok) return;
-        __nanosleep(100);
+        __nanosleep(64);
     }
 }
 

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -169,6 +170,8 @@ void free_slabs(pint_ctx* c) {
 
 void free_problem(pint_ctx* c) {
     dfree(c->d_steps);
+    dfree(c->d_rsteps);
+    c->d_rsteps = nullptr;
     dfree(c->d_mass);
     dfree(c->d_ast);
     dfree(c->d_asid);
@@ -405,6 +408,17 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
         c->h_ast.assign(a_st, a_st + (size_t)n_a * PINT_S2);
         c->h_aref.assign(aref, aref + PINT_S2);
         c->d_steps = upload(c, steps, N);
+        {
+            // x / tau is computed as x * (1/tau) only where that is bit-identical:
+            // tau a power of two (then 1/tau is exact and both round once)
+            std::vector<double> r(N, 0.0);
+            for (int t = 0; t < N; ++t) {
+                int e = 0;
+                const double mant = std::frexp(steps[t], &e);
+                if (mant == 0.5 && e > -1000 && e < 1000) r[t] = std::ldexp(1.0, 1 - e);
+            }
+            c->d_rsteps = upload(c, r.data(), N);
+        }
         c->d_mass = upload(c, mass, PINT_S2);
         c->d_ast = upload(c, a_st, (size_t)n_a * PINT_S2);
         c->d_asid = upload(c, a_sid, N);

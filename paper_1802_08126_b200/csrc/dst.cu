@@ -22,6 +22,7 @@
 // the reference's (scipy/ducc) FFT, so it agrees to rounding (~1e-15
 // relative), not bitwise; the parity tests bound it at the reference's own
 // 1e-13 (tests/test_dst.py:28-41 of the reference).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -300,6 +301,7 @@ void dst_plan_build(DstPlan& d, int N) {
         int P = 65536 / (16 * N);
         if (P < 1) P = 1;
         if (P > 8) P = 8;
+        if (const char* e = getenv("PINT_DST_P")) P = std::max(1, std::min(8, atoi(e)));
         if ((size_t)P * N * 16 > 200 * 1024)
             pint_throw(PINT_INPUT, "time axis too long for the single-CTA sine transform");
         d.pairs = P;

@@ -331,6 +331,7 @@ struct PostBandParams {
     int epi;
     double scale;
     const double* steps;
+    const double* rsteps;
     const double* pin;
     const double* aux;
     double* part;
@@ -340,7 +341,7 @@ template <int SH, int EPI, int NT, int CPT, int H>
 __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
-    __shared__ double meta[MAXSTAGE][PINT_TW + 1];  // stencil, dinv, tau (producer-written)
+    __shared__ double meta[MAXSTAGE][PINT_TW + 2];  // stencil, dinv, tau, 1/tau|0 (producer-written)
     __shared__ double red[NT / 32];
     const int m = P.m, mc = P.mc, mp = m + 2, S = P.stages;
     const long long n = (long long)m * m, nc = (long long)mc * mc;
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
 #pragma unroll
                 for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
                 meta[s][PINT_TW] = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
+                meta[s][PINT_TW + 1] = HAS_TAU ? __ldg(P.rsteps + plane) : 0.0;
                 mbar_expect_tx(&full[s], bytes);
                 band_issue(sb(s), P.b - bob, pb, m, fb, lob, hib, &full[s]);
                 band_issue(se(s), P.ec - boe, pc, mc, fe, loe, hie, &full[s]);
@@ -471,6 +473,8 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
         // x += dinv * (b - A x) on rows y0 .. y1-1, epilogue
         const BandView vq = band_view(sq(s), pq, m, y0, y0);
         const double tau = meta[s][PINT_TW];
+        const double rtau = meta[s][PINT_TW + 1];  // > 0: tau is a power of two
+        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : v / tau; };
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
             const int x = tid + j * NT;
@@ -491,13 +495,13 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
                     if (EPI == EPI_PLAIN) {
                         *o = xn;
                     } else if (EPI == EPI_DIV_TAU) {
-                        *o = xn / tau;
+                        *o = divtau(xn);
                     } else if (EPI == EPI_UZAWA_P) {
-                        const double dp = xn / tau;
+                        const double dp = divtau(xn);
                         *o = vq.row(r, m)[x] + dp;
                         acc += bv * dp;
                     } else if (EPI == EPI_DOT_TAU) {
-                        acc += bv * (xn / tau);
+                        acc += bv * divtau(xn);
                     } else if (EPI == EPI_SCALE) {
                         *o = P.scale * xn;
                     } else if (EPI == EPI_SCALE_DOT) {
@@ -526,6 +530,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
 // ============================================================================
 struct TailParams {
     int lt, L, B;
+    int words_plane;           // smem words per plane group
     int m[12];
     int off_b[12], off_x[12];  // smem word offsets per level
     int off_r;
@@ -537,6 +542,7 @@ struct TailParams {
     int epi;
     double scale;
     const double* steps;
+    const double* rsteps;
     const double* pin;
     const double* aux;
     double* part;
@@ -549,20 +555,37 @@ __device__ __forceinline__ double row_sum_any(const double* c, const double* v, 
     return row_sum<SH_FULL>(c, r0 - m, r0, r0 + m, x, hs, hn, w, e);
 }
 
-__global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
-    extern __shared__ __align__(16) double smem[];
-    const int tid = threadIdx.x;
+template <int GT, int GPB>
+__device__ __forceinline__ void group_sync() {
+    if (GT == 32)
+        __syncwarp();
+    else
+        group_sync<GT, GPB>();
+}
+
+// GT threads cooperate on one plane; GPB planes per CTA (GT = 32: one warp
+// per plane, no CTA barriers -- the small levels are pure latency otherwise)
+template <int GT, int GPB>
+__global__ void __launch_bounds__(GT * GPB) k_mg_tail(TailParams P) {
+    extern __shared__ __align__(16) double smem_all[];
+    const int tid = threadIdx.x % GT;
+    const int grp = threadIdx.x / GT;
+    double* smem = smem_all + (size_t)grp * P.words_plane;
+    auto div_tau = [&](double v, int plane) {
+        const double r = __ldg(P.rsteps + plane);
+        return r > 0.0 ? v * r : v / __ldg(P.steps + plane);
+    };
     double acc = 0.0;
-    for (int plane = blockIdx.x; plane < P.B; plane += gridDim.x) {
+    for (int plane = blockIdx.x * GPB + grp; plane < P.B; plane += gridDim.x * GPB) {
         const int set = __ldg(P.sid + plane);
         const int mt = P.m[P.lt];
         const long long nt = (long long)mt * mt;
         {
             double* B0 = smem + P.off_b[P.lt];
             const double* src = P.b + plane * nt;
-            for (int i = tid; i < nt; i += TT) B0[i] = __ldg(src + i);
+            for (int i = tid; i < nt; i += GT) B0[i] = __ldg(src + i);
         }
-        __syncthreads();
+        group_sync<GT, GPB>();
         // descend
         for (int l = P.lt; l + 1 < P.L; ++l) {
             const int m = P.m[l], mc = P.m[l + 1];
@@ -574,15 +597,15 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
             double* Bl = smem + P.off_b[l];
             double* Xl = smem + P.off_x[l];
             double* R = smem + P.off_r;
-            for (int i = tid; i < m * m; i += TT) Xl[i] = d * Bl[i];
-            __syncthreads();
-            for (int i = tid; i < m * m; i += TT) {
+            for (int i = tid; i < m * m; i += GT) Xl[i] = d * Bl[i];
+            group_sync<GT, GPB>();
+            for (int i = tid; i < m * m; i += GT) {
                 const int y = i / m, x = i - y * m;
                 R[i] = Bl[i] - row_sum_any(ca, Xl, m, y, x);
             }
-            __syncthreads();
+            group_sync<GT, GPB>();
             double* Bc = smem + P.off_b[l + 1];
-            for (int i = tid; i < mc * mc; i += TT) {
+            for (int i = tid; i < mc * mc; i += GT) {
                 const int Y = i / mc, X = i - Y * mc;
                 const double* r0 = R + (2 * Y) * m + 2 * X;
                 const double* r1 = r0 + m;
@@ -598,7 +621,7 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
                 v = v + 0.25 * r2[2];
                 Bc[i] = v;
             }
-            __syncthreads();
+            group_sync<GT, GPB>();
         }
         // coarsest 1x1 (or general single point): x = b / a
         {
@@ -607,8 +630,8 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
             double* Bl = smem + P.off_b[l];
             double* Xl = smem + P.off_x[l];
             const int mm = P.m[l] * P.m[l];
-            for (int i = tid; i < mm; i += TT) Xl[i] = Bl[i] / a;
-            __syncthreads();
+            for (int i = tid; i < mm; i += GT) Xl[i] = Bl[i] / a;
+            group_sync<GT, GPB>();
         }
         // ascend
         for (int l = P.L - 2; l >= P.lt; --l) {
@@ -622,7 +645,7 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
             double* Xl = smem + P.off_x[l];
             const double* Ec = smem + P.off_x[l + 1];
             double* R = smem + P.off_r;
-            for (int i = tid; i < m * m; i += TT) {
+            for (int i = tid; i < m * m; i += GT) {
                 const int y = i / m, x = i - y * m;
                 int ja, jb, ia, ib;
                 double wa, wb, ua, ub;
@@ -646,10 +669,10 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
                 add(vb2 && hb, wb * ub, vb2 && hb ? Ec[jb * mc + ib] : 0.0);
                 Xl[i] = Xl[i] + pe;  // x0 (= dinv*b, kept from the descent) + P e
             }
-            __syncthreads();
+            group_sync<GT, GPB>();
             const bool top = (l == P.lt);
             const long long gplane = plane * (long long)m * m;
-            for (int i = tid; i < m * m; i += TT) {
+            for (int i = tid; i < m * m; i += GT) {
                 const int y = i / m, x = i - y * m;
                 const double bv = Bl[i];
                 const double xn = Xl[i] + d * (bv - row_sum_any(ca, Xl, m, y, x));
@@ -660,14 +683,14 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
                 const long long gi = gplane + i;
                 switch (P.epi) {
                     case EPI_PLAIN: P.out[gi] = xn; break;
-                    case EPI_DIV_TAU: P.out[gi] = xn / __ldg(P.steps + plane); break;
+                    case EPI_DIV_TAU: P.out[gi] = div_tau(xn, plane); break;
                     case EPI_UZAWA_P: {
-                        const double dp = xn / __ldg(P.steps + plane);
+                        const double dp = div_tau(xn, plane);
                         P.out[gi] = __ldg(P.pin + gi) + dp;
                         acc += bv * dp;
                         break;
                     }
-                    case EPI_DOT_TAU: acc += bv * (xn / __ldg(P.steps + plane)); break;
+                    case EPI_DOT_TAU: acc += bv * div_tau(xn, plane); break;
                     case EPI_SCALE: P.out[gi] = P.scale * xn; break;
                     case EPI_SCALE_DOT: {
                         const double w = P.scale * xn;
@@ -678,16 +701,16 @@ __global__ void __launch_bounds__(TT) k_mg_tail(TailParams P) {
                     case EPI_SCALE_DOTONLY: acc += __ldg(P.aux + gi) * (P.scale * xn); break;
                 }
             }
-            __syncthreads();
+            group_sync<GT, GPB>();
             if (!top) {
-                for (int i = tid; i < m * m; i += TT) Xl[i] = R[i];
-                __syncthreads();
+                for (int i = tid; i < m * m; i += GT) Xl[i] = R[i];
+                group_sync<GT, GPB>();
             }
         }
     }
     if (P.part != nullptr) {
-        const double s = block_sum<TT>(acc);
-        if (tid == 0) P.part[blockIdx.x] = s;
+        const double s = block_sum<GT * GPB>(acc);
+        if (threadIdx.x == 0) P.part[blockIdx.x] = s;
     }
 }
 
@@ -710,7 +733,7 @@ static int num_sms() {
     return g_num_sms;
 }
 
-constexpr int TAIL_MAX_M = 63;
+constexpr int TAIL_MAX_M = 31;  // m = 63 runs through the band kernels
 
 // shapes of the level tables: a position is skipped only if it is exactly 0
 // for every set of the level
@@ -728,18 +751,23 @@ void mg_compute_shapes(MgSet& set, const double* tab) {
     }
 }
 
-template <int SH, int NT, int CPT>
-static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+template <int SH, int NT, int CPT, int HC>
+static void launch_pre_h(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
     static bool attr = false;
-    auto* kern = P.Hc == 2 ? k_band_pre<SH, NT, CPT, 2> : k_band_pre<SH, NT, CPT, 4>;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH, NT, CPT, 2>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH, NT, CPT, 4>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH, NT, CPT, HC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    kern<<<grid, NT + 32, smem, c->stream>>>(P);
+    k_band_pre<SH, NT, CPT, HC><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int NT, int CPT>
+static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+    if (P.Hc == 2)
+        launch_pre_h<SH, NT, CPT, 2>(c, P, smem, grid);
+    else
+        launch_pre_h<SH, NT, CPT, 4>(c, P, smem, grid);
 }
 
 template <int SH>
@@ -750,18 +778,30 @@ static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid
     else pint_throw(PINT_INPUT, "grid wider than 511 points is not supported");
 }
 
-template <int SH, int EPI, int NT, int CPT>
-static void launch_post_cfg(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+template <int SH, int EPI, int NT, int CPT, int H>
+static void launch_post_h(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
     static bool attr = false;
-    auto* kern = P.H == 4 ? k_band_post<SH, EPI, NT, CPT, 4> : k_band_post<SH, EPI, NT, CPT, 8>;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI, NT, CPT, 4>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI, NT, CPT, 8>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI, NT, CPT, H>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    kern<<<grid, NT + 32, smem, c->stream>>>(P);
+    k_band_post<SH, EPI, NT, CPT, H><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int EPI, int NT, int CPT>
+static void launch_post_cfg(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    if (P.H == 4)
+        launch_post_h<SH, EPI, NT, CPT, 4>(c, P, smem, grid);
+    else
+        launch_post_h<SH, EPI, NT, CPT, 8>(c, P, smem, grid);
+}
+
+// rows per band (measured, tools/sweep_mg.py: taller bands do not help the
+// coarse levels; 4 rows keep two CTAs per SM at m = 511)
+static int band_rows(int m) {
+    if (const char* e = getenv("PINT_BAND")) return atoi(e) <= 4 ? 4 : 8;
+    return m > 300 ? 4 : 8;
 }
 
 template <int SH, int EPI>
@@ -827,7 +867,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.m = s.m[l];
         P.mc = s.m[l + 1];
         P.B = count;
-        P.Hc = env_int("PINT_BAND", 8) / 2 == 2 ? 2 : 4;  // 4 coarse rows = 8 fine rows
+        P.Hc = band_rows(P.m) / 2;  // coarse rows per unit
         P.nbands = (P.mc + P.Hc - 1) / P.Hc;
         P.words_b = band_words(2 * P.Hc + 3, P.m);
         P.words_r = ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
@@ -877,25 +917,43 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         T.epi = top ? epi : EPI_PLAIN;
         T.scale = scale;
         T.steps = c->d_steps;
+        T.rsteps = c->d_rsteps;
         T.pin = pin;
         T.aux = aux;
-        const size_t smem = sizeof(double) * off;
+        T.words_plane = (off + 1) / 2 * 2;
+        int gpb = (int)((200 * 1024) / (sizeof(double) * (size_t)T.words_plane));
+        gpb = std::max(1, std::min(8, gpb));
+        const bool warp_mode = s.m[lt] <= 31 && gpb >= 1;
+        if (!warp_mode) gpb = 1;
+        const size_t smem = sizeof(double) * (size_t)T.words_plane * gpb;
         static bool attr = false;
         if (!attr) {
-            PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail,
+            PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail<32, 8>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 200 * 1024));
+                                                 220 * 1024));
+            PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail<TT, 1>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 220 * 1024));
             attr = true;
         }
-        if (smem > 200 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
-        const int grid = std::min(count, sms * blocks_per_sm(smem));
+        if (smem > 220 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
+        const int per_cta = warp_mode ? 8 : 1;
+        const int ctas_needed = (count + per_cta - 1) / per_cta;
+        const int grid = std::min(ctas_needed, sms * (warp_mode ? 1 : blocks_per_sm(smem)));
         if (top && dot) {
             ensure_partials(c, grid);
             T.part = c->d_part;
         }
         const double fine = (double)s.m[lt] * s.m[lt];
         ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_TAIL, 8.0 * count * 2.0 * fine);
-        k_mg_tail<<<grid, TT, smem, c->stream>>>(T);
+        if (warp_mode) {
+            // 8 warps per CTA, each owning planes; smem sized for 8 groups
+            const size_t smem8 = sizeof(double) * (size_t)T.words_plane * 8;
+            if (smem8 > 220 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
+            k_mg_tail<32, 8><<<grid, 256, smem8, c->stream>>>(T);
+        } else {
+            k_mg_tail<TT, 1><<<grid, TT, smem, c->stream>>>(T);
+        }
         PINT_LAUNCHED(c);
         PINT_CUDA_CHECK(cudaGetLastError());
         if (top && dot) reduce_partials(c, grid, acc_slot);
@@ -906,7 +964,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.m = s.m[l];
         P.mc = s.m[l + 1];
         P.B = count;
-        P.H = env_int("PINT_BAND", P.m > 300 ? 4 : 8) == 4 ? 4 : 8;
+        P.H = band_rows(P.m);
         P.nbands = (P.m + P.H - 1) / P.H;
         const bool top = l == 0;
         P.epi = top ? epi : EPI_PLAIN;
@@ -924,6 +982,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.out = top ? out : c->lev_x[l];
         P.scale = scale;
         P.steps = c->d_steps;
+        P.rsteps = c->d_rsteps;
         P.pin = pin;
         P.aux = aux;
         const size_t smem =

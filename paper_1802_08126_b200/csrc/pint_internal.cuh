@@ -102,6 +102,7 @@ struct pint_ctx {
     int n_a = 0;
     std::vector<double> h_steps, h_mass, h_ast, h_aref;
     double* d_steps = nullptr;   // [N]
+    double* d_rsteps = nullptr;  // [N] 1/tau_n when tau_n is a power of two (x/tau == x*(1/tau) exactly), else 0
     double* d_mass = nullptr;    // [9]
     double* d_ast = nullptr;     // [n_a][9]
     int* d_asid = nullptr;       // [N]
