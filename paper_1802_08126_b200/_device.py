@@ -16,20 +16,22 @@ import numpy as np
 
 from ._native import MG_ATILDE, MG_HTILDE, Context
 from .errors import InputError
-from .linalg import grid_stencil
-from .spatial import MgHierarchy, galerkin_tables
+from .linalg import grid_stencil, grid_stencil3
+from .spatial import DEFAULT_DAMPING, MgHierarchy, galerkin_tables
 
 
-def _grid_side(spec) -> int:
+def _grid_side(spec):
+    """(dims, m) of the structured interior grid of a problem."""
     meta = getattr(spec, "meta", {}) or {}
     space = meta.get("space", "2d")
-    if space != "2d":
-        raise InputError(f"the GPU path implements the 2d problems (got space={space!r})")
+    if space not in ("2d", "3d"):
+        raise InputError(f"the GPU path implements the 2d and 3d problems (got space={space!r})")
+    dims = 2 if space == "2d" else 3
     mesh = meta.get("mesh")
-    m = int(round(math.sqrt(spec.dim)))
-    if m * m != spec.dim or (mesh is not None and int(mesh) - 1 != m):
-        raise InputError("spatial dimension is not a square structured grid")
-    return m
+    m = int(round(spec.dim ** (1.0 / dims)))
+    if m ** dims != spec.dim or (mesh is not None and int(mesh) - 1 != m):
+        raise InputError("spatial dimension is not a structured grid")
+    return dims, m
 
 
 def proportional_scales(spec):
@@ -52,10 +54,11 @@ class HostProblem:
 
     def __init__(self, spec):
         self.spec = spec
-        self.m = _grid_side(spec)
+        self.dims, self.m = _grid_side(spec)
         self.N = spec.N
         self.n = spec.dim
         m = self.m
+        grid_stencil = self._stencil
         self.steps = np.ascontiguousarray(spec.grid.steps, dtype=np.float64)
         self.mass_st = grid_stencil(spec.mass, m)
         scales = proportional_scales(spec)
@@ -80,6 +83,12 @@ class HostProblem:
         self.a_scale = np.ascontiguousarray(a_scale, dtype=np.float64)
         self.aref_st = grid_stencil(spec.a_ref, m)
 
+    def _stencil(self, mat, m):
+        return grid_stencil(mat, m) if self.dims == 2 else grid_stencil3(mat, m)
+
+    def default_damping(self):
+        return DEFAULT_DAMPING["2d" if self.dims == 2 else "3d"]
+
     def atilde_tables(self, hierarchy: MgHierarchy, damping: float):
         """Per-step hierarchies, one per distinct A_n object (solvers.py:134-140)."""
         ids: dict[int, int] = {}
@@ -90,7 +99,7 @@ class HostProblem:
                 ids[id(a)] = len(ops)
                 ops.append(a)
             sid[k] = ids[id(a)]
-        st = np.stack([grid_stencil(a, self.m) for a in ops])
+        st = np.stack([self._stencil(a, self.m) for a in ops])
         return galerkin_tables(st, hierarchy, damping), sid
 
     def htilde_tables(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray):
@@ -108,7 +117,7 @@ class GpuProblem(HostProblem):
     def __init__(self, spec, device=None):
         super().__init__(spec)
         self.ctx = Context(device)
-        self.ctx.call("pint_problem_set", 2, self.m, self.N, self.steps.ctypes.data,
+        self.ctx.call("pint_problem_set", self.dims, self.m, self.N, self.steps.ctypes.data,
                       self.mass_st.ctypes.data, self.a_st.shape[0], self.a_st.ctypes.data,
                       self.a_sid.ctypes.data, self.a_scale.ctypes.data,
                       self.aref_st.ctypes.data, float(spec.tau_ref))

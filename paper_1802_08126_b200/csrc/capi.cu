@@ -155,12 +155,13 @@ void require_problem(pint_ctx* c) {
 }
 
 void free_slabs(pint_ctx* c) {
-    double** s[] = {&c->d_f,  &c->d_p,  &c->d_u,        &c->d_r1,        &c->d_z,
-                    &c->d_w1, &c->d_w2, &c->d_stage_in, &c->d_stage_out, &c->d_vec};
+    double** s[] = {&c->d_f,  &c->d_p,        &c->d_u,         &c->d_r1,  &c->d_z,  &c->d_w1,
+                    &c->d_w2, &c->d_stage_in, &c->d_stage_out, &c->d_vec, &c->d_t3a, &c->d_t3b};
     for (double** p : s) {
         dfree(*p);
         *p = nullptr;
     }
+    c->t3_cap = 0;
     for (double* p : c->lev_b) dfree(p);
     for (double* p : c->lev_x) dfree(p);
     c->lev_b.clear();
@@ -198,7 +199,7 @@ void ensure_levels(pint_ctx* c, const std::vector<int>& m) {
         c->lev_cap.resize(m.size(), 0);
     }
     for (size_t l = 1; l < m.size(); ++l) {
-        const size_t need = (size_t)c->N * m[l] * m[l];
+        const size_t need = (size_t)c->N * m[l] * m[l] * (c->dims == 3 ? m[l] : 1);
         if (c->lev_cap[l] >= need) continue;
         dfree(c->lev_b[l]);
         dfree(c->lev_x[l]);
@@ -385,7 +386,7 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
                      int n_a, const double* a_st, const int* a_sid, const double* a_scale,
                      const double* aref, double tau_ref) {
     return guarded(c, [&] {
-        if (dims != 2) pint_throw(PINT_INPUT, "only 2D problems are supported by this build");
+        if (dims != 2 && dims != 3) pint_throw(PINT_INPUT, "dims must be 2 or 3");
         if (m < 1 || N < 1 || n_a < 1) pint_throw(PINT_INPUT, "bad problem dimensions");
         if (!steps || !mass || !a_st || !a_sid || !a_scale || !aref)
             pint_throw(PINT_INPUT, "null problem array");
@@ -396,7 +397,8 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
         free_problem(c);
         c->dims = dims;
         c->m = m;
-        c->n = m * m;
+        c->n = dims == 2 ? m * m : m * m * m;
+        const int S = dims == 2 ? 9 : 27;
         c->N = N;
         c->tau_ref = tau_ref;
         c->n_a = n_a;
@@ -404,9 +406,9 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
         c->N_global = N;
         c->has_prev = c->has_next = false;
         c->h_steps.assign(steps, steps + N);
-        c->h_mass.assign(mass, mass + PINT_S2);
-        c->h_ast.assign(a_st, a_st + (size_t)n_a * PINT_S2);
-        c->h_aref.assign(aref, aref + PINT_S2);
+        c->h_mass.assign(mass, mass + S);
+        c->h_ast.assign(a_st, a_st + (size_t)n_a * S);
+        c->h_aref.assign(aref, aref + S);
         c->d_steps = upload(c, steps, N);
         {
             // x / tau is computed as x * (1/tau) only where that is bit-identical:
@@ -419,11 +421,11 @@ int pint_problem_set(pint_ctx* c, int dims, int m, int N, const double* steps, c
             }
             c->d_rsteps = upload(c, r.data(), N);
         }
-        c->d_mass = upload(c, mass, PINT_S2);
-        c->d_ast = upload(c, a_st, (size_t)n_a * PINT_S2);
+        c->d_mass = upload(c, mass, S);
+        c->d_ast = upload(c, a_st, (size_t)n_a * S);
         c->d_asid = upload(c, a_sid, N);
         c->d_ascale = upload(c, a_scale, N);
-        c->d_aref = upload(c, aref, PINT_S2);
+        c->d_aref = upload(c, aref, S);
         pint::dst_plan_build(c->dst, N);
         c->problem_ready = true;
     });
@@ -441,11 +443,12 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
         for (int l = 0; l + 1 < levels; ++l)
             if (level_m[l] != 2 * level_m[l + 1] + 1)
                 pint_throw(PINT_INPUT, "levels must halve the cell count");
+        const int TW = c->dims == 2 ? PINT_TW : 28;
         for (int b = 0; b < c->N; ++b)
             if (sid[b] < 0 || sid[b] >= n_sets) pint_throw(PINT_INPUT, "bad operator-set index");
-        const size_t ntab = (size_t)levels * n_sets * PINT_TW;
+        const size_t ntab = (size_t)levels * n_sets * TW;
         for (int s = 0; s < n_sets; ++s) {
-            const double a = tables[((size_t)(levels - 1) * n_sets + s) * PINT_TW + 4];
+            const double a = tables[((size_t)(levels - 1) * n_sets + s) * TW + (TW - 1) / 2];
             if (!(a > 0.0)) pint_throw(PINT_NOT_SPD, "non-positive pivot: operator is not SPD");
         }
         MgSet& s = c->mg[which];
@@ -457,7 +460,7 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
         s.n_sets = n_sets;
         s.tab = upload(c, tables, ntab);
         s.sid = upload(c, sid, c->N);
-        pint::mg_compute_shapes(s, tables);
+        if (c->dims == 2) pint::mg_compute_shapes(s, tables);
         ensure_levels(c, s.m);
         s.ready = true;
     });

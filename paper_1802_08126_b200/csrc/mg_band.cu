@@ -852,6 +852,10 @@ static int blocks_per_sm(size_t smem) {
 
 void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
             double scale, const double* pin, const double* aux, int acc_slot) {
+    if (c->dims == 3) {
+        vcycle3(c, which, count, b, out, epi, scale, pin, aux, acc_slot);
+        return;
+    }
     MgSet& s = c->mg[which];
     if (!s.ready) pint_throw(PINT_INPUT, "multigrid set not configured");
     const int L = s.levels;

@@ -122,6 +122,8 @@ struct pint_ctx {
     double *d_f = nullptr, *d_p = nullptr, *d_u = nullptr;
     double *d_r1 = nullptr, *d_z = nullptr, *d_w1 = nullptr, *d_w2 = nullptr;
     double *d_stage_in = nullptr, *d_stage_out = nullptr, *d_vec = nullptr;
+    double *d_t3a = nullptr, *d_t3b = nullptr;  // 3D multigrid work slabs
+    size_t t3_cap = 0;
 
     // reductions
     double* d_part = nullptr;    // partial sums
@@ -178,6 +180,13 @@ void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host,
 void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
             double scale, const double* pin, const double* aux, int acc_slot);
 void mg_compute_shapes(MgSet& set, const double* tables);
+// 3D (ops3d.cu)
+void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const double* f,
+                    double* out);
+void launch_apply3(pint_ctx* c, const double* st, const double* in, double* out, int count);
+void launch_fold3(pint_ctx* c, const double* load, const double* u0, double* f);
+void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
+             double scale, const double* pin, const double* aux, int acc_slot);
 
 // sine transforms (dst.cu)
 void dst_plan_build(DstPlan& d, int N);

@@ -180,6 +180,10 @@ static dim3 plane_grid(int m, int planes) {
 
 void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                    double* out) {
+    if (c->dims == 3) {
+        launch_timeop3(c, op, u, p, f, out);
+        return;
+    }
     if ((op == OP_R1 || op == OP_Z) && band_timeop_supported(c) && !getenv("PINT_NO_BAND_TIMEOP")) {
         launch_band_timeop(c, op, u, p, f, out);
         return;
@@ -210,6 +214,10 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
 }
 
 void launch_aref(pint_ctx* c, const double* in, double* out, int count) {
+    if (c->dims == 3) {
+        launch_apply3(c, c->d_aref, in, out, count);
+        return;
+    }
     if (band_timeop_supported(c)) {
         launch_band_apply(c, c->d_aref, c->h_aref.data(), in, out, count);
         return;
@@ -222,6 +230,10 @@ void launch_aref(pint_ctx* c, const double* in, double* out, int count) {
 }
 
 void launch_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f) {
+    if (c->dims == 3) {
+        launch_fold3(c, load, u_init, f);
+        return;
+    }
     ProfScope prof(c, K_FOLD, 16.0 * (double)c->N * c->n);
     k_fold_rhs<<<plane_grid(c->m, c->N), dim3(TX, TY), 0, c->stream>>>(
         c->m, c->N, c->d_steps, c->d_mass, load, u_init, f);

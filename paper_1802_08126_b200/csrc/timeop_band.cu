@@ -417,7 +417,7 @@ void launch_timeop_shapes(pint_ctx* c, const TopParams& P, size_t smem, int grid
 
 }  // namespace
 
-bool band_timeop_supported(const pint_ctx* c) { return c->m >= 64 && c->m <= 512; }
+bool band_timeop_supported(const pint_ctx* c) { return c->dims == 2 && c->m >= 64 && c->m <= 512; }
 
 void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                         double* out) {

@@ -234,12 +234,14 @@ class GpuLocalOps(LocalOps):
     """libpint building blocks for this rank's steps / modes (CUDA tensors)."""
 
     def __init__(self, spec, hierarchy, part: Partition, rank: int, device=None,
-                 damping: float = 4.0 / 5.0):
+                 damping: float | None = None):
         from ._device import HostProblem
         from ._native import MG_ATILDE, MG_HTILDE, Context
         from .schur import frequency_weights
 
         hp = HostProblem(spec)
+        if damping is None:
+            damping = hp.default_damping()
         sl = part.slice(rank)
         self.N, self.n, self.nl = hp.N, hp.n, part.count(rank)
         self.n0 = part.start(rank)
@@ -256,7 +258,7 @@ class GpuLocalOps(LocalOps):
         a_st = np.ascontiguousarray(hp.a_st[used])
         a_sid = np.array([remap[int(s)] for s in a_sid], dtype=np.int32)
         a_scale = np.ascontiguousarray(hp.a_scale[sl])
-        ctx.call("pint_problem_set", 2, hp.m, self.nl, steps.ctypes.data,
+        ctx.call("pint_problem_set", hp.dims, hp.m, self.nl, steps.ctypes.data,
                  hp.mass_st.ctypes.data, a_st.shape[0], a_st.ctypes.data, a_sid.ctypes.data,
                  a_scale.ctypes.data, hp.aref_st.ctypes.data, float(spec.tau_ref))
         ctx.call("pint_set_partition", self.n0, self.N, int(self.n0 > 0),

@@ -22,6 +22,8 @@ DEFAULT_DENSE_EIG_LIMIT = 20_000
 
 # CSR column order of an interior row of a 2D 9-point operator: (dy, dx)
 STENCIL_2D = ((-1, -1), (-1, 0), (-1, 1), (0, -1), (0, 0), (0, 1), (1, -1), (1, 0), (1, 1))
+# ... and of a 3D 27-point operator: (dz, dy, dx), z slowest (EXTENSION, configs 3/5)
+STENCIL_3D = tuple((dz, dy, dx) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1))
 
 
 class SpatialMatrix:
@@ -167,6 +169,62 @@ def stencil_matrix_2d(st: np.ndarray, m: int) -> sp.csr_matrix:
         return sp.csr_matrix((m * m, m * m))
     return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                          shape=(m * m, m * m)).tocsr()
+
+
+def stencil_matrix_3d(st: np.ndarray, m: int) -> sp.csr_matrix:
+    """The m^3 x m^3 CSR matrix of a translation-invariant 27-point stencil."""
+    st = np.asarray(st, dtype=np.float64)
+    z, rem = np.divmod(np.arange(m ** 3), m * m)
+    y, x = np.divmod(rem, m)
+    rows, cols, vals = [], [], []
+    for k, (dz, dy, dx) in enumerate(STENCIL_3D):
+        if st[k] == 0.0:
+            continue
+        ok = ((z + dz >= 0) & (z + dz < m) & (y + dy >= 0) & (y + dy < m)
+              & (x + dx >= 0) & (x + dx < m))
+        idx = np.arange(m ** 3)[ok]
+        rows.append(idx)
+        cols.append(((z[ok] + dz) * m + (y[ok] + dy)) * m + (x[ok] + dx))
+        vals.append(np.full(idx.size, st[k]))
+    if not rows:
+        return sp.csr_matrix((m ** 3, m ** 3))
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(m ** 3, m ** 3)).tocsr()
+
+
+def grid_stencil3(mat, m: int) -> np.ndarray:
+    """27-point stencil of a structured-grid operator on an m^3 interior grid
+    (EXTENSION): exact translation-invariance check as in grid_stencil."""
+    cached = getattr(mat, "_stencil", None)
+    if cached is not None and cached[0] == ("3d", m):
+        return cached[1].copy()
+    csr = _csr_of(mat)
+    if csr.shape != (m ** 3, m ** 3):
+        raise DimensionMismatchError(f"operator of shape {csr.shape} is not on a {m}^3 grid")
+    coo = csr.tocoo()
+    zr, rr = np.divmod(coo.row, m * m)
+    yr, xr = np.divmod(rr, m)
+    zc, rc = np.divmod(coo.col, m * m)
+    yc, xc = np.divmod(rc, m)
+    dz, dy, dx = zc - zr, yc - yr, xc - xr
+    if coo.nnz and max(np.abs(dz).max(), np.abs(dy).max(), np.abs(dx).max()) > 1:
+        raise InputError("operator is not a 27-point stencil on the structured grid")
+    code = ((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1)
+    st = np.zeros(27)
+    for k in range(27):
+        sel = coo.data[code == k]
+        nz = sel[sel != 0.0]
+        if nz.size:
+            st[k] = nz[0]
+    diff = (csr - stencil_matrix_3d(st, m)).tocoo()
+    if np.any(diff.data != 0.0):
+        raise InputError("operator is not translation invariant")
+    if hasattr(mat, "_stencil"):
+        try:
+            mat._stencil = (("3d", m), st.copy())
+        except AttributeError:
+            pass
+    return st
 
 
 def grid_stencil(mat, m: int) -> np.ndarray:

@@ -46,7 +46,8 @@ class SchurPreconditioner:
         self.solver_kind = solver_kind
         self.hierarchy = hierarchy
         self._gp = gpu_problem(spec, device)
-        self._gp.set_htilde(hierarchy, 4.0 / 5.0 if damping is None else damping, self.mu)
+        self._gp.set_htilde(hierarchy, self._gp.default_damping() if damping is None else damping,
+                            self.mu)
 
     def apply_inverse(self, r):
         """One preconditioner action (schur.py:62-76)."""

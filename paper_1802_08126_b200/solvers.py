@@ -140,7 +140,7 @@ class BlockDiagSolver:
         self.steps = spec.grid.steps
         self.hierarchy = hierarchy
         self._gp = gpu_problem(spec, device)
-        self._gp.set_atilde(hierarchy, 4.0 / 5.0 if damping is None else damping)
+        self._gp.set_atilde(hierarchy, self._gp.default_damping() if damping is None else damping)
 
     def apply_inverse(self, b):
         shape = (self.spec.N, self.spec.dim)

@@ -23,7 +23,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .errors import InputError
-from .linalg import STENCIL_2D, grid_stencil
+from .linalg import STENCIL_2D, STENCIL_3D, grid_stencil, grid_stencil3
 
 _PROBE_CELLS = 16
 _CHUNK = 256
@@ -64,13 +64,22 @@ def build_mg_hierarchy(space: str, fine_cells: int) -> MgHierarchy:
     cells = [fine_cells]
     while cells[-1] // 2 >= 2 and cells[-1] > 3:
         cells.append(cells[-1] // 2)
-    if space not in ("1d", "2d"):
+    if space not in ("1d", "2d", "3d"):
         raise InputError(f"unknown space {space!r}")
     pro = []
     for c in cells[1:]:
         p1 = _prolongation_1d(c)
-        pro.append(p1 if space == "1d" else sp.kron(p1, p1).tocsr())
+        if space == "1d":
+            pro.append(p1)
+        elif space == "2d":
+            pro.append(sp.kron(p1, p1).tocsr())
+        else:  # EXTENSION: trilinear transfers for the 3D configs
+            pro.append(sp.kron(sp.kron(p1, p1), p1).tocsr())
     return MgHierarchy(space=space, cells=cells, prolongations=pro)
+
+
+# damped-Jacobi weights: 1D 2/3 and 2D 4/5 (spatial.py:136); 3D 6/7 (EXTENSION)
+DEFAULT_DAMPING = {"1d": 2.0 / 3.0, "2d": 4.0 / 5.0, "3d": 6.0 / 7.0}
 
 
 def _batch_stencil_matrix(st: np.ndarray, m: int) -> sp.csr_matrix:
@@ -114,6 +123,48 @@ def _galerkin_step(st: np.ndarray, fine_cells: int) -> np.ndarray:
     return out
 
 
+def _batch_stencil_matrix3(st: np.ndarray, m: int) -> sp.csr_matrix:
+    B, n = st.shape[0], m ** 3
+    z, rem = np.divmod(np.arange(n), m * m)
+    y, x = np.divmod(rem, m)
+    rows, cols, vals = [], [], []
+    for k, (dz, dy, dx) in enumerate(STENCIL_3D):
+        ok = ((z + dz >= 0) & (z + dz < m) & (y + dy >= 0) & (y + dy < m)
+              & (x + dx >= 0) & (x + dx < m))
+        r = np.arange(n)[ok]
+        c = ((z[ok] + dz) * m + (y[ok] + dy)) * m + (x[ok] + dx)
+        off = (np.arange(B) * n)[:, None]
+        rows.append((off + r[None, :]).ravel())
+        cols.append((off + c[None, :]).ravel())
+        vals.append(np.repeat(st[:, k], r.size))
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(B * n, B * n)).tocsr()
+
+
+def _galerkin_step3(st: np.ndarray, fine_cells: int) -> np.ndarray:
+    """3D analogue of _galerkin_step (probe grid of 8 cells per side)."""
+    cf = min(fine_cells, 8)
+    mf, cc = cf - 1, cf // 2
+    mc = cc - 1
+    p1 = _prolongation_1d(cc)
+    P = sp.kron(sp.kron(p1, p1), p1).tocsr()
+    out = np.zeros((st.shape[0], 27))
+    cz = cy = cx = mc // 2
+    centre = (cz * mc + cy) * mc + cx
+    chunk = 32
+    for s0 in range(0, st.shape[0], chunk):
+        blk = st[s0:s0 + chunk]
+        B = blk.shape[0]
+        A = _batch_stencil_matrix3(blk, mf)
+        Pb = sp.block_diag([P] * B, format="csr")
+        C = (Pb.T @ A @ Pb).tocsr()
+        base = np.arange(B) * (mc ** 3) + centre
+        for k, (dz, dy, dx) in enumerate(STENCIL_3D):
+            if 0 <= cz + dz < mc and 0 <= cy + dy < mc and 0 <= cx + dx < mc:
+                out[s0:s0 + B, k] = np.asarray(C[base, base + (dz * mc + dy) * mc + dx]).ravel()
+    return out
+
+
 def galerkin_tables(fine_stencils: np.ndarray, hierarchy: MgHierarchy,
                     damping: float) -> np.ndarray:
     """Per-(level, set) table of 9 stencil coefficients + dinv, shape (L, S, 10).
@@ -121,17 +172,18 @@ def galerkin_tables(fine_stencils: np.ndarray, hierarchy: MgHierarchy,
     dinv = damping / diag exactly as spatial.py:142; the coarsest level's
     centre coefficient is the 1x1 operator solved directly (spatial.py:143).
     """
-    if hierarchy.space != "2d":
-        raise InputError("the GPU multigrid supports the 2d hierarchy")
+    if hierarchy.space not in ("2d", "3d"):
+        raise InputError("the GPU multigrid supports the 2d and 3d hierarchies")
+    S, step = (9, _galerkin_step) if hierarchy.space == "2d" else (27, _galerkin_step3)
     st = np.atleast_2d(np.asarray(fine_stencils, dtype=np.float64))
     L = hierarchy.levels
-    tab = np.zeros((L, st.shape[0], 10))
+    tab = np.zeros((L, st.shape[0], S + 1))
     cur = st
     for lev in range(L):
-        tab[lev, :, :9] = cur
-        tab[lev, :, 9] = damping / cur[:, 4]
+        tab[lev, :, :S] = cur
+        tab[lev, :, S] = damping / cur[:, S // 2]
         if lev + 1 < L:
-            cur = _galerkin_step(cur, hierarchy.cells[lev])
+            cur = step(cur, hierarchy.cells[lev])
     return tab
 
 
@@ -156,9 +208,9 @@ class MgVCycleSolver(SpatialSolver):
                  smooth_steps: int = 1, damping: float | None = None, device=None):
         _check_mg_options(cycles, smooth_steps, damping)
         if hierarchy.space != "2d":
-            raise InputError("the GPU multigrid supports the 2d hierarchy")
+            raise InputError("the standalone GPU V-cycle supports the 2d hierarchy")
         if damping is None:
-            damping = 4.0 / 5.0
+            damping = DEFAULT_DAMPING["2d"]
         self.target = target
         self.hierarchy = hierarchy
         self.cycles = cycles

@@ -12,7 +12,8 @@ import pytest
 import oracle as orc
 import paper_1802_08126_b200 as pg
 from paper_1802_08126_b200 import _native, spatial
-from paper_1802_08126_b200.linalg import grid_stencil, stencil_matrix_2d
+from paper_1802_08126_b200.linalg import (grid_stencil, grid_stencil3, stencil_matrix_2d,
+                                          stencil_matrix_3d)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -21,6 +22,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_assembly_2d_bitwise(cells):
     m, a = pg.assemble_mass_stiffness_2d(cells)
     om, oa = orc.p1_2d(cells)
+    np.testing.assert_array_equal(m.todense(), om.dense())
+    np.testing.assert_array_equal(a.todense(), oa.dense())
+
+
+@pytest.mark.parametrize("cells", [2, 4, 8])
+def test_assembly_3d_bitwise(cells):
+    """3D extension: Kuhn-split P1 on the unit cube == oracle.p1_3d."""
+    m, a = pg.assemble_mass_stiffness_3d(cells)
+    om, oa = orc.p1_3d(cells)
     np.testing.assert_array_equal(m.todense(), om.dense())
     np.testing.assert_array_equal(a.todense(), oa.dense())
 
@@ -93,6 +103,28 @@ def test_galerkin_tables_match_oracle_hierarchy(cells):
             else:
                 assert mat.toarray()[0, 0] == tab[lvl, s, 4]
             np.testing.assert_array_equal(vc.dinv[lvl], np.full(ml * ml, tab[lvl, s, 9]))
+
+
+@pytest.mark.parametrize("cells", [4, 8, 16])
+def test_galerkin_tables_3d_match_oracle_hierarchy(cells):
+    """3D: 27-point probe-grid Galerkin stencils == the oracle's full-size
+    (P^T A P) with trilinear transfers; damping 6/7."""
+    om, oa = orc.p1_3d(cells)
+    lev = orc.mg_levels("3d", cells)
+    hier = pg.build_mg_hierarchy("3d", cells)
+    ops = [orc.sym_add(mu, om, 1.0, oa.scaled(0.0123)) for mu in orc.frequency_weights(3)] + [oa]
+    st0 = np.stack([grid_stencil3(o.csr, cells - 1) for o in ops])
+    tab = spatial.galerkin_tables(st0, hier, spatial.DEFAULT_DAMPING["3d"])
+    for s, o in enumerate(ops):
+        vc = orc.VCycle(o, lev)
+        for lvl, mat in enumerate(vc.mats):
+            ml = lev.cells[lvl] - 1
+            if ml >= 3:
+                diff = (mat - stencil_matrix_3d(tab[lvl, s, :27], ml)).tocoo()
+                assert not np.any(diff.data), (s, lvl)
+            else:
+                assert mat.toarray()[0, 0] == tab[lvl, s, 13]
+            np.testing.assert_array_equal(vc.dinv[lvl], np.full(ml ** 3, tab[lvl, s, 27]))
 
 
 def test_schur_block_stencils_match_add_matrices():
