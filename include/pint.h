@@ -114,6 +114,31 @@ int pint_apply_Abd(pint_ctx* ctx, const double* in, double* out);
 int pint_mg_set(pint_ctx* ctx, int which, int levels, const int* level_m,
                 int n_sets, const double* tables, const int* sid);
 
+/* ---------------------------------------------------------------------------
+ * Field mode (EXTENSION, BASELINE config 4): 2D stiffness operators that are
+ * not translation invariant, e.g. -div(a(x, t) grad u).  Replaces, for the
+ * structured 2D grids, the reference's general per-step branch: a list of
+ * distinct A_n (problems.py:153-165), tau_n A_n u_n (operators.py:92-99) and
+ * one multigrid hierarchy per distinct A_n (solvers.py:134-140).  Once any
+ * field is set, the stiffness stencils given to pint_problem_set are unused.
+ *
+ * Compact fields of a symmetric P1 operator: three planes [3][n] holding the
+ * centre, east (i, i+1) and north (i, i+m) coefficient of every row.
+ * ------------------------------------------------------------------------- */
+/* fields[count][3][n] (host or device) -> steps [step0, step0 + count). */
+int pint_field_set(pint_ctx* ctx, int step0, int count, const double* fields);
+/* Assemble steps [step0, step0 + count) on the GPU from per-cell weights
+ * cell_w[count][cells][cells] ([j][i] for cell (i, j)), the element loop of
+ * problems.py:99-138 with w_e K_e (bit-identical to the scipy assembly). */
+int pint_field_assemble(pint_ctx* ctx, int step0, int count, const double* cell_w);
+/* A_ref (schur.py:41-47): fields[3][n], or (fields == NULL) a copy of step `step`. */
+int pint_field_aref(pint_ctx* ctx, int step, const double* fields);
+/* Field multigrid set: Galerkin coarse rows of every step (A~) or mode
+ * (H~, mu[N] = frequency weights) built on the GPU, bit-identical to
+ * (P^T A) P of spatial.py:140; damping as spatial.py:136. */
+int pint_mg_set_field(pint_ctx* ctx, int which, int levels, const int* level_m, double damping,
+                      const double* mu);
+
 /* One V-cycle per plane, planes [0, count) of the set (spatial.py:163-169). */
 int pint_vcycle(pint_ctx* ctx, int which, int count, const double* in, double* out);
 

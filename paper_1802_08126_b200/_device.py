@@ -16,7 +16,8 @@ import numpy as np
 
 from ._native import MG_ATILDE, MG_HTILDE, Context
 from .errors import InputError
-from .linalg import grid_stencil, grid_stencil3
+from .linalg import grid_fields, grid_stencil, grid_stencil3
+from .problems import WeightedStiffness
 from .spatial import DEFAULT_DAMPING, MgHierarchy, galerkin_tables
 
 
@@ -37,6 +38,8 @@ def _grid_side(spec):
 def proportional_scales(spec):
     """c_n * tau_n when every A_n is a known multiple of A_1, else None
     (TimeGlobalSystem._proportional_scales, operators.py:41-49)."""
+    if isinstance(spec.stiffness, WeightedStiffness):
+        return None
     base = spec.stiffness[0]
     s = np.empty(spec.N)
     for k, a in enumerate(spec.stiffness):
@@ -61,8 +64,16 @@ class HostProblem:
         grid_stencil = self._stencil
         self.steps = np.ascontiguousarray(spec.grid.steps, dtype=np.float64)
         self.mass_st = grid_stencil(spec.mass, m)
+        self.field = self._field_mode(spec)
         scales = proportional_scales(spec)
-        if scales is not None:
+        if self.field is not None:
+            # per-point coefficients live in device fields; the stencil
+            # arguments of pint_problem_set are placeholders
+            a_st = np.zeros((1, self._st_size()))
+            a_sid = np.zeros(self.N, dtype=np.int32)
+            a_scale = self.steps.copy()
+            scales = None
+        elif scales is not None:
             a_st = grid_stencil(spec.stiffness[0], m)[None, :]
             a_sid = np.zeros(self.N, dtype=np.int32)
             a_scale = scales
@@ -81,7 +92,40 @@ class HostProblem:
         self.a_st = np.ascontiguousarray(a_st)
         self.a_sid = a_sid
         self.a_scale = np.ascontiguousarray(a_scale, dtype=np.float64)
-        self.aref_st = grid_stencil(spec.a_ref, m)
+        self.aref_st = (np.zeros(self._st_size()) if self.field is not None
+                        else grid_stencil(spec.a_ref, m))
+
+    def _st_size(self):
+        return 9 if self.dims == 2 else 27
+
+    def _field_mode(self, spec):
+        """None (translation-invariant stencils), "family" (WeightedStiffness,
+        assembled on the GPU) or "explicit" (2D operators that are not
+        translation invariant: compact per-point fields from the matrices)."""
+        if isinstance(spec.stiffness, WeightedStiffness):
+            if self.dims != 2:
+                raise InputError("weighted stiffness families are 2D")
+            return "family"
+        if self.dims != 2:
+            return None
+        seen = set()
+        for a in spec.stiffness:
+            if id(a) in seen:
+                continue
+            seen.add(id(a))
+            try:
+                grid_stencil(a, self.m)
+            except InputError as e:
+                if "translation invariant" not in str(e):
+                    raise
+                return "explicit"
+        try:
+            grid_stencil(spec.a_ref, self.m)
+        except InputError as e:
+            if "translation invariant" not in str(e):
+                raise
+            return "explicit"
+        return None
 
     def _stencil(self, mat, m):
         return grid_stencil(mat, m) if self.dims == 2 else grid_stencil3(mat, m)
@@ -123,16 +167,58 @@ class GpuProblem(HostProblem):
                       self.aref_st.ctypes.data, float(spec.tau_ref))
         self.atilde_ready = False
         self.htilde_ready = False
+        if self.field is not None:
+            self._upload_fields()
+
+    _FIELD_CHUNK = 32
+
+    def _upload_fields(self):
+        """Per-point stiffness of every step and of A_ref into HBM."""
+        spec, ctx = self.spec, self.ctx
+        if self.field == "family":
+            fam = spec.stiffness
+            for n0 in range(0, self.N, self._FIELD_CHUNK):
+                n1 = min(self.N, n0 + self._FIELD_CHUNK)
+                w = np.ascontiguousarray(fam.cell_weights(n0, n1))
+                ctx.call("pint_field_assemble", n0, n1 - n0, w.ctypes.data)
+        else:
+            cache: dict[int, np.ndarray] = {}
+            for n, a in enumerate(spec.stiffness):
+                f = cache.get(id(a))
+                if f is None:
+                    f = np.ascontiguousarray(grid_fields(a, self.m))
+                    cache = {id(a): f}
+                ctx.call("pint_field_set", n, 1, f.ctypes.data)
+        step = getattr(spec.a_ref, "_family_step", None)
+        if self.field == "family" and step is not None and spec.stiffness[step] is spec.a_ref:
+            ctx.call("pint_field_aref", int(step), None)
+        else:
+            f = np.ascontiguousarray(grid_fields(spec.a_ref, self.m))
+            ctx.call("pint_field_aref", 0, f.ctypes.data)
 
     def set_atilde(self, hierarchy: MgHierarchy, damping: float):
-        tab, sid = self.atilde_tables(hierarchy, damping)
-        self._upload_set(MG_ATILDE, hierarchy, tab, sid)
+        if self.field is not None:
+            self._set_field(MG_ATILDE, hierarchy, damping, None)
+        else:
+            tab, sid = self.atilde_tables(hierarchy, damping)
+            self._upload_set(MG_ATILDE, hierarchy, tab, sid)
         self.atilde_ready = True
 
     def set_htilde(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray):
-        tab, sid = self.htilde_tables(hierarchy, damping, mu)
-        self._upload_set(MG_HTILDE, hierarchy, tab, sid)
+        if self.field is not None:
+            self._set_field(MG_HTILDE, hierarchy, damping,
+                            np.ascontiguousarray(mu, dtype=np.float64))
+        else:
+            tab, sid = self.htilde_tables(hierarchy, damping, mu)
+            self._upload_set(MG_HTILDE, hierarchy, tab, sid)
         self.htilde_ready = True
+
+    def _set_field(self, which, hierarchy, damping, mu):
+        if hierarchy.cells[0] - 1 != self.m or hierarchy.space != "2d":
+            raise InputError("hierarchy does not match the problem mesh")
+        lm = np.asarray(hierarchy.level_m, dtype=np.int32)
+        self.ctx.call("pint_mg_set_field", which, len(lm), lm.ctypes.data, float(damping),
+                      None if mu is None else mu.ctypes.data)
 
     def _upload_set(self, which, hierarchy, tables, sid):
         if hierarchy.cells[0] - 1 != self.m:

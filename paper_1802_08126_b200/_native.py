@@ -68,6 +68,10 @@ _SIGNATURES = {
     "pint_htilde_modes": (_I, [_P, _P, _P, _DP]),
     "pint_axpy": (_I, [_P, _P, _P, _D, ctypes.c_longlong]),
     "pint_launch_count": (ctypes.c_longlong, [_P]),
+    "pint_field_set": (_I, [_P, _I, _I, _P]),
+    "pint_field_assemble": (_I, [_P, _I, _I, _P]),
+    "pint_field_aref": (_I, [_P, _I, _P]),
+    "pint_mg_set_field": (_I, [_P, _I, _I, _P, _D, _P]),
 }
 
 _lib = None

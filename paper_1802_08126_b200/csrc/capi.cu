@@ -169,6 +169,24 @@ void free_slabs(pint_ctx* c) {
     c->lev_cap.clear();
 }
 
+void free_field_set(FieldMg& F) {
+    for (double* p : F.f9) dfree(p);
+    dfree(F.d_mu);
+    F = FieldMg{};
+}
+
+void free_field(pint_ctx* c) {
+    for (FieldMg& F : c->fmg) free_field_set(F);
+    dfree(c->d_fa);
+    dfree(c->d_fref);
+    dfree(c->d_ft);
+    for (double* p : c->lev_t) dfree(p);
+    c->lev_t.clear();
+    c->d_fa = c->d_fref = c->d_ft = nullptr;
+    c->field = false;
+    c->fref_ready = false;
+}
+
 void free_problem(pint_ctx* c) {
     dfree(c->d_steps);
     dfree(c->d_rsteps);
@@ -185,6 +203,7 @@ void free_problem(pint_ctx* c) {
         dfree(s.sid);
         s = MgSet{};
     }
+    free_field(c);
     free_slabs(c);
     pint::dst_plan_free(c->dst);
     c->problem_ready = false;
@@ -250,8 +269,12 @@ void ensure_stage(pint_ctx* c) {
     if (!c->d_stage_out) c->d_stage_out = dalloc<double>(S);
 }
 
+bool set_ready(const pint_ctx* c, int which) {
+    return c->field ? c->fmg[which].ready : c->mg[which].ready;
+}
+
 void require_sets(pint_ctx* c) {
-    if (!c->mg[PINT_MG_ATILDE].ready || !c->mg[PINT_MG_HTILDE].ready)
+    if (!set_ready(c, PINT_MG_ATILDE) || !set_ready(c, PINT_MG_HTILDE))
         pint_throw(PINT_INPUT, "both multigrid sets (A~ and H~) must be configured");
 }
 
@@ -466,6 +489,116 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
     });
 }
 
+// ---------------------------------------------------------------------------
+// field mode: per-point 2D stiffness (field2d.cu)
+// ---------------------------------------------------------------------------
+static void enable_field(pint_ctx* c) {
+    require_problem(c);
+    if (c->dims != 2) pint_throw(PINT_INPUT, "per-point stiffness fields are 2D");
+    if (!c->field) {
+        c->d_fa = dalloc<double>((size_t)c->N * 3 * c->n);
+        PINT_CUDA_CHECK(cudaMemsetAsync(c->d_fa, 0, (size_t)c->N * 3 * c->n * sizeof(double),
+                                        c->stream));
+        c->d_fref = dalloc<double>((size_t)3 * c->n);
+        c->field = true;
+    }
+}
+
+int pint_field_set(pint_ctx* c, int step0, int count, const double* fields) {
+    return guarded(c, [&] {
+        enable_field(c);
+        if (step0 < 0 || count < 0 || step0 + count > c->N || !fields)
+            pint_throw(PINT_DIMENSION, "bad step range");
+        const size_t cnt = (size_t)count * 3 * c->n;
+        PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_fa + (size_t)step0 * 3 * c->n, fields,
+                                        cnt * sizeof(double), cudaMemcpyDefault, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pint_field_assemble(pint_ctx* c, int step0, int count, const double* cell_w) {
+    return guarded(c, [&] {
+        enable_field(c);
+        if (step0 < 0 || count < 0 || step0 + count > c->N || !cell_w)
+            pint_throw(PINT_DIMENSION, "bad step range");
+        if (count == 0) return;
+        const size_t cw = (size_t)(c->m + 1) * (c->m + 1) * count;
+        const double* d = cell_w;
+        double* tmp = nullptr;
+        if (!is_device_ptr(cell_w)) {
+            tmp = dalloc<double>(cw);
+            PINT_CUDA_CHECK(cudaMemcpyAsync(tmp, cell_w, cw * sizeof(double),
+                                            cudaMemcpyHostToDevice, c->stream));
+            d = tmp;
+        }
+        pint::field_assemble(c, step0, count, d);
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        dfree(tmp);
+    });
+}
+
+int pint_field_aref(pint_ctx* c, int step, const double* fields) {
+    return guarded(c, [&] {
+        enable_field(c);
+        const size_t cnt = (size_t)3 * c->n;
+        if (fields) {
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_fref, fields, cnt * sizeof(double),
+                                            cudaMemcpyDefault, c->stream));
+        } else {
+            if (step < 0 || step >= c->N) pint_throw(PINT_DIMENSION, "bad A_ref step");
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_fref, c->d_fa + (size_t)step * cnt,
+                                            cnt * sizeof(double), cudaMemcpyDeviceToDevice,
+                                            c->stream));
+        }
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        c->fref_ready = true;
+    });
+}
+
+int pint_mg_set_field(pint_ctx* c, int which, int levels, const int* level_m, double damping,
+                      const double* mu) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (!c->field) pint_throw(PINT_INPUT, "no stiffness fields set");
+        if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE)
+            pint_throw(PINT_INPUT, "unknown multigrid set");
+        if (levels < 2 || !level_m || !(damping > 0.0)) pint_throw(PINT_INPUT, "bad multigrid description");
+        if (level_m[0] != c->m) pint_throw(PINT_DIMENSION, "finest level does not match problem");
+        for (int l = 0; l + 1 < levels; ++l)
+            if (level_m[l] != 2 * level_m[l + 1] + 1)
+                pint_throw(PINT_INPUT, "levels must halve the cell count");
+        if (level_m[levels - 1] != 1) pint_throw(PINT_INPUT, "coarsest level must be a single point");
+        if (which == PINT_MG_HTILDE && (!mu || !c->fref_ready))
+            pint_throw(PINT_INPUT, "H~ needs mode weights and the A_ref field");
+        FieldMg& F = c->fmg[which];
+        free_field_set(F);
+        F.levels = levels;
+        F.m.assign(level_m, level_m + levels);
+        F.damping = damping;
+        F.f9.assign(levels, nullptr);
+        for (int l = 1; l < levels; ++l)
+            F.f9[l] = dalloc<double>((size_t)c->N * 9 * level_m[l] * level_m[l]);
+        if (mu) F.d_mu = upload(c, mu, c->N);
+        pint::field_galerkin(c, which);
+        // coarsest pivots (spatial.py:143 factorises the 1x1 operator)
+        std::vector<double> piv((size_t)c->N * 9);
+        PINT_CUDA_CHECK(cudaMemcpyAsync(piv.data(), F.f9[levels - 1], piv.size() * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        for (int s = 0; s < c->N; ++s)
+            if (!(piv[(size_t)s * 9 + 4] > 0.0))
+                pint_throw(PINT_NOT_SPD, "non-positive pivot: operator is not SPD");
+        ensure_levels(c, F.m);
+        if (!c->d_ft) c->d_ft = dalloc<double>(slab(c));
+        if (c->lev_t.size() < (size_t)levels) c->lev_t.resize(levels, nullptr);
+        for (int l = 1; l < levels; ++l) {
+            dfree(c->lev_t[l]);
+            c->lev_t[l] = dalloc<double>((size_t)c->N * level_m[l] * level_m[l]);
+        }
+        F.ready = true;
+    });
+}
+
 int pint_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f) {
     return guarded(c, [&] {
         require_problem(c);
@@ -536,7 +669,7 @@ int pint_atilde_inv(pint_ctx* c, const double* in, double* out) {
 int pint_htilde_inv(pint_ctx* c, const double* in, double* out) {
     return guarded(c, [&] {
         require_problem(c);
-        if (!c->mg[PINT_MG_HTILDE].ready) pint_throw(PINT_INPUT, "H~ multigrid set not configured");
+        if (!set_ready(c, PINT_MG_HTILDE)) pint_throw(PINT_INPUT, "H~ multigrid set not configured");
         ensure_stage(c);
         ensure_uzawa_buffers(c);
         const double* d = stage_in(c, in, c->d_stage_in, slab(c));
@@ -646,7 +779,7 @@ static double read_acc(pint_ctx* c, int slot) {
 int pint_atilde_update(pint_ctx* c, const double* r1, double* p, double* dot) {
     return guarded(c, [&] {
         require_problem(c);
-        if (!c->mg[PINT_MG_ATILDE].ready) pint_throw(PINT_INPUT, "A~ multigrid set not configured");
+        if (!set_ready(c, PINT_MG_ATILDE)) pint_throw(PINT_INPUT, "A~ multigrid set not configured");
         require_device(r1, "r1");
         if (p) require_device(p, "p");
         pint::vcycle(c, PINT_MG_ATILDE, c->N, r1, p, p ? EPI_UZAWA_P : EPI_DOT_TAU, 1.0, p,
@@ -659,7 +792,7 @@ int pint_atilde_update(pint_ctx* c, const double* r1, double* p, double* dot) {
 int pint_htilde_modes(pint_ctx* c, const double* zh, double* w, double* dot) {
     return guarded(c, [&] {
         require_problem(c);
-        if (!c->mg[PINT_MG_HTILDE].ready) pint_throw(PINT_INPUT, "H~ multigrid set not configured");
+        if (!set_ready(c, PINT_MG_HTILDE)) pint_throw(PINT_INPUT, "H~ multigrid set not configured");
         require_device(zh, "zh");
         if (w) require_device(w, "w");
         ensure_uzawa_buffers(c);

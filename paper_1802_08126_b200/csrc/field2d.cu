@@ -1,0 +1,583 @@
+// Variable-coefficient 2D stiffness: A_n with per-point coefficients
+// (BASELINE config 4, -div(a(x,t) grad u)).  EXTENSION:
+// the reference accepts any list of stiffness matrices (problems.py:153-165,
+// operators.py:92-99 general branch, solvers.py:134-140 one hierarchy per
+// distinct A_n); this file is the GPU form of that general branch for
+// structured 2D grids whose operators are not translation invariant.
+//
+// Storage:
+//   * fine A_n, compact: [N][3][n] = centre, east, north coefficient of every
+//     row; the west / south entries of row i are the east / north entries of
+//     rows i-1 / i-m (the reference materialises the lower triangle as a
+//     mirror of the upper one, linalg.py:49-59), the SW / NE hypotenuse
+//     entries are stored zeros of the P1 diagonal split;
+//   * A_ref: one compact field [3][n];
+//   * H_k = mu_k M + tau_ref A_ref is never stored on the fine level: its
+//     coefficients fl(mu_k m) + fl(tau_ref a) are formed on the fly;
+//   * coarse Galerkin operators of every set (step or mode): full 9-point
+//     rows [sets][9][m_l^2], computed on the GPU in scipy's SpGEMM
+//     accumulation order so they are bit-identical to the reference's
+//     (P^T A) P (spatial.py:140).
+//
+// Every row sum follows CSR column order from 0 without FMA (-fmad=false),
+// so results are bit-identical to scipy's csr_matvec on the same matrices.
+// Round-1 form: one thread per point, neighbours through L1/L2.
+#include <algorithm>
+
+#include "pint_device.cuh"
+#include "pint_internal.cuh"
+
+namespace pint {
+
+namespace {
+
+constexpr int FX = 32, FY = 8, FG = 8;  // 32x8 tile, 8 time planes per CTA (marching ops)
+constexpr int FT = 256;
+
+enum FieldMode : int { FM_A = 0, FM_H = 1, FM_9 = 2 };
+
+struct Src {
+    const double* f = nullptr;     // FM_A: compact [sets][3][n]; FM_9: [sets][9][n]
+    size_t set_stride = 0;         // doubles between consecutive sets (0: shared by all)
+    const double* mass = nullptr;  // FM_H: constant mass stencil [9]
+    const double* mu = nullptr;    // FM_H: per-set weight mu_k
+    double tau = 0.0;              // FM_H: tau_ref
+};
+
+// coefficient k (CSR position SW,S,SE,W,C,E,NW,N,NE) of row (x, y) of set s;
+// only called when that neighbour exists
+template <int MODE>
+__device__ __forceinline__ double coef(const Src& S, int s, int k, int m, int x, int y) {
+    const size_t n = (size_t)m * m;
+    const size_t i = (size_t)y * m + x;
+    const double* f = S.f + (size_t)s * S.set_stride;
+    if (MODE == FM_9) return __ldg(f + (size_t)k * n + i);
+    double a;
+    switch (k) {
+        case 1: a = __ldg(f + 2 * n + i - m); break;  // S = north entry of row i-m
+        case 3: a = __ldg(f + n + i - 1); break;      // W = east entry of row i-1
+        case 4: a = __ldg(f + i); break;
+        case 5: a = __ldg(f + n + i); break;
+        case 7: a = __ldg(f + 2 * n + i); break;
+        default: a = 0.0;
+    }
+    if (MODE == FM_A) return a;
+    // add_matrices(mu_k, M, 1.0, A_ref.scaled(tau_ref)) entry (schur.py:41-47, linalg.py:118-127)
+    return __ldg(S.mu + s) * __ldg(S.mass + k) + 1.0 * (S.tau * a);
+}
+
+template <int MODE>
+__device__ __forceinline__ bool structural(int k) {
+    // FM_A: only S, W, C, E, N can be non-zero (SW / NE are stored zeros);
+    // FM_H: SE / NW are absent from both M and A
+    if (MODE == FM_A) return k == 1 || k == 3 || k == 4 || k == 5 || k == 7;
+    if (MODE == FM_H) return k != 2 && k != 6;
+    return true;
+}
+
+// CSR row sum at (x, y) of plane v (m x m): sum = 0; sum += a_k v_k in column order
+template <int MODE>
+__device__ __forceinline__ double frow(const Src& S, int s, const double* __restrict__ v, int m,
+                                      int x, int y) {
+    const int i = y * m + x;
+    const bool w = x > 0, e = x < m - 1, so = y > 0, no = y < m - 1;
+    const bool ok[9] = {so && w, so, so && e, w, true, e, no && w, no, no && e};
+    const int off[9] = {-m - 1, -m, -m + 1, -1, 0, 1, m - 1, m, m + 1};
+    double r = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        if (!structural<MODE>(k) || !ok[k]) continue;
+        r = r + coef<MODE>(S, s, k, m, x, y) * __ldg(v + i + off[k]);
+    }
+    return r;
+}
+
+// ---- assembly ------------------------------------------------------------------
+// Compact fields of the P1 stiffness with per-cell weights w[j][i] (both
+// triangles of cell (i, j) carry the weight; problems.py:99-138 element loop
+// with w_e K_e).  The centre is the sum of six triangle contributions in the
+// order scipy's coo -> csr conversion sums the duplicates (sort_indices, then
+// left to right; translation invariant, probed by tests/test_field.py); east
+// and north are two-term sums (order-free).
+__global__ void __launch_bounds__(FT)
+    k_f_assemble(int c, const double* __restrict__ w, double* __restrict__ fa) {
+    const int m = c - 1;
+    const size_t n = (size_t)m * m;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)n) return;
+    const int t = blockIdx.y;
+    const int jj = (int)(g / m), ii = (int)(g - (long long)jj * m);
+    const int i = ii + 1, j = jj + 1;
+    const double* W = w + (size_t)t * c * c;
+    auto cw = [&](int ci, int cj) { return __ldg(W + (size_t)cj * c + ci); };
+    double s = cw(i - 1, j - 1) * 0.5;
+    s = s + cw(i, j) * 0.5;
+    s = s + cw(i, j) * 0.5;
+    s = s + cw(i - 1, j) * 1.0;
+    s = s + cw(i, j - 1) * 1.0;
+    s = s + cw(i - 1, j - 1) * 0.5;
+    // entries towards the Dirichlet boundary do not exist: stored as 0
+    const double e = ii < m - 1 ? cw(i, j) * -0.5 + cw(i, j - 1) * -0.5 : 0.0;
+    const double no = jj < m - 1 ? cw(i, j) * -0.5 + cw(i - 1, j) * -0.5 : 0.0;
+    double* F = fa + (size_t)t * 3 * n;
+    F[g] = s;
+    F[n + g] = e;
+    F[2 * n + g] = no;
+}
+
+// ---- time-global operators ---------------------------------------------------------
+template <int OP>
+__global__ void __launch_bounds__(FX* FY)
+    k_f_timeop(int m, int N, int qmin, int qmax, const double* __restrict__ mass, Src A,
+               const double* __restrict__ ascale, const double* __restrict__ u,
+               const double* __restrict__ p, const double* __restrict__ f,
+               double* __restrict__ out) {
+    const int x = blockIdx.x * FX + threadIdx.x;
+    const int y = blockIdx.y * FY + threadIdx.y;
+    if (x >= m || y >= m) return;
+    const size_t n = (size_t)m * m;
+    const size_t i = (size_t)y * m + x;
+    const int n0 = blockIdx.z * FG;
+    const int n1 = min(N, n0 + FG);
+    double cm[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cm[k] = __ldg(mass + k);
+    auto Mv = [&](const double* v, long long t) { return stencil9_global(cm, v + t * (long long)n, m, x, y); };
+    auto Av = [&](const double* v, int t) {
+        return __ldg(ascale + t) * frow<FM_A>(A, t, v + (size_t)t * n, m, x, y);
+    };
+    if (OP == OP_ABD) {
+        for (int t = n0; t < n1; ++t) out[t * n + i] = Av(u, t);
+        return;
+    }
+    if (OP == OP_R1) {
+        double mprev = (n0 - 1 >= qmin) ? Mv(u, n0 - 1) : 0.0;
+        for (int t = n0; t < n1; ++t) {
+            const double mcur = Mv(u, t);
+            const double ku = (t - 1 >= qmin) ? mcur - mprev : mcur;
+            out[t * n + i] = (ku - Av(p, t)) - __ldg(f + t * n + i);
+            mprev = mcur;
+        }
+        return;
+    }
+    // OP_Z
+    double muprev = (n0 - 1 >= qmin) ? Mv(u, n0 - 1) : 0.0;
+    double mucur = Mv(u, n0), mpcur = Mv(p, n0);
+    for (int t = n0; t < n1; ++t) {
+        const bool hn = t + 1 <= qmax;
+        const double munext = hn ? Mv(u, t + 1) : 0.0;
+        const double mpnext = hn ? Mv(p, t + 1) : 0.0;
+        const double ktp = hn ? mpcur - mpnext : mpcur;
+        const double ku = (t - 1 >= qmin) ? mucur - muprev : mucur;
+        const double ktu = hn ? mucur - munext : mucur;
+        out[t * n + i] = (__ldg(f + t * n + i) - ktp) - ((ku + ktu) + Av(u, t));
+        muprev = mucur;
+        mucur = munext;
+        mpcur = mpnext;
+    }
+}
+
+// out_t = A_set(t) in_t over `count` planes
+template <int MODE>
+__global__ void __launch_bounds__(FX* FY)
+    k_f_apply(int m, int count, Src A, const double* __restrict__ in, double* __restrict__ out) {
+    const int x = blockIdx.x * FX + threadIdx.x;
+    const int y = blockIdx.y * FY + threadIdx.y;
+    if (x >= m || y >= m) return;
+    const size_t n = (size_t)m * m;
+    const size_t i = (size_t)y * m + x;
+    const int n0 = blockIdx.z * FG;
+    const int n1 = min(count, n0 + FG);
+    for (int t = n0; t < n1; ++t) out[t * n + i] = frow<MODE>(A, t, in + (size_t)t * n, m, x, y);
+}
+
+// ---- multigrid -----------------------------------------------------------------------
+// x0 = dinv * b with dinv = damping / diag  (spatial.py:142, 153)
+template <int MODE>
+__global__ void __launch_bounds__(FT)
+    k_f_x0(int m, Src A, double damping, const double* __restrict__ b, double* __restrict__ x0) {
+    const size_t n = (size_t)m * m;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)n) return;
+    const int t = blockIdx.y;
+    const int y = (int)(g / m), x = (int)(g - (long long)y * m);
+    const double d = damping / coef<MODE>(A, t, 4, m, x, y);
+    x0[t * n + g] = d * __ldg(b + t * n + g);
+}
+
+// b_c = P^T (b - A x0): the nine fine residuals of each coarse point, summed
+// over ascending fine index with weights (1/4, 1/2, 1) (spatial.py:156)
+template <int MODE>
+__global__ void __launch_bounds__(FT)
+    k_f_rr(int m, int mc, Src A, const double* __restrict__ b, const double* __restrict__ x0,
+           double* __restrict__ bc) {
+    const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)nc) return;
+    const int t = blockIdx.y;
+    const int Y = (int)(g / mc), X = (int)(g - (long long)Y * mc);
+    const double* bp = b + (size_t)t * n;
+    const double* xp = x0 + (size_t)t * n;
+    const double wt[3] = {0.5, 1.0, 0.5};
+    double v = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int fy = 2 * Y + a, fx = 2 * X + q;
+            const double r = __ldg(bp + (size_t)fy * m + fx) - frow<MODE>(A, t, xp, m, fx, fy);
+            const double term = (wt[a] * wt[q]) * r;
+            v = (a == 0 && q == 0) ? term : v + term;
+        }
+    bc[t * nc + g] = v;
+}
+
+// x = x0 + P e (csr_matvec of P, ascending coarse index); on the last
+// level above the 1x1 coarsest grid e = b_c / a_c (spatial.py:149-150, 157)
+__global__ void __launch_bounds__(FT)
+    k_f_prolong(int m, int mc, const double* __restrict__ ac9, size_t ac_stride, int direct,
+                const double* __restrict__ ec, double* __restrict__ x) {
+    const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)n) return;
+    const int t = blockIdx.y;
+    const int y = (int)(g / m), xx = (int)(g - (long long)y * m);
+    const double ac = direct ? __ldg(ac9 + (size_t)t * ac_stride + 4 * nc) : 1.0;
+    int ja, jb, ia, ib;
+    double wa, wb, ua, ub;
+    if (y & 1) { ja = (y - 1) >> 1; wa = 1.0; jb = -1; wb = 0.0; }
+    else { ja = (y >> 1) - 1; wa = 0.5; jb = y >> 1; wb = 0.5; }
+    if (xx & 1) { ia = (xx - 1) >> 1; ua = 1.0; ib = -1; ub = 0.0; }
+    else { ia = (xx >> 1) - 1; ua = 0.5; ib = xx >> 1; ub = 0.5; }
+    const bool va = ja >= 0, vb = jb >= 0 && jb < mc;
+    const bool ha = ia >= 0, hb = ib >= 0 && ib < mc;
+    const double* ep = ec + (size_t)t * nc;
+    double pe = 0.0;
+    bool first = true;
+    auto add = [&](bool ok, double w, int jy, int jx) {
+        if (!ok) return;
+        double e = __ldg(ep + (size_t)jy * mc + jx);
+        if (direct) e = e / ac;
+        const double term = w * e;
+        pe = first ? term : pe + term;
+        first = false;
+    };
+    add(va && ha, wa * ua, ja, ia);
+    add(va && hb, wa * ub, ja, ib);
+    add(vb && ha, wb * ua, jb, ia);
+    add(vb && hb, wb * ub, jb, ib);
+    x[t * n + g] = x[t * n + g] + pe;
+}
+
+struct FSmooth {
+    int m;
+    const double* b;
+    const double* x;
+    double* out;
+    int epi;
+    double damping, scale;
+    const double* steps;
+    const double* rsteps;
+    const double* pin;
+    const double* aux;
+    double* part;
+};
+
+// x += dinv (b - A x)  (spatial.py:159-160) and the finest-level epilogues
+template <int MODE>
+__global__ void __launch_bounds__(FT) k_f_smooth(Src A, FSmooth P) {
+    const int m = P.m;
+    const size_t n = (size_t)m * m;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    const int t = blockIdx.y;
+    double acc = 0.0;
+    if (g < (long long)n) {
+        const int y = (int)(g / m), x = (int)(g - (long long)y * m);
+        const size_t gi = (size_t)t * n + g;
+        const double d = P.damping / coef<MODE>(A, t, 4, m, x, y);
+        const double bv = __ldg(P.b + gi);
+        const double xn = __ldg(P.x + gi) + d * (bv - frow<MODE>(A, t, P.x + (size_t)t * n, m, x, y));
+        auto divtau = [&](double v) {
+            const double r = __ldg(P.rsteps + t);
+            return r > 0.0 ? v * r : v / __ldg(P.steps + t);
+        };
+        switch (P.epi) {
+            case EPI_PLAIN: P.out[gi] = xn; break;
+            case EPI_DIV_TAU: P.out[gi] = divtau(xn); break;
+            case EPI_UZAWA_P: {
+                const double dp = divtau(xn);
+                P.out[gi] = __ldg(P.pin + gi) + dp;
+                acc = bv * dp;
+                break;
+            }
+            case EPI_DOT_TAU: acc = bv * divtau(xn); break;
+            case EPI_SCALE: P.out[gi] = P.scale * xn; break;
+            case EPI_SCALE_DOT: {
+                const double w = P.scale * xn;
+                P.out[gi] = w;
+                acc = __ldg(P.aux + gi) * w;
+                break;
+            }
+            case EPI_SCALE_DOTONLY: acc = __ldg(P.aux + gi) * (P.scale * xn); break;
+        }
+    }
+    if (P.part) {
+        const double s = block_sum<FT>(acc);
+        if (threadIdx.x == 0) P.part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+// Galerkin coarse rows C = (P^T A) P of one set, in scipy's SpGEMM order
+// (spatial.py:140 via csc/csr matmat):
+//   B[I,k] = sum over fine l ascending of A[l,k] P[l,I]      (0 + ...)
+//   C[I,J] = sum over fine k ascending of P[k,J] B[I,k]      (0 + ...)
+template <int MODE>
+__global__ void __launch_bounds__(FT)
+    k_f_galerkin(int m, int mc, Src A, double* __restrict__ out) {
+    const size_t nc = (size_t)mc * mc;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)nc) return;
+    const int s = blockIdx.y;
+    const int Y = (int)(g / mc), X = (int)(g - (long long)Y * mc);
+    const double wt[3] = {0.5, 1.0, 0.5};
+    // fine box (2X-1 .. 2X+3) x (2Y-1 .. 2Y+3)
+    double B[5][5];
+#pragma unroll
+    for (int by = 0; by < 5; ++by)
+#pragma unroll
+        for (int bx = 0; bx < 5; ++bx) B[by][bx] = 0.0;
+    // l = (2Y+a, 2X+q) ascending; contributes to k in its 3x3 neighbourhood.
+    // For each k the l's arrive in ascending order, as in the reference.
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int ly = 2 * Y + a, lx = 2 * X + q;
+            const double pl = wt[a] * wt[q];
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int k = (dy + 1) * 3 + (dx + 1);
+                    if (!structural<MODE>(k)) continue;
+                    const int ky = ly + dy, kx = lx + dx;
+                    if (ky < 0 || ky >= m || kx < 0 || kx >= m) continue;
+                    const double alk = coef<MODE>(A, s, k, m, lx, ly);
+                    B[a + dy + 1][q + dx + 1] = B[a + dy + 1][q + dx + 1] + alk * pl;
+                }
+        }
+    double* o = out + (size_t)s * 9 * nc;
+#pragma unroll
+    for (int jy = -1; jy <= 1; ++jy)
+#pragma unroll
+        for (int jx = -1; jx <= 1; ++jx) {
+            const int J = (jy + 1) * 3 + (jx + 1);
+            double cv = 0.0;
+            if (Y + jy >= 0 && Y + jy < mc && X + jx >= 0 && X + jx < mc) {
+                // k = (2(Y+jy)+ry, 2(X+jx)+rx), ascending; box index = 2j + r + 1
+#pragma unroll
+                for (int ry = 0; ry < 3; ++ry)
+#pragma unroll
+                    for (int rx = 0; rx < 3; ++rx) {
+                        const int by = 2 * jy + ry + 1, bx = 2 * jx + rx + 1;
+                        if (by < 0 || by > 4 || bx < 0 || bx > 4) continue;
+                        cv = cv + (wt[ry] * wt[rx]) * B[by][bx];
+                    }
+            }
+            o[(size_t)J * nc + g] = cv;
+        }
+}
+
+dim3 tile_grid(int m, int planes) {
+    return dim3((m + FX - 1) / FX, (m + FY - 1) / FY, (planes + FG - 1) / FG);
+}
+
+dim3 pt_grid(size_t pts, int planes) {
+    return dim3((unsigned)((pts + FT - 1) / FT), (unsigned)planes);
+}
+
+bool epi_dot(int epi) {
+    return epi == EPI_UZAWA_P || epi == EPI_DOT_TAU || epi == EPI_SCALE_DOT ||
+           epi == EPI_SCALE_DOTONLY;
+}
+
+Src fine_src(pint_ctx* c, int which) {
+    Src S;
+    if (which == PINT_MG_ATILDE) {
+        S.f = c->d_fa;
+        S.set_stride = 3 * (size_t)c->n;
+    } else {
+        S.f = c->d_fref;
+        S.set_stride = 0;
+        S.mass = c->d_mass;
+        S.mu = c->fmg[which].d_mu;
+        S.tau = c->tau_ref;
+    }
+    return S;
+}
+
+Src coarse_src(const FieldMg& F, int l) {
+    Src S;
+    S.f = F.f9[l];
+    S.set_stride = 9 * (size_t)F.m[l] * F.m[l];
+    return S;
+}
+
+}  // namespace
+
+void field_assemble(pint_ctx* c, int step0, int count, const double* w_dev) {
+    const int cells = c->m + 1;
+    k_f_assemble<<<pt_grid((size_t)c->n, count), FT, 0, c->stream>>>(
+        cells, w_dev, c->d_fa + (size_t)step0 * 3 * c->n);
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_timeop_field(pint_ctx* c, int op, const double* u, const double* p, const double* f,
+                         double* out) {
+    if (op == OP_K || op == OP_KT) pint_throw(PINT_INPUT, "K / K^T have no stiffness part");
+    static const int kid[] = {K_TIMEOP_K, K_TIMEOP_KT, K_TIMEOP_ABD, K_TIMEOP_R1, K_TIMEOP_Z};
+    static const int passes[] = {2, 2, 5, 7, 7};   // + 3 compact coefficient fields
+    ProfScope prof(c, kid[op], 8.0 * passes[op] * (double)c->N * c->n);
+    Src A;
+    A.f = c->d_fa;
+    A.set_stride = 3 * (size_t)c->n;
+    const dim3 g = tile_grid(c->m, c->N), b(FX, FY);
+    const int qmin = c->has_prev ? -1 : 0, qmax = c->has_next ? c->N : c->N - 1;
+    switch (op) {
+        case OP_ABD:
+            k_f_timeop<OP_ABD><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
+                                                       c->d_ascale, u, p, f, out);
+            break;
+        case OP_R1:
+            k_f_timeop<OP_R1><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
+                                                      c->d_ascale, u, p, f, out);
+            break;
+        case OP_Z:
+            k_f_timeop<OP_Z><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
+                                                     c->d_ascale, u, p, f, out);
+            break;
+        default: pint_throw(PINT_INPUT, "unknown time operator");
+    }
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_aref_field(pint_ctx* c, const double* in, double* out, int count) {
+    if (!c->fref_ready) pint_throw(PINT_INPUT, "A_ref coefficient field not set");
+    ProfScope prof(c, K_AREF, 16.0 * (double)count * c->n);
+    Src A;
+    A.f = c->d_fref;
+    A.set_stride = 0;
+    k_f_apply<FM_A><<<tile_grid(c->m, count), dim3(FX, FY), 0, c->stream>>>(c->m, count, A, in, out);
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
+void field_galerkin(pint_ctx* c, int which) {
+    FieldMg& F = c->fmg[which];
+    for (int l = 0; l + 1 < F.levels; ++l) {
+        const int m = F.m[l], mc = F.m[l + 1];
+        const dim3 g = pt_grid((size_t)mc * mc, c->N);
+        if (l == 0) {
+            const Src S = fine_src(c, which);
+            if (which == PINT_MG_ATILDE)
+                k_f_galerkin<FM_A><<<g, FT, 0, c->stream>>>(m, mc, S, F.f9[1]);
+            else
+                k_f_galerkin<FM_H><<<g, FT, 0, c->stream>>>(m, mc, S, F.f9[1]);
+        } else {
+            k_f_galerkin<FM_9><<<g, FT, 0, c->stream>>>(m, mc, coarse_src(F, l), F.f9[l + 1]);
+        }
+        PINT_LAUNCHED(c);
+        PINT_CUDA_CHECK(cudaGetLastError());
+    }
+}
+
+namespace {
+
+template <int MODE>
+void pre_level(pint_ctx* c, const Src& S, int m, int mc, int count, double damping,
+               const double* b, double* x0, double* bc, bool fine) {
+    ProfScope prof(c, fine ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
+                   8.0 * count * (3.0 * m * m + (double)mc * mc));
+    k_f_x0<MODE><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(m, S, damping, b, x0);
+    k_f_rr<MODE><<<pt_grid((size_t)mc * mc, count), FT, 0, c->stream>>>(m, mc, S, b, x0, bc);
+    c->launches += 2;
+}
+
+template <int MODE>
+void post_level(pint_ctx* c, const Src& S, const FieldMg& F, int l, int count, const double* b,
+                double* x, double* out, int epi, double scale, const double* pin,
+                const double* aux, int acc_slot) {
+    const int m = F.m[l], mc = F.m[l + 1];
+    const bool top = l == 0;
+    const bool direct = l + 1 == F.levels - 1;
+    const double* ec = direct ? c->lev_b[l + 1] : c->lev_x[l + 1];
+    ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE,
+                   8.0 * count * (4.0 * m * m + (double)mc * mc));
+    k_f_prolong<<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(
+        m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, direct ? 1 : 0, ec, x);
+    FSmooth P{};
+    P.m = m;
+    P.b = b;
+    P.x = x;
+    P.out = out;
+    P.epi = top ? epi : EPI_PLAIN;
+    P.damping = F.damping;
+    P.scale = scale;
+    P.steps = c->d_steps;
+    P.rsteps = c->d_rsteps;
+    P.pin = pin;
+    P.aux = aux;
+    const dim3 g = pt_grid((size_t)m * m, count);
+    const bool dot = top && epi_dot(epi);
+    if (dot) {
+        ensure_partials(c, (size_t)g.x * g.y);
+        P.part = c->d_part;
+    }
+    k_f_smooth<MODE><<<g, FT, 0, c->stream>>>(S, P);
+    c->launches += 2;
+    if (dot) reduce_partials(c, (int)(g.x * g.y), acc_slot);
+}
+
+}  // namespace
+
+void vcycle_field(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
+                  double scale, const double* pin, const double* aux, int acc_slot) {
+    FieldMg& F = c->fmg[which];
+    if (!F.ready) pint_throw(PINT_INPUT, "multigrid set not configured");
+    const int L = F.levels;
+    const Src S0 = fine_src(c, which);
+    // descend: x0 = dinv b kept per level (the prolongation adds to it)
+    const double* bl = b;
+    for (int l = 0; l + 1 < L; ++l) {
+        const int m = F.m[l], mc = F.m[l + 1];
+        double* x0 = l == 0 ? c->d_ft : c->lev_t[l];
+        if (l == 0) {
+            if (which == PINT_MG_ATILDE)
+                pre_level<FM_A>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true);
+            else
+                pre_level<FM_H>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true);
+        } else {
+            pre_level<FM_9>(c, coarse_src(F, l), m, mc, count, F.damping, bl, x0, c->lev_b[l + 1],
+                            false);
+        }
+        bl = c->lev_b[l + 1];
+    }
+    PINT_CUDA_CHECK(cudaGetLastError());
+    for (int l = L - 2; l >= 0; --l) {
+        double* x = l == 0 ? c->d_ft : c->lev_t[l];
+        if (l == 0) {
+            if (which == PINT_MG_ATILDE)
+                post_level<FM_A>(c, S0, F, 0, count, b, x, out, epi, scale, pin, aux, acc_slot);
+            else
+                post_level<FM_H>(c, S0, F, 0, count, b, x, out, epi, scale, pin, aux, acc_slot);
+        } else {
+            post_level<FM_9>(c, coarse_src(F, l), F, l, count, c->lev_b[l], x, c->lev_x[l],
+                             EPI_PLAIN, 1.0, nullptr, nullptr, 0);
+        }
+    }
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace pint

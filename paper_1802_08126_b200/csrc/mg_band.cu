@@ -856,6 +856,10 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         vcycle3(c, which, count, b, out, epi, scale, pin, aux, acc_slot);
         return;
     }
+    if (c->field) {
+        vcycle_field(c, which, count, b, out, epi, scale, pin, aux, acc_slot);
+        return;
+    }
     MgSet& s = c->mg[which];
     if (!s.ready) pint_throw(PINT_INPUT, "multigrid set not configured");
     const int L = s.levels;

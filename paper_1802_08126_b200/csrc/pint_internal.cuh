@@ -54,6 +54,17 @@ struct MgSet {
     bool ready = false;
 };
 
+// field-mode (per-point coefficient) multigrid set: coarse Galerkin rows of
+// every set on every level >= 1 (field2d.cu)
+struct FieldMg {
+    int levels = 0;
+    std::vector<int> m;
+    double damping = 0.0;
+    std::vector<double*> f9;  // [l] device [N][9][m_l^2], l >= 1 (f9[0] unused)
+    double* d_mu = nullptr;   // H~: per-mode weights [N]
+    bool ready = false;
+};
+
 struct DstPlan {
     int N = 0;
     bool fast = false;        // power of two -> FFT path
@@ -111,6 +122,14 @@ struct pint_ctx {
     bool problem_ready = false;
 
     MgSet mg[2];
+    // field mode (pint_field_set / pint_field_assemble): per-point stiffness
+    bool field = false;
+    double* d_fa = nullptr;      // [N][3][n] compact fine A_n (centre, east, north)
+    double* d_fref = nullptr;    // [3][n] compact A_ref
+    bool fref_ready = false;
+    FieldMg fmg[2];
+    double* d_ft = nullptr;      // [N][n] fine-level V-cycle work slab
+    std::vector<double*> lev_t;  // coarse-level work planes
     DstPlan dst;
     DstPlan dst_raw;   // plan of the problem-free pint_dst_raw entry
 
@@ -187,6 +206,15 @@ void launch_apply3(pint_ctx* c, const double* st, const double* in, double* out,
 void launch_fold3(pint_ctx* c, const double* load, const double* u0, double* f);
 void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
              double scale, const double* pin, const double* aux, int acc_slot);
+
+// field mode, 2D per-point stiffness (field2d.cu)
+void field_assemble(pint_ctx* c, int step0, int count, const double* w_dev);
+void field_galerkin(pint_ctx* c, int which);
+void launch_timeop_field(pint_ctx* c, int op, const double* u, const double* p, const double* f,
+                         double* out);
+void launch_aref_field(pint_ctx* c, const double* in, double* out, int count);
+void vcycle_field(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
+                  double scale, const double* pin, const double* aux, int acc_slot);
 
 // sine transforms (dst.cu)
 void dst_plan_build(DstPlan& d, int N);

@@ -184,6 +184,10 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
         launch_timeop3(c, op, u, p, f, out);
         return;
     }
+    if (c->field && (op == OP_ABD || op == OP_R1 || op == OP_Z)) {
+        launch_timeop_field(c, op, u, p, f, out);
+        return;
+    }
     if ((op == OP_R1 || op == OP_Z) && band_timeop_supported(c) && !getenv("PINT_NO_BAND_TIMEOP")) {
         launch_band_timeop(c, op, u, p, f, out);
         return;
@@ -216,6 +220,10 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
 void launch_aref(pint_ctx* c, const double* in, double* out, int count) {
     if (c->dims == 3) {
         launch_apply3(c, c->d_aref, in, out, count);
+        return;
+    }
+    if (c->field) {
+        launch_aref_field(c, in, out, count);
         return;
     }
     if (band_timeop_supported(c)) {

@@ -265,3 +265,37 @@ def grid_stencil(mat, m: int) -> np.ndarray:
         except AttributeError:
             pass
     return st
+
+
+def grid_fields(mat, m: int) -> np.ndarray:
+    """Compact per-point form (3, m*m) = centre, east (i, i+1), north (i, i+m)
+    coefficients of a symmetric operator on an m x m grid whose only
+    non-zeros are the S, W, C, E, N positions (the P1 diagonal-split pattern;
+    SW / NE may hold stored zeros).  EXTENSION for the GPU field mode
+    (csrc/field2d.cu): operators that are not translation invariant.
+    Exact: raises InputError unless the lower triangle mirrors the upper
+    one bit for bit and nothing else is non-zero."""
+    csr = _csr_of(mat)
+    n = m * m
+    if csr.shape != (n, n):
+        raise DimensionMismatchError(f"operator of shape {csr.shape} is not on a {m}x{m} grid")
+    coo = csr.tocoo()
+    jr, ir = np.divmod(coo.row, m)
+    jc, ic = np.divmod(coo.col, m)
+    dy, dx = jc - jr, ic - ir
+    allowed = (np.abs(dy) + np.abs(dx)) <= 1
+    if np.any(coo.data[~allowed] != 0.0):
+        raise InputError("operator is not a 5-point-pattern P1 stiffness on the structured grid")
+    idx = np.arange(n)
+    y, x = np.divmod(idx, m)
+    out = np.zeros((3, n))
+    out[0] = csr.diagonal()
+    e_ok = x < m - 1
+    n_ok = y < m - 1
+    out[1, e_ok] = np.asarray(csr[idx[e_ok], idx[e_ok] + 1]).ravel()
+    out[2, n_ok] = np.asarray(csr[idx[n_ok], idx[n_ok] + m]).ravel()
+    west = np.asarray(csr[idx[e_ok] + 1, idx[e_ok]]).ravel()
+    south = np.asarray(csr[idx[n_ok] + m, idx[n_ok]]).ravel()
+    if np.any(west != out[1, e_ok]) or np.any(south != out[2, n_ok]):
+        raise InputError("operator is not exactly symmetric")
+    return out

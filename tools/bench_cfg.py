@@ -1,0 +1,64 @@
+"""Per-iteration timing and kernel shares for the non-headline BASELINE
+configs (c3: 3D 63^3, N=512; c5 at G=1: 3D 63^3, N=1024).  Development tool;
+bench.py remains the contract for the headline c2 line."""
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+CFG = {
+    "c3": dict(space="3d", cells=64, N=512, T=1.0),
+    "c5": dict(space="3d", cells=64, N=1024, T=1.0),
+    "c2": dict(space="2d", cells=256, N=1024, T=1.0),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3", choices=sorted(CFG))
+    ap.add_argument("--steps", type=int, default=5)
+    args = ap.parse_args()
+    import paper_1802_08126_b200 as pg
+
+    c = CFG[args.config]
+    cells, N, space = c["cells"], c["N"], c["space"]
+    n = (cells - 1) ** (3 if space == "3d" else 2)
+    rng = np.random.default_rng(0)
+    load = rng.standard_normal((N, n))
+    u0 = rng.uniform(0.0, 1.0, n) if args.config == "c3" else np.zeros(n)
+    spec = pg.problem_from_arrays(space, cells, pg.build_time_grid("uniform", N, c["T"]),
+                                  load, u0, alpha=1.0)
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy(space, cells))
+    ht = pg.build_schur_preconditioner(spec, "mg")
+    ctx = system._gp.ctx
+    f = np.ascontiguousarray(system.rhs)
+    ref = ctypes.c_double()
+    ctx.call("pint_uzawa_begin", f.ctypes.data, None, None, ctypes.byref(ref))
+    nums = np.zeros(64)
+    ms = ctypes.c_double()
+    ctx.call("pint_uzawa_run", 0.9, 3, nums.ctypes.data, ctypes.byref(ms))
+    ctx.call("pint_uzawa_run", 0.9, args.steps, nums.ctypes.data, ctypes.byref(ms))
+    ms_it = ms.value / args.steps
+    ctx.call("pint_profile", 1)
+    ctx.call("pint_uzawa_run", 0.9, 2, nums.ctypes.data, ctypes.byref(ms))
+    stats = ctx.kernel_stats()
+    ctx.call("pint_profile", 0)
+    tot = sum(v[0] for v in stats.values())
+    out = {"config": args.config, "n": n, "N": N, "ms_per_iter": ms_it,
+           "DoF_per_s": N * n / (ms_it / 1e3),
+           "iteration_alg_GBps": 224.0 * N * n / (ms_it / 1e3) / 1e9,
+           "kernels": {k: {"ms": v[0] / v[1], "share": round(v[0] / tot, 4),
+                           "GBps": round(v[2] / v[0] / 1e6, 1), "launches": v[1]}
+                       for k, v in sorted(stats.items(), key=lambda kv: -kv[1][0]) if v[1]}}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
