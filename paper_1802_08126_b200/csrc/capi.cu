@@ -821,6 +821,12 @@ int pint_uzawa_begin(pint_ctx* c, const double* f, const double* p0, const doubl
     return guarded(c, [&] {
         require_problem(c);
         require_sets(c);
+        // host staging slabs are not part of the iteration's working set:
+        // release them first (config 4 needs the room; they come back on demand)
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        dfree(c->d_stage_in);
+        dfree(c->d_stage_out);
+        c->d_stage_in = c->d_stage_out = nullptr;
         ensure_uzawa_buffers(c);
         const size_t S = slab(c), bytes = S * sizeof(double);
         const cudaMemcpyKind any = cudaMemcpyDefault;

@@ -58,20 +58,22 @@ __device__ __forceinline__ int dif_pos(int k, int lgN) {
     return ((t & 0x55555555) << 1) | ((t >> 1) & 0x55555555);
 }
 
-// in-place DIF FFT (forward, e^{-2 pi i jk/N}) of P columns of length N in smem
+// in-place DIF FFT (forward, e^{-2 pi i jk/N}) of P columns of length N in
+// smem, pair-interleaved layout buf[pos * P + pair] (a warp touches
+// consecutive double2s: no bank conflicts except on the last radix-4 stage)
 template <int P>
 __device__ __forceinline__ void fft_dif(double2* buf, int lgN, const double2* __restrict__ tw) {
+    constexpr int lgP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : 3;
     const int tid = threadIdx.x;
-    const int N = 1 << lgN;
     int lgL = lgN;
     if (lgN & 1) {
         const int lgs = lgN - 1, s = 1 << lgs;
-        for (int item = tid; item < P * s; item += DST_THREADS) {
-            const int pr = item >> lgs, j = item & (s - 1);
-            double2* p = buf + ((size_t)pr << lgN) + j;
-            const double2 a = p[0], b = p[s];
+        for (int item = tid; item < (P << lgs); item += DST_THREADS) {
+            const int pr = item & (P - 1), j = item >> lgP;
+            double2* p = buf + ((size_t)j << lgP) + pr;
+            const double2 a = p[0], b = p[(size_t)s << lgP];
             p[0] = cadd(a, b);
-            p[s] = cmul(csub(a, b), __ldg(tw + j));
+            p[(size_t)s << lgP] = cmul(csub(a, b), __ldg(tw + j));
         }
         __syncthreads();
         lgL = lgs;
@@ -82,10 +84,11 @@ __device__ __forceinline__ void fft_dif(double2* buf, int lgN, const double2* __
         const int lgstride = lgN - lgL;
 #pragma unroll 4
         for (int item = tid; item < (P << lgq); item += DST_THREADS) {
-            const int pr = item >> lgq, t = item & ((1 << lgq) - 1);
+            const int pr = item & (P - 1), t = item >> lgP;
             const int blk = t >> lgs, j = t & (s - 1);
-            double2* p = buf + ((size_t)pr << lgN) + (blk << lgL) + j;
-            const double2 x0 = p[0], x1 = p[s], x2 = p[2 * s], x3 = p[3 * s];
+            double2* p = buf + ((size_t)((blk << lgL) + j) << lgP) + pr;
+            const int sp = s << lgP;
+            const double2 x0 = p[0], x1 = p[sp], x2 = p[2 * sp], x3 = p[3 * sp];
             const double2 a0 = cadd(x0, x2), a1 = csub(x0, x2);
             const double2 b0 = cadd(x1, x3), b1 = csub(x1, x3);
             // y1 = a1 - i b1 ; y3 = a1 + i b1
@@ -95,20 +98,19 @@ __device__ __forceinline__ void fft_dif(double2* buf, int lgN, const double2* __
             const double2 y3 = make_double2(a1.x - b1.y, a1.y + b1.x);
             p[0] = y0;
             if (j == 0) {
-                p[s] = y1;
-                p[2 * s] = y2;
-                p[3 * s] = y3;
+                p[sp] = y1;
+                p[2 * sp] = y2;
+                p[3 * sp] = y3;
             } else {
                 const int js = j << lgstride;
-                p[s] = cmul(y1, __ldg(tw + js));
-                p[2 * s] = cmul(y2, __ldg(tw + 2 * js));
-                p[3 * s] = cmul(y3, __ldg(tw + 3 * js));
+                p[sp] = cmul(y1, __ldg(tw + js));
+                p[2 * sp] = cmul(y2, __ldg(tw + 2 * js));
+                p[3 * sp] = cmul(y3, __ldg(tw + 3 * js));
             }
         }
         __syncthreads();
         lgL = lgs;
     }
-    (void)N;
 }
 
 struct DstArgs {
@@ -165,25 +167,22 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
             } else {
                 pos = N - 1 - j;
             }
-            reinterpret_cast<double*>(buf + ((size_t)(cc >> 1) << lgN) + pos)[cc & 1] = x;
+            reinterpret_cast<double*>(buf + (size_t)pos * P + (cc >> 1))[cc & 1] = x;
         }
     }
     __syncthreads();
     if (KIND == 1 && a.debug < 2) {
         // Q_k = (t_k Z_k + conj(t_k') Z_k') / 2,  k' = (N - k) mod N,  t_k = e^{-i pi k / 2N}
-#pragma unroll
-        for (int pr = 0; pr < P; ++pr) {
-            double2* col = buf + ((size_t)pr << lgN);
-            for (int k = tid; k <= (N >> 1); k += DST_THREADS) {
-                const int kp = (N - k) & (N - 1);
-                const double2 zk = col[k], zp = col[kp];
-                const double2 q = __ldg(a.tq + k), qp = __ldg(a.tq + kp);
-                const double2 tk = make_double2(q.x, -q.y), tp = make_double2(qp.x, -qp.y);
-                const double2 u1 = cadd(cmul(tk, zk), cmul(qp, zp));
-                const double2 u2 = cadd(cmul(tp, zp), cmul(q, zk));
-                col[k] = make_double2(0.5 * u1.x, 0.5 * u1.y);
-                if (kp != k) col[kp] = make_double2(0.5 * u2.x, 0.5 * u2.y);
-            }
+        for (int item = tid; item < P * ((N >> 1) + 1); item += DST_THREADS) {
+            const int pr = item % P, k = item / P;
+            const int kp = (N - k) & (N - 1);
+            const double2 zk = buf[(size_t)k * P + pr], zp = buf[(size_t)kp * P + pr];
+            const double2 q = __ldg(a.tq + k), qp = __ldg(a.tq + kp);
+            const double2 tk = make_double2(q.x, -q.y), tp = make_double2(qp.x, -qp.y);
+            const double2 u1 = cadd(cmul(tk, zk), cmul(qp, zp));
+            const double2 u2 = cadd(cmul(tp, zp), cmul(q, zk));
+            buf[(size_t)k * P + pr] = make_double2(0.5 * u1.x, 0.5 * u1.y);
+            if (kp != k) buf[(size_t)kp * P + pr] = make_double2(0.5 * u2.x, 0.5 * u2.y);
         }
         __syncthreads();
     }
@@ -204,12 +203,12 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
             const int idx = base + i * DST_THREADS;
             const int j = idx >> lgW, cc = idx & (W - 1);
             if (idx >= total || cc >= ncol) continue;
-            const double2* col = buf + ((size_t)(cc >> 1) << lgN);
+            const double2* col = buf + (cc >> 1);
             double v;
             if (KIND == 0) {
                 const int mm = N - 1 - j;  // out_{N-1-m} = X_m
-                const double2 C = col[dif_pos(mm, lgN)];
-                const double2 D = col[dif_pos((N - mm) & (N - 1), lgN)];
+                const double2 C = col[(size_t)dif_pos(mm, lgN) * P];
+                const double2 D = col[(size_t)dif_pos((N - mm) & (N - 1), lgN) * P];
                 const double2 q = __ldg(a.tq + mm);
                 if ((cc & 1) == 0)
                     v = 0.5 * (q.x * (C.x + D.x) + q.y * (C.y - D.y));
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
                     v = 0.5 * (q.x * (C.y + D.y) - q.y * (C.x - D.x));
             } else {
                 const int pos = (j & 1) ? N - 1 - (j >> 1) : (j >> 1);
-                const double2 Dv = col[dif_pos(pos, lgN)];
+                const double2 Dv = col[(size_t)dif_pos(pos, lgN) * P];
                 v = (cc & 1) ? Dv.y : Dv.x;
                 if (j & 1) v = -v;
             }

@@ -525,6 +525,218 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
     }
 }
 
+// ----------------------------------------------------------------------------
+// Paired-column form of k_band_post (default): consumer thread t owns the fine
+// columns xa = 2t-1 (odd) and xb = 2t (even), t = 0..mc, which share their
+// coarse columns t-1 and t.  The band's row parity is known at compile time
+// (bands start at even rows), so the prolongation is branch-free: absent
+// coarse neighbours enter as exact zeros (0 + v == v, v + (+-0) == v), which
+// leaves every sum bit-identical to the ascending-coarse-index csr_matvec of P.
+// The smoothing window is 3 rows x 4 padded columns in registers, reading one
+// 16-byte pair plus two scalars of the padded x tile per row.
+template <int SH, int EPI, int NT, int H>
+__global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
+    __shared__ double meta[MAXSTAGE][PINT_TW + 2];
+    __shared__ double red[NT / 32 > 0 ? NT / 32 : 1];
+    static_assert(H % 2 == 0, "bands start at even rows");
+    const int m = P.m, mc = P.mc, S = P.stages;
+    const int mp = m + 3;  // even pitch: padded column c sits at index c, pairs are 16-byte aligned
+    const long long n = (long long)m * m, nc = (long long)mc * mc;
+    const int wstage = P.words_b + P.words_e + P.words_q;
+    double* sx = smem + S * wstage;  // (H+2) x mp, zero-padded columns 0 and m+1
+    const int units = P.B * P.nbands;
+    const int tid = threadIdx.x;
+    const double* qsrc0 = EPI == EPI_UZAWA_P ? P.pin : P.aux;
+    const int bob = (int)((reinterpret_cast<uintptr_t>(P.b) >> 3) & 1);
+    const int boe = (int)((reinterpret_cast<uintptr_t>(P.ec) >> 3) & 1);
+    const int boq = (int)((reinterpret_cast<uintptr_t>(qsrc0) >> 3) & 1);
+    constexpr bool HAS_Q = EPI == EPI_UZAWA_P || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
+    constexpr bool HAS_DOT =
+        EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
+    constexpr bool HAS_TAU = EPI == EPI_DIV_TAU || EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU;
+    auto sb = [&](int s) { return smem + s * wstage; };
+    auto se = [&](int s) { return smem + s * wstage + P.words_b; };
+    auto sq = [&](int s) { return smem + s * wstage + P.words_b + P.words_e; };
+    auto unit_rows = [&](int u, int& plane, int& y0, int& y1) {
+        plane = u / P.nbands;
+        const int j = u - plane * P.nbands;
+        y0 = j * H;
+        y1 = min(m, y0 + H);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    for (int i = tid; i < P.words_x; i += NT + 32) sx[i] = 0.0;
+    __syncthreads();
+    if (tid >= NT) {  // ---- producer warp (as k_band_post) ----
+        if (tid == NT) {
+            int k = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+                const int s = k % S;
+                if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
+                int plane, y0, y1;
+                unit_rows(u, plane, y0, y1);
+                const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
+                const int fb = y0 - 1, lob = max(0, fb), hib = min(m, y1 + 1);
+                const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
+                uint32_t bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
+                if (HAS_Q) bytes += band_bytes(pq, m, y0, y1);
+                const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+#pragma unroll
+                for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
+                meta[s][PINT_TW] = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
+                meta[s][PINT_TW + 1] = HAS_TAU ? __ldg(P.rsteps + plane) : 0.0;
+                mbar_expect_tx(&full[s], bytes);
+                band_issue(sb(s), P.b - bob, pb, m, fb, lob, hib, &full[s]);
+                band_issue(se(s), P.ec - boe, pc, mc, fe, loe, hie, &full[s]);
+                if (HAS_Q) band_issue(sq(s), qsrc0 - boq, pq, m, y0, y0, y1, &full[s]);
+            }
+        }
+        return;
+    }
+    const int t = tid;
+    const bool active = t <= mc;
+    const bool has_a = t >= 1 && active;   // column xa = 2t-1 exists (and coarse column t-1)
+    const bool has_cb = t < mc;            // coarse column t exists
+    const int xa = 2 * t - 1, xb = 2 * t;
+    double acc = 0.0;
+    int k = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % S;
+        int plane, y0, y1;
+        unit_rows(u, plane, y0, y1);
+        const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
+        const int fb = y0 - 1, lob = max(0, fb);
+        const int fe = y0 / 2 - 1, loe = max(0, fe);
+        const int nrow = y1 - y0;
+        mbar_wait(&full[s], (k / S) & 1);
+        double ca[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
+        const double d = meta[s][9];
+        const BandView vb = band_view(sb(s), pb, m, fb, lob);
+        const BandView ve = band_view(se(s), pc, mc, fe, loe);
+        if (active) {
+            // x = dinv*b + P e on tile rows 0 .. nrow+1 (fine rows y0-1 .. y1)
+            const double* brow = vb.p + xb;       // slot r at brow + r*m
+            const double* erow = ve.p + (t - 1);  // coarse column t-1 of slot 0
+#pragma unroll
+            for (int r = 0; r < H + 2; ++r) {
+                if (r > nrow + 1) continue;
+                const int gy = fb + r;
+                double xva = 0.0, xvb = 0.0;
+                if (gy >= 0 && gy < m) {
+                    const double* bp = brow + r * m;
+                    const double bva = has_a ? bp[-1] : 0.0;
+                    const double bvb = bp[0];
+                    double pa, pbv;
+                    if ((r & 1) == 0) {
+                        // odd fine row: one coarse row, slot r/2
+                        const double* e = erow + (r >> 1) * mc;
+                        const double e0 = has_a ? e[0] : 0.0;
+                        const double e1 = has_cb ? e[1] : 0.0;
+                        pa = (1.0 * 1.0) * e0;
+                        pbv = (1.0 * 0.5) * e0;
+                        pbv = pbv + (1.0 * 0.5) * e1;
+                    } else {
+                        // even fine row gy: coarse rows gy/2-1 (slot (r-1)/2) and gy/2 (slot (r+1)/2)
+                        const bool va = gy >= 2, vbr = (gy >> 1) < mc;
+                        const double* e = erow + ((r - 1) >> 1) * mc;
+                        const double a0 = (va && has_a) ? e[0] : 0.0;
+                        const double a1 = (va && has_cb) ? e[1] : 0.0;
+                        const double b0 = (vbr && has_a) ? e[mc] : 0.0;
+                        const double b1 = (vbr && has_cb) ? e[mc + 1] : 0.0;
+                        pa = (0.5 * 1.0) * a0;
+                        pa = pa + (0.5 * 1.0) * b0;
+                        pbv = (0.5 * 0.5) * a0;
+                        pbv = pbv + (0.5 * 0.5) * a1;
+                        pbv = pbv + (0.5 * 0.5) * b0;
+                        pbv = pbv + (0.5 * 0.5) * b1;
+                    }
+                    xva = has_a ? d * bva + pa : 0.0;
+                    xvb = d * bvb + pbv;
+                }
+                *reinterpret_cast<double2*>(sx + r * mp + 2 * t) = make_double2(xva, xvb);
+            }
+        }
+        consumer_sync<NT>();
+        const BandView vq = band_view(sq(s), pq, m, y0, y0);
+        const double tau = meta[s][PINT_TW];
+        const double rtau = meta[s][PINT_TW + 1];
+        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : v / tau; };
+        if (active) {
+            // x += dinv * (b - A x) on rows y0 .. y1-1; padded columns 2t-1 .. 2t+2
+            const double* col = sx + 2 * t;
+            auto ldrow = [&](int r, double& c0, double& c1, double& c2, double& c3) {
+                const double* q = col + r * mp;
+                c0 = t >= 1 ? q[-1] : 0.0;
+                const double2 mid = *reinterpret_cast<const double2*>(q);
+                c1 = mid.x;
+                c2 = mid.y;
+                c3 = q[2];
+            };
+            double a0, a1, a2, a3, b0, b1, b2, b3;
+            ldrow(0, a0, a1, a2, a3);
+            ldrow(1, b0, b1, b2, b3);
+            double* orow = P.out + plane * n + (long long)y0 * m + xb;
+            const double* brow = vb.p + m + xb;  // slot r+1
+            const double* qrow = vq.p + xb;
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+                if (r < nrow) {
+                    double c0, c1, c2, c3;
+                    ldrow(r + 2, c0, c1, c2, c3);
+                    const double bvb = brow[r * m];
+                    const double bva = has_a ? brow[r * m - 1] : 0.0;
+                    const double xna =
+                        b1 + d * (bva - win_sum<SH>(ca, a0, a1, a2, b0, b1, b2, c0, c1, c2));
+                    const double xnb =
+                        b2 + d * (bvb - win_sum<SH>(ca, a1, a2, a3, b1, b2, b3, c1, c2, c3));
+                    double* o = orow + (long long)r * m;
+                    auto emit = [&](double xn, double bv, int off, bool ok) {
+                        if (!ok) return;
+                        if (EPI == EPI_PLAIN) {
+                            o[off] = xn;
+                        } else if (EPI == EPI_DIV_TAU) {
+                            o[off] = divtau(xn);
+                        } else if (EPI == EPI_UZAWA_P) {
+                            const double dp = divtau(xn);
+                            o[off] = qrow[r * m + off] + dp;
+                            acc += bv * dp;
+                        } else if (EPI == EPI_DOT_TAU) {
+                            acc += bv * divtau(xn);
+                        } else if (EPI == EPI_SCALE) {
+                            o[off] = P.scale * xn;
+                        } else if (EPI == EPI_SCALE_DOT) {
+                            const double wv = P.scale * xn;
+                            o[off] = wv;
+                            acc += qrow[r * m + off] * wv;
+                        } else if (EPI == EPI_SCALE_DOTONLY) {
+                            acc += qrow[r * m + off] * (P.scale * xn);
+                        }
+                    };
+                    emit(xna, bva, -1, has_a);
+                    emit(xnb, bvb, 0, true);
+                    a0 = b0; a1 = b1; a2 = b2; a3 = b3;
+                    b0 = c0; b1 = c1; b2 = c2; b3 = c3;
+                }
+            }
+        }
+        consumer_sync<NT>();
+        if (tid == 0) mbar_arrive(&empty[s]);
+    }
+    if (HAS_DOT) {
+        const double sum = consumer_sum<NT>(acc, red);
+        if (tid == 0) P.part[blockIdx.x] = sum;
+    }
+}
+
 // ============================================================================
 // tail: levels lt..L-1 of one plane entirely in shared memory
 // ============================================================================
@@ -804,8 +1016,53 @@ static int band_rows(int m) {
     return m > 300 ? 4 : 8;
 }
 
+template <int SH, int EPI, int NT, int H>
+static void launch_post2_h(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    static bool attr = false;
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post2<SH, EPI, NT, H>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    k_band_post2<SH, EPI, NT, H><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+// consumer threads of the paired kernel: mc + 1 rounded up to warps
+static int post2_threads(int m) {
+    const int mc = (m - 1) / 2;
+    return ((mc + 1 + 31) / 32) * 32;
+}
+
+template <int SH, int EPI, int NT>
+static void launch_post2_nt(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    if (P.H == 4)
+        launch_post2_h<SH, EPI, NT, 4>(c, P, smem, grid);
+    else
+        launch_post2_h<SH, EPI, NT, 8>(c, P, smem, grid);
+}
+
+template <int SH, int EPI>
+static void launch_post2_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    switch (post2_threads(P.m)) {
+        case 32: launch_post2_nt<SH, EPI, 32>(c, P, smem, grid); break;
+        case 64: launch_post2_nt<SH, EPI, 64>(c, P, smem, grid); break;
+        case 128: launch_post2_nt<SH, EPI, 128>(c, P, smem, grid); break;
+        case 256: launch_post2_nt<SH, EPI, 256>(c, P, smem, grid); break;
+        default: pint_throw(PINT_INPUT, "unsupported grid width for the paired post kernel");
+    }
+}
+
+static bool use_post2() {
+    static const int v = getenv("PINT_POST1") ? 0 : 1;
+    return v != 0;
+}
+
 template <int SH, int EPI>
 static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+    if (use_post2()) {
+        launch_post2_epi<SH, EPI>(c, P, smem, grid);
+        return;
+    }
     if (P.m <= 128) launch_post_cfg<SH, EPI, 128, 1>(c, P, smem, grid);
     else if (P.m <= 256) launch_post_cfg<SH, EPI, 256, 1>(c, P, smem, grid);
     else if (P.m <= 512) launch_post_cfg<SH, EPI, 256, 2>(c, P, smem, grid);
@@ -981,7 +1238,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_b = band_words(P.H + 2, P.m);
         P.words_e = band_words(P.H / 2 + 2, P.mc);
         P.words_q = has_q ? band_words(P.H, P.m) : 0;
-        P.words_x = (P.H + 2) * (P.m + 2);
+        P.words_x = (P.H + 2) * (use_post2() ? P.m + 3 : P.m + 2);
         P.stages = env_int("PINT_STAGES", pick_stages(P.words_b + P.words_e + P.words_q, P.words_x));
         P.b = top ? b : c->lev_b[l];
         P.ec = c->lev_x[l + 1];
