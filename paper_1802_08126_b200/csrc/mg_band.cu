@@ -317,6 +317,155 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
     }
 }
 
+// Paired-column form of k_band_pre (default): consumer thread t computes the
+// residual of fine columns 2t-1 and 2t from a 4-column register window of
+// x0 = dinv*b (one multiply per loaded value instead of three), stores the
+// pair as one 16-byte word of the padded residual tile, and then restricts
+// coarse column t from padded columns 2t+1 .. 2t+3.
+template <int SH, int NT, int HC>
+__global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
+    __shared__ double meta[MAXSTAGE][PINT_TW];
+    constexpr int RR = 2 * HC + 1;  // residual rows per unit
+    const int m = P.m, mc = P.mc, S = P.stages;
+    const int mp = m + 3;           // padded residual pitch (even): fine x at index x+1
+    const long long n = (long long)m * m, nc = (long long)mc * mc;
+    double* sr = smem + S * P.words_b;  // RR x mp
+    const int units = P.B * P.nbands;
+    const int tid = threadIdx.x;
+    const int bob = (int)((reinterpret_cast<uintptr_t>(P.b) >> 3) & 1);
+    const double* gb = P.b - bob;
+    auto unit_rows = [&](int u, int& plane, int& Y0, int& Y1) {
+        plane = u / P.nbands;
+        const int j = u - plane * P.nbands;
+        Y0 = j * HC;
+        Y1 = min(mc, Y0 + HC);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid >= NT) {  // ---- producer warp (as k_band_pre) ----
+        if (tid == NT) {
+            int k = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+                const int s = k % S;
+                if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
+                int plane, Y0, Y1;
+                unit_rows(u, plane, Y0, Y1);
+                const long long pb = plane * n + bob;
+                const int first = 2 * Y0 - 1;
+                const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
+                const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+#pragma unroll
+                for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
+                mbar_expect_tx(&full[s], band_bytes(pb, m, lo, hi));
+                band_issue(smem + s * P.words_b, gb, pb, m, first, lo, hi, &full[s]);
+            }
+        }
+        return;
+    }
+    const int t = tid;
+    const bool active = t <= mc;
+    const bool has_a = t >= 1;          // fine column 2t-1 exists
+    const bool has_l = t >= 1;          // fine column 2t-2 exists
+    const bool has_r = t < mc;          // fine column 2t+1 exists
+    int k = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % S;
+        int plane, Y0, Y1;
+        unit_rows(u, plane, Y0, Y1);
+        const long long pb = plane * n + bob;
+        const int first = 2 * Y0 - 1;
+        const int lo = max(0, first);
+        const int nr = 2 * (Y1 - Y0) + 1;
+        mbar_wait(&full[s], (k / S) & 1);
+        double ca[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
+        const double d = meta[s][9];
+        const BandView vb = band_view(smem + s * P.words_b, pb, m, first, lo);
+        if (active) {
+            // window columns: 0 = 2t-2, 1 = 2t-1 (xa), 2 = 2t (xb), 3 = 2t+1
+            const double* bcol = vb.p + 2 * t;
+            auto ld = [&](int slot, double& w0, double& w1, double& w2, double& w3, double& ra,
+                          double& rb) {
+                const int gy = first + slot;
+                const bool in = gy >= 0 && gy < m;
+                const double* row = bcol + slot * m;
+                ra = (in && has_a) ? row[-1] : 0.0;
+                rb = in ? row[0] : 0.0;
+                w0 = (in && has_l) ? d * row[-2] : 0.0;
+                w1 = d * ra;
+                w2 = d * rb;
+                w3 = (in && has_r) ? d * row[1] : 0.0;
+            };
+            double a0, a1, a2, a3, b0, b1, b2, b3, bra, brb, dummy0, dummy1;
+            ld(0, a0, a1, a2, a3, dummy0, dummy1);
+            ld(1, b0, b1, b2, b3, bra, brb);
+            double* out = sr + 2 * t;  // padded columns 2t, 2t+1 = fine 2t-1, 2t
+#pragma unroll
+            for (int rho = 0; rho < RR; ++rho) {
+                if (rho < nr) {
+                    double c0, c1, c2, c3, cra, crb;
+                    ld(rho + 2, c0, c1, c2, c3, cra, crb);
+                    const double ra = has_a ? bra - win_sum<SH>(ca, a0, a1, a2, b0, b1, b2, c0, c1, c2)
+                                            : 0.0;
+                    const double rb = brb - win_sum<SH>(ca, a1, a2, a3, b1, b2, b3, c1, c2, c3);
+                    *reinterpret_cast<double2*>(out + rho * mp) = make_double2(ra, rb);
+                    a0 = b0; a1 = b1; a2 = b2; a3 = b3;
+                    b0 = c0; b1 = c1; b2 = c2; b3 = c3;
+                    bra = cra;
+                    brb = crb;
+                }
+            }
+        }
+        consumer_sync<NT>();
+        if (tid == 0) mbar_arrive(&empty[s]);  // stage s fully consumed
+        // restriction: P^T r, ascending fine index (csc_matvec order);
+        // coarse X = t reads fine columns 2X .. 2X+2 = padded 2X+1 .. 2X+3
+        const int ncr = Y1 - Y0;
+        if (t < mc) {
+            const double* col = sr + 2 * t;
+            auto ld3 = [&](int row, double& v0, double& v1, double& v2) {
+                const double* q = col + row * mp;
+                v0 = q[1];
+                const double2 pr = *reinterpret_cast<const double2*>(q + 2);
+                v1 = pr.x;
+                v2 = pr.y;
+            };
+            double p0, p1, p2;
+            ld3(0, p0, p1, p2);
+            double* outc = P.bc + plane * nc + (long long)Y0 * mc + t;
+#pragma unroll
+            for (int r = 0; r < HC; ++r) {
+                if (r < ncr) {
+                    double q0, q1, q2, t0, t1, t2;
+                    ld3(2 * r + 1, q0, q1, q2);
+                    ld3(2 * r + 2, t0, t1, t2);
+                    double v = 0.25 * p0;
+                    v = v + 0.5 * p1;
+                    v = v + 0.25 * p2;
+                    v = v + 0.5 * q0;
+                    v = v + 1.0 * q1;
+                    v = v + 0.5 * q2;
+                    v = v + 0.25 * t0;
+                    v = v + 0.5 * t1;
+                    v = v + 0.25 * t2;
+                    outc[(long long)r * mc] = v;
+                    p0 = t0; p1 = t1; p2 = t2;
+                }
+            }
+        }
+        consumer_sync<NT>();
+    }
+}
+
 // ============================================================================
 // prolongation + post-smoothing (+ finest-level epilogue), level (mc -> m)
 // ============================================================================
@@ -963,27 +1112,85 @@ void mg_compute_shapes(MgSet& set, const double* tab) {
     }
 }
 
+// tuning overrides (diagnostic sweeps only): PINT_STAGES, PINT_BAND, PINT_CTAS
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+// persistent grid: as many CTAs as are co-resident (registers and shared
+// memory of this instantiation), never more than `cap`
+template <typename K>
+static int occupancy_grid(K kernel, int threads, size_t smem, int cap) {
+    int occ = 0;
+    PINT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+    occ = std::max(occ, 1);
+    const int lim = env_int("PINT_CTAS", 0);
+    if (lim > 0) occ = std::min(occ, lim);
+    return std::max(1, std::min(cap, num_sms() * occ));
+}
+
 template <int SH, int NT, int CPT, int HC>
-static void launch_pre_h(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+static void launch_pre_h(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
         PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre<SH, NT, CPT, HC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
+    grid = occupancy_grid(k_band_pre<SH, NT, CPT, HC>, NT + 32, smem, grid);
     k_band_pre<SH, NT, CPT, HC><<<grid, NT + 32, smem, c->stream>>>(P);
 }
 
 template <int SH, int NT, int CPT>
-static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
     if (P.Hc == 2)
         launch_pre_h<SH, NT, CPT, 2>(c, P, smem, grid);
     else
         launch_pre_h<SH, NT, CPT, 4>(c, P, smem, grid);
 }
 
+template <int SH, int NT, int HC>
+static void launch_pre2_h(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+    static bool attr = false;
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre2<SH, NT, HC>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    grid = occupancy_grid(k_band_pre2<SH, NT, HC>, NT + 32, smem, grid);
+    k_band_pre2<SH, NT, HC><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int NT>
+static void launch_pre2_nt(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+    if (P.Hc == 2)
+        launch_pre2_h<SH, NT, 2>(c, P, smem, grid);
+    else
+        launch_pre2_h<SH, NT, 4>(c, P, smem, grid);
+}
+
+static int pair_threads(int m) {
+    const int mc = (m - 1) / 2;
+    return ((mc + 1 + 31) / 32) * 32;
+}
+
+static bool use_pre2() {
+    static const int v = getenv("PINT_PRE1") ? 0 : 1;
+    return v != 0;
+}
+
 template <int SH>
-static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid) {
+static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+    if (use_pre2()) {
+        switch (pair_threads(P.m)) {
+            case 32: launch_pre2_nt<SH, 32>(c, P, smem, grid); return;
+            case 64: launch_pre2_nt<SH, 64>(c, P, smem, grid); return;
+            case 128: launch_pre2_nt<SH, 128>(c, P, smem, grid); return;
+            case 256: launch_pre2_nt<SH, 256>(c, P, smem, grid); return;
+            default: pint_throw(PINT_INPUT, "unsupported grid width for the paired pre kernel");
+        }
+    }
     if (P.m <= 128) launch_pre_cfg<SH, 128, 1>(c, P, smem, grid);
     else if (P.m <= 256) launch_pre_cfg<SH, 256, 1>(c, P, smem, grid);
     else if (P.m <= 512) launch_pre_cfg<SH, 256, 2>(c, P, smem, grid);
@@ -991,18 +1198,19 @@ static void launch_pre_sh(pint_ctx* c, const PreParams& P, size_t smem, int grid
 }
 
 template <int SH, int EPI, int NT, int CPT, int H>
-static void launch_post_h(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post_h(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
         PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post<SH, EPI, NT, CPT, H>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
+    grid = occupancy_grid(k_band_post<SH, EPI, NT, CPT, H>, NT + 32, smem, grid);
     k_band_post<SH, EPI, NT, CPT, H><<<grid, NT + 32, smem, c->stream>>>(P);
 }
 
 template <int SH, int EPI, int NT, int CPT>
-static void launch_post_cfg(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post_cfg(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     if (P.H == 4)
         launch_post_h<SH, EPI, NT, CPT, 4>(c, P, smem, grid);
     else
@@ -1017,13 +1225,14 @@ static int band_rows(int m) {
 }
 
 template <int SH, int EPI, int NT, int H>
-static void launch_post2_h(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post2_h(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
         PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post2<SH, EPI, NT, H>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
+    grid = occupancy_grid(k_band_post2<SH, EPI, NT, H>, NT + 32, smem, grid);
     k_band_post2<SH, EPI, NT, H><<<grid, NT + 32, smem, c->stream>>>(P);
 }
 
@@ -1034,7 +1243,7 @@ static int post2_threads(int m) {
 }
 
 template <int SH, int EPI, int NT>
-static void launch_post2_nt(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post2_nt(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     if (P.H == 4)
         launch_post2_h<SH, EPI, NT, 4>(c, P, smem, grid);
     else
@@ -1042,7 +1251,7 @@ static void launch_post2_nt(pint_ctx* c, const PostBandParams& P, size_t smem, i
 }
 
 template <int SH, int EPI>
-static void launch_post2_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post2_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     switch (post2_threads(P.m)) {
         case 32: launch_post2_nt<SH, EPI, 32>(c, P, smem, grid); break;
         case 64: launch_post2_nt<SH, EPI, 64>(c, P, smem, grid); break;
@@ -1058,7 +1267,7 @@ static bool use_post2() {
 }
 
 template <int SH, int EPI>
-static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     if (use_post2()) {
         launch_post2_epi<SH, EPI>(c, P, smem, grid);
         return;
@@ -1070,7 +1279,7 @@ static void launch_post_epi(pint_ctx* c, const PostBandParams& P, size_t smem, i
 }
 
 template <int SH>
-static void launch_post_sh(pint_ctx* c, const PostBandParams& P, size_t smem, int grid) {
+static void launch_post_sh(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     switch (P.epi) {
         case EPI_PLAIN: launch_post_epi<SH, EPI_PLAIN>(c, P, smem, grid); break;
         case EPI_DIV_TAU: launch_post_epi<SH, EPI_DIV_TAU>(c, P, smem, grid); break;
@@ -1091,11 +1300,6 @@ static int pick_stages(int words_stage, int words_work) {
     return 2;
 }
 
-// tuning overrides (diagnostic sweeps only): PINT_STAGES, PINT_BAND, PINT_CTAS
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 
 static int blocks_per_sm(size_t smem) {
     const size_t per_sm = 227 * 1024;
@@ -1135,7 +1339,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.Hc = band_rows(P.m) / 2;  // coarse rows per unit
         P.nbands = (P.mc + P.Hc - 1) / P.Hc;
         P.words_b = band_words(2 * P.Hc + 3, P.m);
-        P.words_r = ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
+        P.words_r = use_pre2() ? (2 * P.Hc + 1) * (P.m + 3) : ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
         P.stages = env_int("PINT_STAGES", pick_stages(P.words_b, P.words_r));
         P.b = bl;
         P.bc = c->lev_b[l + 1];
@@ -1143,7 +1347,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.sid = s.sid;
         const size_t smem = sizeof(double) * (P.stages * P.words_b + P.words_r);
         const int units = P.B * P.nbands;
-        const int grid = std::min(units, sms * blocks_per_sm(smem));
+        int grid = std::min(units, sms * 8);
         ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
                        8.0 * count * ((double)P.m * P.m + (double)P.mc * P.mc));
         switch (s.shape[l]) {
@@ -1253,7 +1457,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         const size_t smem =
             sizeof(double) * (P.stages * (P.words_b + P.words_e + P.words_q) + P.words_x);
         const int units = P.B * P.nbands;
-        const int grid = std::min(units, sms * blocks_per_sm(smem));
+        int grid = std::min(units, sms * 8);
         const bool dl = top && dot;
         if (dl) {
             ensure_partials(c, grid);

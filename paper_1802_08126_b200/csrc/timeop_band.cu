@@ -279,6 +279,203 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
     }
 }
 
+// Paired-column form (default): consumer thread t owns columns 2t and 2t+1,
+// sharing a 4-column register window of u and p (2 loads per point instead
+// of 3) and interleaving two independent CSR-order sums.
+template <int OP, int NT, int H, int SHM, int SHA, int ONEA>
+__global__ void __launch_bounds__(NT + 32) k_band_timeop2(TopParams P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) uint64_t full[TB_MAXSTAGE], empty[TB_MAXSTAGE];
+    __shared__ double meta[TB_MAXSTAGE][10];
+    const int m = P.m, N = P.N, S = P.stages;
+    const long long n = (long long)m * m;
+    const int units = P.nbands * P.nchunks;
+    const int tid = threadIdx.x;
+    const int bou = (int)((reinterpret_cast<uintptr_t>(P.u) >> 3) & 1);
+    const int bop = (int)((reinterpret_cast<uintptr_t>(P.p) >> 3) & 1);
+    const int bof = (int)((reinterpret_cast<uintptr_t>(P.f) >> 3) & 1);
+    auto unit = [&](int u, int& y0, int& y1, int& n0, int& n1) {
+        const int c = u / P.nbands, j = u - c * P.nbands;
+        y0 = j * H;
+        y1 = min(m, y0 + H);
+        n0 = c * P.G;
+        n1 = min(N, n0 + P.G);
+    };
+    auto qrange = [&](int n0, int n1, int& qs, int& qe) {
+        qs = max(P.qmin, n0 - 1);
+        qe = OP == 0 ? n1 : min(P.qmax + 1, n1 + 1);
+    };
+    const int wst = 2 * P.words + P.wordsf;
+    auto ustage = [&](int s) { return smem + s * wst; };
+    auto pstage = [&](int s) { return smem + s * wst + P.words; };
+    auto fstage = [&](int s) { return smem + s * wst + 2 * P.words; };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid >= NT) {  // ---- producer warp (as k_band_timeop) ----
+        if (tid == NT) {
+            int k = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int y0, y1, n0, n1, qs, qe;
+                unit(u, y0, y1, n0, n1);
+                qrange(n0, n1, qs, qe);
+                const int first = y0 - 1, lo = max(0, first), hi = min(m, y1 + 1);
+                for (int q = qs; q < qe; ++q, ++k) {
+                    const int s = k % S;
+                    if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
+                    const long long pb = q * n;
+                    const Span sp = span_of(pb + bou + (long long)lo * m, pb + bou + (long long)hi * m);
+                    const Span spp = span_of(pb + bop + (long long)lo * m, pb + bop + (long long)hi * m);
+                    const bool need_p = OP == 1 || q >= n0;
+                    const int t = OP == 0 ? q : q - 1;
+                    const bool need_f = t >= n0 && t < n1;
+                    const long long tb = (long long)t * n;
+                    const uint32_t fbytes =
+                        need_f ? span_of(tb + bof + (long long)y0 * m, tb + bof + (long long)y1 * m).bytes
+                               : 0;
+                    if (!ONEA) {
+                        const double* a = P.ast + 9 * __ldg(P.asid + q);
+#pragma unroll
+                        for (int t2 = 0; t2 < 9; ++t2) meta[s][t2] = __ldg(a + t2);
+                    }
+                    meta[s][9] = __ldg(P.ascale + q);
+                    mbar_expect_tx(&full[s], sp.bytes + (need_p ? spp.bytes : 0) + fbytes);
+                    tb_issue(ustage(s), P.u - bou, pb + bou, m, first, lo, hi, &full[s]);
+                    if (need_p) tb_issue(pstage(s), P.p - bop, pb + bop, m, first, lo, hi, &full[s]);
+                    if (need_f) tb_issue(fstage(s), P.f - bof, tb + bof, m, y0, y0, y1, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+    const double* cm = P.cmass;
+    const int t0c = 2 * tid;            // columns xa = 2t, xb = 2t+1
+    const bool act = t0c < m;
+    const bool hb = t0c + 1 < m;        // column xb exists
+    const bool hl = t0c >= 1;           // column 2t-1 exists
+    const bool hr = t0c + 2 < m;        // column 2t+2 exists
+    int k = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int y0, y1, n0, n1, qs, qe;
+        unit(u, y0, y1, n0, n1);
+        qrange(n0, n1, qs, qe);
+        const int first = y0 - 1, lo = max(0, first);
+        const int nrow = y1 - y0;
+        double mu_prev[2][H], mu_cur[2][H], mp_cur[2][H], au_cur[2][H];
+        const int qlast = OP == 0 ? qe - 1 : qe;
+        for (int q = qs; q <= qlast; ++q) {
+            const bool staged = q < qe;
+            const int s = k % S;
+            const long long pb = q * n;
+            double ca[9];
+            double sc = 0.0;
+            const int t = OP == 0 ? q : q - 1;
+            const bool emit = t >= n0 && t < n1;
+            if (staged) {
+                mbar_wait(&full[s], (k / S) & 1);
+                if (!ONEA) {
+#pragma unroll
+                    for (int t2 = 0; t2 < 9; ++t2) ca[t2] = meta[s][t2];
+                }
+                sc = meta[s][9];
+            }
+            const double* A = ONEA ? P.a0 : ca;
+            if (act) {
+                const double* us = ustage(s) + tb_shift(pb + bou, m, first, lo) + t0c;
+                const double* ps = pstage(s) + tb_shift(pb + bop, m, first, lo) + t0c;
+                const double* fs = fstage(s) + tb_shift((long long)t * n + bof, m, y0, y0) + t0c;
+                // 4-wide window rows: columns 2t-1, 2t, 2t+1, 2t+2
+                auto wr4 = [&](const double* row, bool in, double* v) {
+                    v[0] = (in && hl) ? row[-1] : 0.0;
+                    v[1] = in ? row[0] : 0.0;
+                    v[2] = (in && hb) ? row[1] : 0.0;
+                    v[3] = (in && hr) ? row[2] : 0.0;
+                };
+                double ua[4], ub[4], uc[4], pa[4], pbv[4], pc[4];
+                const bool need_p = OP == 1 || q >= n0;
+                if (staged) {
+                    wr4(us, first >= 0, ua);
+                    wr4(us + m, true, ub);
+                    if (need_p) {
+                        wr4(ps, first >= 0, pa);
+                        wr4(ps + m, true, pbv);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < H; ++r) {
+                    if (r >= nrow) continue;
+                    const int gy = y0 + r;
+                    double mu[2] = {0.0, 0.0}, mp[2] = {0.0, 0.0}, au[2] = {0.0, 0.0},
+                           ap[2] = {0.0, 0.0};
+                    if (staged) {
+                        wr4(us + (r + 2) * m, gy + 1 < m, uc);
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            mu[c] = wsum<SHM>(cm, ua + c, ub + c, uc + c);
+                            if (OP == 1) au[c] = sc * wsum<SHA>(A, ua + c, ub + c, uc + c);
+                        }
+                        if (need_p) {
+                            wr4(ps + (r + 2) * m, gy + 1 < m, pc);
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                if (OP == 1) mp[c] = wsum<SHM>(cm, pa + c, pbv + c, pc + c);
+                                else ap[c] = sc * wsum<SHA>(A, pa + c, pbv + c, pc + c);
+                            }
+                        }
+                    }
+                    double* o = P.out + t * n + (long long)gy * m + t0c;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const bool ok = c == 0 || hb;
+                        if (OP == 0) {
+                            if (emit && ok) {
+                                const double ku = t - 1 >= P.qmin ? mu[c] - mu_prev[c][r] : mu[c];
+                                o[c] = (ku - ap[c]) - fs[r * m + c];
+                            }
+                            mu_prev[c][r] = mu[c];
+                        } else {
+                            if (emit && ok) {
+                                const bool has_next = t + 1 <= P.qmax;
+                                const double ktp = has_next ? mp_cur[c][r] - mp[c] : mp_cur[c][r];
+                                const double ku =
+                                    t - 1 >= P.qmin ? mu_cur[c][r] - mu_prev[c][r] : mu_cur[c][r];
+                                const double ktu = has_next ? mu_cur[c][r] - mu[c] : mu_cur[c][r];
+                                const double fval =
+                                    staged ? fs[r * m + c]
+                                           : __ldg(P.f + t * n + (long long)gy * m + t0c + c);
+                                o[c] = (fval - ktp) - ((ku + ktu) + au_cur[c][r]);
+                            }
+                            mu_prev[c][r] = mu_cur[c][r];
+                            mu_cur[c][r] = mu[c];
+                            mp_cur[c][r] = mp[c];
+                            au_cur[c][r] = au[c];
+                        }
+                    }
+                    if (staged) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            ua[i] = ub[i];
+                            ub[i] = uc[i];
+                            pa[i] = pbv[i];
+                            pbv[i] = pc[i];
+                        }
+                    }
+                }
+            }
+            if (staged) {
+                consumer_sync<NT>();
+                if (tid == 0) mbar_arrive(&empty[s]);
+                ++k;
+            }
+        }
+    }
+}
+
 // out_plane = A stencil (one stencil for all planes) * in_plane, planes [0, count)
 struct ApplyParams {
     int m, count, nbands, H, stages, words;
@@ -406,6 +603,42 @@ void launch_timeop_cfg(pint_ctx* c, const TopParams& P, size_t smem, int grid) {
         k_band_timeop<OP, CPT, H, SHM, SHA, 0><<<grid, TB_NT + 32, smem, c->stream>>>(P);
 }
 
+template <int OP, int NT, int SHM, int SHA>
+void launch_timeop2_cfg(pint_ctx* c, const TopParams& P, size_t smem, int units) {
+    constexpr int H = 4;
+    static bool attr = false;
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_timeop2<OP, NT, H, SHM, SHA, 0>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_timeop2<OP, NT, H, SHM, SHA, 1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    int occ = 0;
+    if (P.one_a) {
+        PINT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, k_band_timeop2<OP, NT, H, SHM, SHA, 1>, NT + 32, smem));
+    } else {
+        PINT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, k_band_timeop2<OP, NT, H, SHM, SHA, 0>, NT + 32, smem));
+    }
+    occ = std::max(1, occ);
+    if (const char* e = getenv("PINT_CTAS")) occ = std::max(1, std::min(occ, atoi(e)));
+    const int grid = std::max(1, std::min(units, sms_count() * occ));
+    if (P.one_a)
+        k_band_timeop2<OP, NT, H, SHM, SHA, 1><<<grid, NT + 32, smem, c->stream>>>(P);
+    else
+        k_band_timeop2<OP, NT, H, SHM, SHA, 0><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int OP, int NT>
+void launch_timeop2_shapes(pint_ctx* c, const TopParams& P, size_t smem, int units, int shm,
+                           int sha) {
+    if (shm == TS_SEVEN && sha == TS_FIVE) launch_timeop2_cfg<OP, NT, TS_SEVEN, TS_FIVE>(c, P, smem, units);
+    else if (shm == TS_SEVEN) launch_timeop2_cfg<OP, NT, TS_SEVEN, TS_FULL>(c, P, smem, units);
+    else launch_timeop2_cfg<OP, NT, TS_FULL, TS_FULL>(c, P, smem, units);
+}
+
 template <int OP, int CPT>
 void launch_timeop_shapes(pint_ctx* c, const TopParams& P, size_t smem, int grid, int shm,
                           int sha) {
@@ -464,6 +697,22 @@ void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, c
     for (int s = 0; s < c->n_a; ++s) sha = std::min(sha, shape_of(&c->h_ast[9 * s]));
     ProfScope prof(c, op == OP_R1 ? K_TIMEOP_R1 : K_TIMEOP_Z, 8.0 * 4 * (double)c->N * c->n);
     const bool wide = P.m > 256;
+    if (!getenv("PINT_TOP1")) {
+        const int units = P.nbands * P.nchunks;
+        const int nt = ((P.m + 1) / 2 + 31) / 32 * 32;   // one thread per column pair
+        if (op == OP_R1) {
+            if (nt <= 64) launch_timeop2_shapes<0, 64>(c, P, smem, units, shm, sha);
+            else if (nt <= 128) launch_timeop2_shapes<0, 128>(c, P, smem, units, shm, sha);
+            else launch_timeop2_shapes<0, 256>(c, P, smem, units, shm, sha);
+        } else {
+            if (nt <= 64) launch_timeop2_shapes<1, 64>(c, P, smem, units, shm, sha);
+            else if (nt <= 128) launch_timeop2_shapes<1, 128>(c, P, smem, units, shm, sha);
+            else launch_timeop2_shapes<1, 256>(c, P, smem, units, shm, sha);
+        }
+        PINT_LAUNCHED(c);
+        PINT_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     if (op == OP_R1) {
         if (wide) launch_timeop_shapes<0, 2>(c, P, smem, grid, shm, sha);
         else launch_timeop_shapes<0, 1>(c, P, smem, grid, shm, sha);
