@@ -20,7 +20,7 @@ from .errors import (
     SolverDivergenceError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpint.so")
+LIB_PATH = os.environ.get("PINT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpint.so")
 
 PINT_OK, PINT_INPUT, PINT_DIMENSION, PINT_NOT_SPD, PINT_DIVERGED, PINT_CUDA = range(6)
 MG_ATILDE, MG_HTILDE = 0, 1
