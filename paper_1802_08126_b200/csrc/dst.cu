@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "band.cuh"
 #include "pint_internal.cuh"
 
 namespace pint {
@@ -227,6 +228,416 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-radix transform (N = 2^LG, 8 <= LG <= 13): the same S / S^T
+// algebra as k_dst_fft, restructured so the tile crosses shared memory only
+// between radix passes.  ncu on k_dst_fft (profiles/r1_v2_ncu_dst.txt) showed
+// it L1/shared-pipe bound (L1 80 %, DRAM 24 %): ~14 shared-memory sweeps of the
+// tile per transform.  Here:
+//   pass 1  (radix 16, length N): global -> registers (Makhoul permutation /
+//           Hermitian pre-twiddle applied on the fly) -> DFT-16 -> twiddle -> smem
+//   middle  (radix 16/8/4): smem -> registers -> DFT -> twiddle -> smem (in place)
+//   final   (radix 4, length 4): smem -> registers -> DFT-4 -> post-processing
+//           (spectrum split / inverse permutation, alpha, base) -> global
+// i.e. 1 + 2*(middle passes) + 1 shared-memory sweeps (4 for N = 1024).
+// Digit-reversed order is never materialised: the final pass maps its group
+// index to the frequency base by a mixed-radix digit reversal.  S^T needs the
+// spectra at k and N-k together; one final-pass work unit owns both partner
+// groups so the split happens in registers.
+// Shared layout: double2 buf[pos * P + pair].  Every per-thread access set is
+// an arithmetic progression in pos, so all shared/global offsets are
+// compile-time multiples of one per-thread base address.
+// ---------------------------------------------------------------------------
+
+__host__ __device__ constexpr int dst_reg_pairs(int lg) { return lg >= 12 ? 1 : 4096 >> lg; }
+
+namespace dstreg {
+
+constexpr int T = 256;
+
+__device__ __forceinline__ constexpr int swz(int pos) { return pos; }
+
+// e^{-2 pi i k / 16}
+template <int K>
+__device__ __forceinline__ double2 w16(double2 a) {
+    constexpr int k = K & 15;
+    constexpr double C = 0.92387953251128673848, S = 0.38268343236508978178,
+                     Q = 0.70710678118654752440;
+    if constexpr (k == 0) return a;
+    else if constexpr (k == 4) return make_double2(a.y, -a.x);
+    else if constexpr (k == 8) return make_double2(-a.x, -a.y);
+    else if constexpr (k == 12) return make_double2(-a.y, a.x);
+    else if constexpr (k == 2) return make_double2(Q * (a.x + a.y), Q * (a.y - a.x));
+    else if constexpr (k == 6) return make_double2(Q * (a.y - a.x), -Q * (a.x + a.y));
+    else if constexpr (k == 10) return make_double2(-Q * (a.x + a.y), Q * (a.x - a.y));
+    else if constexpr (k == 14) return make_double2(Q * (a.x - a.y), Q * (a.x + a.y));
+    else {
+        constexpr double cs[16][2] = {{1, 0}, {C, -S}, {Q, -Q}, {S, -C}, {0, -1}, {-S, -C},
+                                      {-Q, -Q}, {-C, -S}, {-1, 0}, {-C, S}, {-Q, Q},
+                                      {-S, C}, {0, 1}, {S, C}, {Q, Q}, {C, S}};
+        return make_double2(cs[k][0] * a.x - cs[k][1] * a.y, cs[k][0] * a.y + cs[k][1] * a.x);
+    }
+}
+
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+    const double2 a0 = cadd(x0, x2), a1 = csub(x0, x2);
+    const double2 b0 = cadd(x1, x3), b1 = csub(x1, x3);
+    x0 = cadd(a0, b0);
+    x2 = csub(a0, b0);
+    x1 = make_double2(a1.x + b1.y, a1.y - b1.x);
+    x3 = make_double2(a1.x - b1.y, a1.y + b1.x);
+}
+
+// in-register forward DFT of R = 4, 8 or 16 points, natural order in and out
+template <int R>
+__device__ __forceinline__ void dft(double2* x) {
+    if constexpr (R == 4) {
+        dft4(x[0], x[1], x[2], x[3]);
+    } else if constexpr (R == 8) {
+        // n = q + 2 n1 (q < 2, n1 < 4), k = t + 4 u
+        double2 a[8];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double2 y0 = x[q], y1 = x[q + 2], y2 = x[q + 4], y3 = x[q + 6];
+            dft4(y0, y1, y2, y3);
+            a[q * 4 + 0] = y0;
+            a[q * 4 + 1] = y1;
+            a[q * 4 + 2] = y2;
+            a[q * 4 + 3] = y3;
+        }
+        // twiddle W8^{q t} = W16^{2 q t}
+        a[5] = w16<2>(a[5]);
+        a[6] = w16<4>(a[6]);
+        a[7] = w16<6>(a[7]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const double2 p = a[t], r = a[4 + t];
+            x[t] = cadd(p, r);
+            x[t + 4] = csub(p, r);
+        }
+    } else {
+        // n = q + 4 n1, k = t + 4 u:  X[t + 4u] = sum_q W4^{qu} W16^{qt} sum_n1 x[q + 4 n1] W4^{n1 t}
+        double2 a[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double2 y0 = x[q], y1 = x[q + 4], y2 = x[q + 8], y3 = x[q + 12];
+            dft4(y0, y1, y2, y3);
+            a[q * 4 + 0] = y0;
+            a[q * 4 + 1] = y1;
+            a[q * 4 + 2] = y2;
+            a[q * 4 + 3] = y3;
+        }
+        a[5] = w16<1>(a[5]);
+        a[6] = w16<2>(a[6]);
+        a[7] = w16<3>(a[7]);
+        a[9] = w16<2>(a[9]);
+        a[10] = w16<4>(a[10]);
+        a[11] = w16<6>(a[11]);
+        a[13] = w16<3>(a[13]);
+        a[14] = w16<6>(a[14]);
+        a[15] = w16<9>(a[15]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            double2 y0 = a[t], y1 = a[4 + t], y2 = a[8 + t], y3 = a[12 + t];
+            dft4(y0, y1, y2, y3);
+            x[t] = y0;
+            x[t + 4] = y1;
+            x[t + 8] = y2;
+            x[t + 12] = y3;
+        }
+    }
+}
+
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
+// radix schedule: pass 1 radix 16, final radix 4, middle passes in between
+//   2^8: 16.4.4  2^9: 16.8.4  2^10: 16.16.4  2^11: 16.8.4.4  2^12: 16.16.4.4  2^13: 16.16.8.4
+__host__ __device__ constexpr int sched_np(int lg) { return lg <= 10 ? 3 : 4; }
+__host__ __device__ constexpr int sched_r(int lg, int i) {
+    return i == 0 ? 16
+         : i == sched_np(lg) - 1 ? 4
+         : lg == 8 ? 4 : lg == 9 ? 8 : lg == 10 ? 16 : lg == 11 ? (i == 1 ? 8 : 4)
+         : lg == 12 ? (i == 1 ? 16 : 4) : (i == 1 ? 16 : 8);
+}
+template <int LG>
+struct Sched {
+    static constexpr int np = sched_np(LG);
+    static constexpr int r1 = sched_r(LG, 1), r2 = sched_r(LG, 2);
+};
+
+// frequency base r (k mod N/4) of final-pass group g: mixed-radix digit reversal
+template <int LG>
+__device__ __forceinline__ int group_freq(int g) {
+    using S = Sched<LG>;
+    int r = 0, mul = 1, rem = 1 << (LG - 2);
+#pragma unroll
+    for (int i = 0; i + 1 < S::np; ++i) {
+        const int ri = sched_r(LG, i);
+        rem >>= ilog2(ri);
+        const int d = (g / rem) & (ri - 1);
+        r += d * mul;
+        mul *= ri;
+    }
+    return r;
+}
+template <int LG>
+__device__ __forceinline__ int freq_group(int r) {
+    using S = Sched<LG>;
+    int g = 0, rem = 1 << (LG - 2);
+#pragma unroll
+    for (int i = 0; i + 1 < S::np; ++i) {
+        const int ri = sched_r(LG, i);
+        rem >>= ilog2(ri);
+        g += (r & (ri - 1)) * rem;
+        r >>= ilog2(ri);
+    }
+    return g;
+}
+
+// middle pass: radix R on sub-blocks of length 2^LGL, in place in smem
+template <int R, int LGL, int LG, int P, int NT>
+__device__ __forceinline__ void mid_pass(double2* buf, const double2* __restrict__ tw) {
+    constexpr int lgR = ilog2(R), lgP = ilog2(P);
+    constexpr int items = P << (LG - lgR);
+    constexpr int lgB = LGL - lgR;  // butterflies per sub-block
+#pragma unroll 1
+    for (int item = threadIdx.x; item < items; item += NT) {
+        const int pr = item & (P - 1), t = item >> lgP;
+        const int blk = t >> lgB, j = t & ((1 << lgB) - 1);
+        double2* p = buf + ((((blk << LGL) + j) << lgP) + pr);
+        double2 x[R];
+#pragma unroll
+        for (int s = 0; s < R; ++s) x[s] = p[(s << lgB) << lgP];
+        dft<R>(x);
+        p[0] = x[0];
+        if (j == 0) {
+#pragma unroll
+            for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = x[s];
+        } else {
+            const double2* w = tw + (j << (LG - LGL));
+            const int dw = j << (LG - LGL);
+#pragma unroll
+            for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + (s - 1) * dw));
+        }
+    }
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// threads per CTA: pass 1 has exactly one radix-16 butterfly per thread
+template <int LG, int P>
+__host__ __device__ constexpr int reg_threads() {
+    return P << (LG - 4);
+}
+
+template <int KIND, int LG, int P>
+__global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 512 ? 1 : 512 / reg_threads<LG, P>())
+    k_dst_reg(DstArgs a) {
+    extern __shared__ double2 buf[];
+    using S = Sched<LG>;
+    constexpr int NT = reg_threads<LG, P>();
+    constexpr int N = 1 << LG, W = 2 * P, lgP = ilog2(P), lgW = lgP + 1;
+    static_assert((P << (LG - 4)) == NT, "one pass-1 butterfly per thread");
+    const int n = a.n, tid = threadIdx.x;
+    const long long c0 = (long long)blockIdx.x * W;
+    const int ncol = (int)min((long long)W, (long long)n - c0);
+    double* sd = reinterpret_cast<double*>(buf);
+    // ---- stage: coalesced row segments -> smem (pass-1 input order) ----
+    // KIND 0: v[pos] <- u[row] with pos = row/2 (even rows), N-1-row/2 (odd rows);
+    // KIND 1: Z_k <- r[N-1-k].  Signs and in_last are applied in pass 1.
+    // A thread keeps one column and rows row0 + i*DR (DR even), so its source,
+    // position and swizzled smem offsets are all linear in i.
+    constexpr int DR = NT >> lgW;
+    static_assert(DR % 8 == 0, "row step must keep swizzle bit 2");
+    const int cc = tid & (W - 1), row0 = tid >> lgW;
+    const bool cok = cc < ncol;
+    {
+        const double* src = a.in + c0 + (cok ? (long long)row0 * n + cc : 0);
+        const long long sstep = cok ? (long long)DR * n : 0;
+        int pos0, dpos;
+        if (KIND == 0) {
+            pos0 = (row0 & 1) ? N - 1 - (row0 >> 1) : (row0 >> 1);
+            dpos = (row0 & 1) ? -(DR / 2) : DR / 2;
+        } else {
+            pos0 = N - 1 - row0;
+            dpos = -DR;
+        }
+        double* dst = sd + ((swz(pos0) << lgP) + (cc >> 1)) * 2 + (cc & 1);
+        const int dstep = (dpos << lgP) * 2;
+#pragma unroll 16
+        for (int i = 0; i < N / DR; ++i) {
+            cp_async8(dst, src, cok);
+            src += sstep;
+            dst += dstep;
+        }
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    // ---- pass 1: radix 16 over the whole column, one butterfly per thread ----
+    // thread (pr, j) owns positions j + s N/16; position < N/2 <=> s < 8
+    {
+        constexpr int lgB = LG - 4, B = 1 << lgB;
+        const int pr = tid & (P - 1), j = tid >> lgP;
+        double2* p = buf + ((j << lgP) + pr);
+        double2 x[16];
+        if (KIND == 0) {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                double2 v = p[(s << lgB) << lgP];
+                if (s == 8 && j == 0) v = make_double2(v.x * a.in_last, v.y * a.in_last);
+                x[s] = s < 8 ? v : make_double2(-v.x, -v.y);
+            }
+        } else {
+            // Q_k = (conj(q_k) Z_k + q_{k'} Z_{k'}) / 2,  k' = (N-k) mod N:
+            // j > 0: k' = (B - j) + (15 - s) B;  j = 0: k' = (16 - s) B mod N
+            const int jp = j == 0 ? 0 : B - j;
+            const double2* pp = buf + ((jp << lgP) + pr);
+            const double2* q = a.tq + j;
+            const double2* qq = a.tq + jp;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                double2 zk = p[(s << lgB) << lgP];
+                const int sp = j == 0 ? (16 - s) & 15 : 15 - s;
+                double2 zp = pp[(sp << lgB) << lgP];
+                if (s == 0 && j == 0) {
+                    zk = make_double2(zk.x * a.in_last, zk.y * a.in_last);
+                    zp = zk;
+                }
+                const double2 qk = __ldg(q + (s << lgB)), qp = __ldg(qq + (sp << lgB));
+                const double2 u1 = cadd(cmul(make_double2(qk.x, -qk.y), zk), cmul(qp, zp));
+                x[s] = make_double2(0.5 * u1.x, 0.5 * u1.y);
+            }
+            __syncthreads();  // partners' reads before anyone overwrites
+        }
+        dft<16>(x);
+        p[0] = x[0];
+        if (j == 0) {
+#pragma unroll
+            for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = x[s];
+        } else {
+            const double2* w = a.tw + j;
+#pragma unroll
+            for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + (s - 1) * j));
+        }
+    }
+    __syncthreads();
+    // ---- middle passes ----
+    if constexpr (S::np >= 3) {
+        constexpr int L2 = LG - 4;
+        mid_pass<S::r1, L2, LG, P, NT>(buf, a.tw);
+        __syncthreads();
+        if constexpr (S::np == 4) {
+            constexpr int L3 = L2 - ilog2(S::r1);
+            mid_pass<S::r2, L3, LG, P, NT>(buf, a.tw);
+            __syncthreads();
+        }
+    }
+    // ---- final radix-4 pass: results to smem in output-row order ----
+    // (reads of every group finish before the barrier, writes after it)
+    constexpr int Q4 = N / 4;
+    auto load_group = [&](int g, int pr, double2* x) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) x[s] = buf[(swz(4 * g + s) << lgP) + pr];
+        dft4(x[0], x[1], x[2], x[3]);
+    };
+    if (KIND == 1) {
+        // D at k = r + s N/4;  out_j = (-1)^j x_j, x = inverse Makhoul permutation of (Re D | Im D)
+        constexpr int per = (P * Q4) / NT;
+        double2 x[per][4];
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            load_group(item >> lgP, item & (P - 1), x[i]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            const int pr = item & (P - 1), r = group_freq<LG>(item >> lgP);
+            // k = r + s N/4 < N/2 <=> s < 2:  rows 2k (s < 2), 2(N-1-k)+1 (s >= 2)
+            buf[((2 * r) << lgP) + pr] = x[i][0];
+            buf[((2 * (r + Q4)) << lgP) + pr] = x[i][1];
+            buf[((2 * (N - 1 - r - 2 * Q4) + 1) << lgP) + pr] = make_double2(-x[i][2].x, -x[i][2].y);
+            buf[((2 * (N - 1 - r - 3 * Q4) + 1) << lgP) + pr] = make_double2(-x[i][3].x, -x[i][3].y);
+        }
+    } else {
+        // X_m of the two real columns from C_m and C_{N-m}; out_{N-1-m} = X_m
+        constexpr int per = (P * (Q4 / 2)) / NT;
+        double2 x[per][4], y[per][4];
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            const int pr = item & (P - 1), u = item >> lgP;
+            load_group(freq_group<LG>(u == 0 ? 0 : u), pr, x[i]);
+            load_group(freq_group<LG>(u == 0 ? N / 8 : Q4 - u), pr, y[i]);
+        }
+        __syncthreads();
+        auto emit = [&](int m, int pr, double2 C, double2 D) {
+            const double2 q = __ldg(a.tq + m);
+            const double va = 0.5 * (q.x * (C.x + D.x) + q.y * (C.y - D.y));
+            const double vb = 0.5 * (q.x * (C.y + D.y) - q.y * (C.x - D.x));
+            buf[(swz(N - 1 - m) << lgP) + pr] = make_double2(va, vb);
+        };
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            const int pr = item & (P - 1), u = item >> lgP;
+            if (u == 0) {
+                // self-partnered groups r = 0 (N-k = (4-s) N/4) and r = N/8 (N-k = N/8 + (3-s) N/4)
+                emit(0, pr, x[i][0], x[i][0]);
+                emit(Q4, pr, x[i][1], x[i][3]);
+                emit(2 * Q4, pr, x[i][2], x[i][2]);
+                emit(3 * Q4, pr, x[i][3], x[i][1]);
+#pragma unroll
+                for (int s = 0; s < 4; ++s) emit(N / 8 + s * Q4, pr, y[i][s], y[i][3 - s]);
+            } else {
+                // k = r + s N/4  <->  N - k = rp + (3 - s) N/4
+                const int r = u, rp = Q4 - u;
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    emit(r + s * Q4, pr, x[i][s], y[i][3 - s]);
+                    emit(rp + s * Q4, pr, y[i][s], x[i][3 - s]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // ---- store: coalesced row segments, alpha / out_last / base ----
+    if (cok) {
+        const long long step = (long long)DR * n;
+        double* out = a.out + c0 + (long long)row0 * n + cc;
+        const double* basep = a.base ? a.base + c0 + (long long)row0 * n + cc : nullptr;
+        const double* sp = sd + ((swz(row0) << lgP) + (cc >> 1)) * 2 + (cc & 1);
+        constexpr int sstep = (DR << lgP) * 2;
+        constexpr int LB = 8;
+        const double alpha = a.alpha;
+#pragma unroll 1
+        for (int i0 = 0; i0 < N / DR; i0 += LB) {
+            double bv[LB];
+            if (basep) {
+#pragma unroll
+                for (int i = 0; i < LB; ++i) bv[i] = __ldg(basep + (i0 + i) * step);
+            }
+#pragma unroll
+            for (int i = 0; i < LB; ++i) {
+                const int row = row0 + (i0 + i) * DR;
+                double v = alpha * sp[(i0 + i) * sstep];
+                if (row == N - 1) v *= a.out_last;
+                out[(i0 + i) * step] = basep ? bv[i] + v : v;
+            }
+        }
+    }
+}
+
+}  // namespace dstreg
+
 // dense fallback (non power of two N): kernel[k][t] = sin((2k+1)(t+1) pi / 2N), 0-based
 template <int KIND>
 __global__ void __launch_bounds__(256) k_dst_dense(DstArgs a, const double* __restrict__ kern) {
@@ -304,6 +715,30 @@ void dst_plan_build(DstPlan& d, int N) {
         if ((size_t)P * N * 16 > 200 * 1024)
             pint_throw(PINT_INPUT, "time axis too long for the single-CTA sine transform");
         d.pairs = P;
+        // register-radix kernel (k_dst_reg) for 2^8 <= N <= 2^13
+        d.reg_lg = (lg >= 8 && lg <= 13 && !getenv("PINT_DST_OLD")) ? lg : 0;
+        if (d.reg_lg) {
+            d.reg_p = dst_reg_pairs(lg);
+            if (const char* e = getenv("PINT_DST_P")) {
+                const int want = atoi(e);
+                if ((lg == 10 && (want == 2 || want == 4)) || (lg == 9 && (want == 4 || want == 8)))
+                    d.reg_p = want;
+            }
+            static bool attr_done = false;
+            if (!attr_done) {
+#define PINT_REGATTR(LGV, PV)                                                                   \
+                PINT_CUDA_CHECK(cudaFuncSetAttribute(dstreg::k_dst_reg<0, LGV, PV>,              \
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                     PV * (16 << LGV)));                          \
+                PINT_CUDA_CHECK(cudaFuncSetAttribute(dstreg::k_dst_reg<1, LGV, PV>,              \
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                     PV * (16 << LGV)));
+                PINT_REGATTR(8, 16) PINT_REGATTR(9, 8) PINT_REGATTR(9, 4) PINT_REGATTR(10, 4)
+                PINT_REGATTR(10, 2) PINT_REGATTR(11, 2) PINT_REGATTR(12, 1) PINT_REGATTR(13, 1)
+#undef PINT_REGATTR
+                attr_done = true;
+            }
+        }
         // the attribute is per function, shared by every plan in the process:
         // allow the largest plan once instead of the current one
         static const int kMaxSmem = 200 * 1024;
@@ -360,7 +795,20 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
     }
     ProfScope prof(c, K == 0 ? K_DST : K_DST_T,
                    8.0 * (double)d.N * (double)ncols * (base ? 3.0 : 2.0));
-    if (d.fast) {
+    if (d.fast && d.reg_lg) {
+        const int P = d.reg_p;
+        const dim3 g((unsigned)((ncols + 2 * P - 1) / (2 * P)));
+        const size_t smem = (size_t)P * d.N * 16;
+        auto launch = [&](auto kern, int nt) { kern<<<g, nt, smem, c->stream>>>(a); };
+#define PINT_REGL(LGV, PV)                                                                       \
+    if (d.reg_lg == LGV && P == PV) {                                                            \
+        if (K == 0) launch(dstreg::k_dst_reg<0, LGV, PV>, dstreg::reg_threads<LGV, PV>());      \
+        else launch(dstreg::k_dst_reg<1, LGV, PV>, dstreg::reg_threads<LGV, PV>());             \
+    }
+        PINT_REGL(8, 16) PINT_REGL(9, 8) PINT_REGL(9, 4) PINT_REGL(10, 4) PINT_REGL(10, 2)
+        PINT_REGL(11, 2) PINT_REGL(12, 1) PINT_REGL(13, 1)
+#undef PINT_REGL
+    } else if (d.fast) {
         const int W = 2 * d.pairs;
         const dim3 g((unsigned)((ncols + W - 1) / W));
         const size_t smem = (size_t)d.pairs * d.N * 16;

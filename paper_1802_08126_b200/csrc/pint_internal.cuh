@@ -74,6 +74,8 @@ struct DstPlan {
     double* dense = nullptr;  // sin((2k-1) n pi / 2N), k-major (non power of two)
     int radix2_first = 0;
     int pairs = 0;            // column pairs per CTA
+    int reg_lg = 0;           // log2 N when the register-radix kernel runs (0: k_dst_fft)
+    int reg_p = 0;            // its column pairs per CTA
 };
 
 // kernel families timed individually in profiling mode (pint_profile)
