@@ -174,6 +174,13 @@ int pint_uzawa_begin(pint_ctx* ctx, const double* f, const double* p0, const dou
                      double* ref_out);
 int pint_uzawa_step(pint_ctx* ctx, double omega, double* res_num_out);
 int pint_uzawa_end(pint_ctx* ctx, double* p, double* u);
+/* Host output buffers (p, u of pint_uzawa_end) may be fresh pageable
+ * allocations; this starts background first-touch of their pages so the
+ * device-to-host copy later runs at copy-engine rate.  Asynchronous; the next
+ * host copy out of this context waits for it.  Device pointers are ignored.
+ * (No reference counterpart: a transfer-path detail of uzawa_solve's
+ * numpy-in/numpy-out contract, solvers.py:177-264.) */
+int pint_host_prefault(pint_ctx* ctx, void* host, long long bytes);
 int pint_uzawa(pint_ctx* ctx, const double* f, double* p, double* u, double omega,
                double tol, int max_iter, int use_initial, double* res_hist, int* iters,
                int* converged, double* phase_ms);

@@ -125,9 +125,23 @@ size_t slab(const pint_ctx* c) { return (size_t)c->N * c->n; }
 const double* stage_in(pint_ctx* c, const double* p, double* staging, size_t count) {
     if (p == nullptr) pint_throw(PINT_INPUT, "null input");
     if (is_device_ptr(p)) return p;
-    PINT_CUDA_CHECK(
-        cudaMemcpyAsync(staging, p, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    pint::copy_h2d(c, staging, p, count * sizeof(double));
     return staging;
+}
+
+// any-kind source/destination: device pointers copy on the stream, host
+// pointers go through the pinned multi-threaded staging (hostcopy.cu)
+void copy_in(pint_ctx* c, double* dev, const double* src, size_t bytes) {
+    if (is_device_ptr(src))
+        PINT_CUDA_CHECK(cudaMemcpyAsync(dev, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    else
+        pint::copy_h2d(c, dev, src, bytes);
+}
+void copy_out(pint_ctx* c, double* dst, const double* dev, size_t bytes) {
+    if (is_device_ptr(dst))
+        PINT_CUDA_CHECK(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    else
+        pint::copy_d2h(c, dst, dev, bytes);
 }
 
 struct OutBuf {
@@ -143,9 +157,7 @@ OutBuf stage_out(pint_ctx* c, double* p, double* staging) {
 }
 
 void finish_out(pint_ctx* c, const OutBuf& o, size_t count) {
-    if (o.host)
-        PINT_CUDA_CHECK(cudaMemcpyAsync(o.host, o.dev, count * sizeof(double),
-                                        cudaMemcpyDeviceToHost, c->stream));
+    if (o.host) pint::copy_d2h(c, o.host, o.dev, count * sizeof(double));
     PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     pint_prof_drain(c);
 }
@@ -325,6 +337,7 @@ int pint_ctx_destroy(pint_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->prof_pool) cudaEventDestroy(e);
+    pint::host_xfer_free(c);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return PINT_OK;
@@ -829,14 +842,13 @@ int pint_uzawa_begin(pint_ctx* c, const double* f, const double* p0, const doubl
         c->d_stage_in = c->d_stage_out = nullptr;
         ensure_uzawa_buffers(c);
         const size_t S = slab(c), bytes = S * sizeof(double);
-        const cudaMemcpyKind any = cudaMemcpyDefault;
-        PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_f, f, bytes, any, c->stream));
+        copy_in(c, c->d_f, f, bytes);
         if (p0)
-            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_p, p0, bytes, any, c->stream));
+            copy_in(c, c->d_p, p0, bytes);
         else
             PINT_CUDA_CHECK(cudaMemsetAsync(c->d_p, 0, bytes, c->stream));
         if (u0)
-            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_u, u0, bytes, any, c->stream));
+            copy_in(c, c->d_u, u0, bytes);
         else
             PINT_CUDA_CHECK(cudaMemsetAsync(c->d_u, 0, bytes, c->stream));
         // ref = sqrt(max(f.A~^-1 f + f.H~^-1 f, 0))   (solvers.py:212-217)
@@ -882,12 +894,20 @@ int pint_uzawa_step(pint_ctx* c, double omega, double* res_num_out) {
     });
 }
 
+int pint_host_prefault(pint_ctx* c, void* host, long long bytes) {
+    return guarded(c, [&] {
+        if (!host || bytes < 0) pint_throw(PINT_INPUT, "bad host buffer");
+        if (is_device_ptr(host)) return;
+        pint::host_prefault_async(c, host, (size_t)bytes);
+    });
+}
+
 int pint_uzawa_end(pint_ctx* c, double* p, double* u) {
     return guarded(c, [&] {
         if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
         const size_t bytes = slab(c) * sizeof(double);
-        if (p) PINT_CUDA_CHECK(cudaMemcpyAsync(p, c->d_p, bytes, cudaMemcpyDefault, c->stream));
-        if (u) PINT_CUDA_CHECK(cudaMemcpyAsync(u, c->d_u, bytes, cudaMemcpyDefault, c->stream));
+        if (p) copy_out(c, p, c->d_p, bytes);
+        if (u) copy_out(c, u, c->d_u, bytes);
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }

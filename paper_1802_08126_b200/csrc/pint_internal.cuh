@@ -97,12 +97,17 @@ struct ProfRec {
     cudaEvent_t a, b;
 };
 
+namespace pint {
+struct HostXfer;
+}
+
 struct pint_ctx {
     int dev = 0, rank = 0, world = 1;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;  // created by the context; `stream` may be a caller's
     std::string err;
     long long launches = 0;
+    pint::HostXfer* xfer = nullptr;  // pinned staging for host block vectors (hostcopy.cu)
 
     // problem
     int dims = 0, m = 0, n = 0, N = 0;
@@ -225,6 +230,12 @@ void dst_plan_free(DstPlan& d);
 void dst_apply(pint_ctx* c, int kind, const double* in, double* out, const double* base,
                double alpha);
 // same on an arbitrary (N, ncols) slab with plan d
+// host <-> device block-vector copies through pinned multi-threaded staging (hostcopy.cu)
+void copy_h2d(pint_ctx* c, void* dev, const void* host, size_t bytes);
+void copy_d2h(pint_ctx* c, void* host, const void* dev, size_t bytes);  // synchronous
+void host_xfer_free(pint_ctx* c);
+void host_prefault_async(pint_ctx* c, void* p, size_t bytes);
+void host_prefault_join(pint_ctx* c);
 void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const double* in,
              double* out, const double* base, double alpha);
 

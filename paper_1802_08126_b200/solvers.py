@@ -191,6 +191,10 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
         hist.converged = True
         ctx.call("pint_uzawa_end", ptr_of(p_out), ptr_of(u_out))
         return (p_out, u_out), hist
+    for arr in (p_out, u_out):
+        if isinstance(arr, np.ndarray):
+            # fault the host output pages in while the device iterates
+            ctx.call("pint_host_prefault", arr.ctypes.data, arr.nbytes)
     ctx.call("pint_set_timing", 1)
     ms = np.zeros(3)
     num = ctypes.c_double(0.0)
