@@ -83,9 +83,11 @@ int guarded(pint_ctx* c, F&& f) {
         return PINT_OK;
     } catch (const PintFail& e) {
         c->err = e.msg;
+        c->mu3_trust = false;
         return e.code;
     } catch (const std::exception& e) {
         c->err = e.what();
+        c->mu3_trust = false;
         return PINT_CUDA;
     }
 }
@@ -168,12 +170,14 @@ void require_problem(pint_ctx* c) {
 
 void free_slabs(pint_ctx* c) {
     double** s[] = {&c->d_f,  &c->d_p,        &c->d_u,         &c->d_r1,  &c->d_z,  &c->d_w1,
-                    &c->d_w2, &c->d_stage_in, &c->d_stage_out, &c->d_vec, &c->d_t3a, &c->d_t3b};
+                    &c->d_w2, &c->d_stage_in, &c->d_stage_out, &c->d_vec, &c->d_t3a, &c->d_t3b,
+                    &c->d_mu3, &c->d_mp3};
     for (double** p : s) {
         dfree(*p);
         *p = nullptr;
     }
     c->t3_cap = 0;
+    c->mu3_src = nullptr;
     for (double* p : c->lev_b) dfree(p);
     for (double* p : c->lev_x) dfree(p);
     c->lev_b.clear();
@@ -497,6 +501,14 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
         s.tab = upload(c, tables, ntab);
         s.sid = upload(c, sid, c->N);
         if (c->dims == 2) pint::mg_compute_shapes(s, tables);
+        if (c->dims == 3)
+            for (int l = 0; l < levels; ++l) {
+                uint32_t mask = 0;
+                for (int q = 0; q < n_sets; ++q)
+                    for (int k = 0; k < 27; ++k)
+                        if (tables[((size_t)l * n_sets + q) * TW + k] != 0.0) mask |= 1u << k;
+                s.shape3.push_back(mask);
+            }
         ensure_levels(c, s.m);
         s.ready = true;
     });
@@ -870,12 +882,15 @@ int pint_uzawa_step(pint_ctx* c, double omega, double* res_num_out) {
     return guarded(c, [&] {
         if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
         rec(c, 0);
+        // u is not written between the two residuals: the 3D path may reuse M u
+        c->mu3_trust = true;
         pint::launch_timeop(c, pint::OP_R1, c->d_u, c->d_p, c->d_f, c->d_r1);
         rec(c, 4);
         pint::vcycle(c, PINT_MG_ATILDE, c->N, c->d_r1, c->d_p, EPI_UZAWA_P, 1.0, c->d_p,
                      nullptr, 0);
         rec(c, 5);
         pint::launch_timeop(c, pint::OP_Z, c->d_u, c->d_p, c->d_f, c->d_z);
+        c->mu3_trust = false;
         schur_mode_space(c, c->d_z, c->d_z, EPI_SCALE_DOT, c->d_w2, 1);
         pint::dst_apply(c, 0, c->d_w2, c->d_u, c->d_u, omega);
         rec(c, 6);

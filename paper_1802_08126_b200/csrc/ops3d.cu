@@ -13,6 +13,7 @@
 // Round-1 form: thread per point, neighbours through L1/L2 (no TMA bands),
 // one launch per level and phase over every plane of the batch.
 #include <algorithm>
+#include <type_traits>
 
 #include "pint_device.cuh"
 #include "pint_internal.cuh"
@@ -325,6 +326,448 @@ __global__ void __launch_bounds__(T3) k3_smooth(Smooth3 a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// z-marching stencil engine (round-1 rewrite of the thread-per-point form).
+// A thread owns one (x, y) column of a 32 x 8 tile and a chunk of ZC
+// consecutive z; it keeps a 3-slice register window of the (dy, dx)
+// positions its stencil pattern touches, so every input value is loaded once
+// per thread instead of once per stencil term (7 loads per point for the
+// 15-point mass, 5 for the 7-point stiffness, 9 for Galerkin 27-point
+// operators).  Coefficients of the plane's operator are per-CTA registers.
+// The row sum runs over the pattern in CSR order (dz, dy, dx lexicographic)
+// with no FMA (-fmad=false); positions outside the pattern are exact zeros
+// in every table (checked on the host), so skipping them changes no value.
+// ---------------------------------------------------------------------------
+constexpr int ZX = 32, ZY = 8, ZC = 8;
+
+// x / y out of line: a select between v * (1/tau) and v / tau would otherwise
+// be if-converted and the (slow-path-prone) division evaluated for every point
+__device__ __noinline__ double div_rn(double x, double y) { return x / y; }
+
+// stencil patterns: bit k = (dz+1)*9 + (dy+1)*3 + (dx+1)
+constexpr uint32_t PAT_A7 = (1u << 4) | (1u << 10) | (1u << 12) | (1u << 13) | (1u << 14) |
+                            (1u << 16) | (1u << 22);
+// P1 mass on the Kuhn split: 0, +-x, +-y, +-z, +-(1,1,0), +-(0,1,1), +-(1,0,1), +-(1,1,1)
+constexpr uint32_t PAT_M15 = PAT_A7 | (1u << 0) | (1u << 26) | (1u << 9) | (1u << 17) |
+                             (1u << 1) | (1u << 25) | (1u << 3) | (1u << 23);
+constexpr uint32_t PAT_F27 = (1u << 27) - 1;
+
+__host__ __device__ constexpr bool pat_has(uint32_t pat, int k) { return (pat >> k) & 1u; }
+// (dy, dx) position q = (dy+1)*3 + (dx+1) needed in any z role
+__host__ __device__ constexpr bool pat_need(uint32_t pat, int q) {
+    return pat_has(pat, q) || pat_has(pat, 9 + q) || pat_has(pat, 18 + q);
+}
+
+uint32_t pattern_of(const double* st, int count) {
+    uint32_t mask = 0;
+    for (int s = 0; s < count; ++s)
+        for (int k = 0; k < 27; ++k)
+            if (st[(size_t)s * 27 + k] != 0.0) mask |= 1u << k;
+    return mask;
+}
+// smallest compiled pattern containing mask
+uint32_t pattern_pick(uint32_t mask) {
+    if ((mask & ~PAT_A7) == 0) return PAT_A7;
+    if ((mask & ~PAT_M15) == 0) return PAT_M15;
+    return PAT_F27;
+}
+
+struct ZTile {
+    int x, y, z0, zn;  // column and z range [z0, z0 + zn)
+    bool ok;
+};
+
+// blockIdx.x enumerates (tile, z chunk) of a plane; blockIdx.y the plane
+__device__ __forceinline__ ZTile ztile(int m) {
+    const int tx = (m + ZX - 1) / ZX, ty = (m + ZY - 1) / ZY;
+    int b = blockIdx.x;
+    const int xt = b % tx;
+    b /= tx;
+    const int yt = b % ty;
+    const int zc = b / ty;
+    ZTile t;
+    t.x = xt * ZX + (int)threadIdx.x;
+    t.y = yt * ZY + (int)threadIdx.y;
+    t.z0 = zc * ZC;
+    t.zn = min(ZC, m - t.z0);
+    t.ok = t.x < m && t.y < m;
+    return t;
+}
+inline dim3 zgrid(int m, int planes) {
+    const int tx = (m + ZX - 1) / ZX, ty = (m + ZY - 1) / ZY, tz = (m + ZC - 1) / ZC;
+    return dim3((unsigned)(tx * ty * tz), (unsigned)planes);
+}
+
+// per-thread neighbourhood of a column: in-domain flags of x-1, x+1, y-1,
+// y+1 and the element offsets of the 9 (dy, dx) positions inside a slice
+struct ZNbr {
+    bool xl, xr, yl, yr;
+    int off[9];
+};
+__device__ __forceinline__ ZNbr znbr(int m, int x, int y) {
+    ZNbr b;
+    b.xl = x > 0;
+    b.xr = x + 1 < m;
+    b.yl = y > 0;
+    b.yr = y + 1 < m;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) b.off[q] = (q / 3 - 1) * m + (q % 3 - 1);
+    return b;
+}
+__device__ __forceinline__ bool znbr_in(const ZNbr& b, int q) {
+    const int dy = q / 3 - 1, dx = q % 3 - 1;
+    return (dy < 0 ? b.yl : dy > 0 ? b.yr : true) && (dx < 0 ? b.xl : dx > 0 ? b.xr : true);
+}
+
+// the needed (dy, dx) values of the slice at column pointer p (zero outside
+// the domain or when !zin), times d when SCALED
+template <uint32_t PAT, bool SCALED>
+__device__ __forceinline__ void zslice(double* w, const double* p, bool zin, const ZNbr& nb,
+                                       double d) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        if (!pat_need(PAT, q)) continue;
+        const bool in = zin && znbr_in(nb, q);
+        const double v = in ? __ldg(p + nb.off[q]) : 0.0;
+        w[q] = SCALED ? (in ? d * v : 0.0) : v;
+    }
+}
+
+// row sum over the pattern in CSR order; c[k] coefficient registers
+template <uint32_t PAT>
+__device__ __forceinline__ double zsum(const double* c, const double (&w)[3][9]) {
+    double s = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int k = 0; k < 27; ++k) {
+        if (!pat_has(PAT, k)) continue;
+        const double t = c[k] * w[k / 9][k % 9];
+        s = first ? t : s + t;
+        first = false;
+    }
+    return s;
+}
+
+template <uint32_t PAT>
+__device__ __forceinline__ void zcoef(double* c, const double* __restrict__ tb) {
+#pragma unroll
+    for (int k = 0; k < 27; ++k) c[k] = pat_has(PAT, k) ? __ldg(tb + k) : 0.0;
+}
+
+// march z over the chunk: f(z, sum, centre value) for every point of the column
+template <uint32_t PAT, bool SCALED, typename F>
+__device__ __forceinline__ void zmarch(const ZTile& t, int m, const double* __restrict__ v,
+                                       const double* c, double d, F&& f) {
+    const ZNbr nb = znbr(m, t.x, t.y);
+    const long long S = (long long)m * m;
+    const double* p = v + ((long long)(t.z0 - 1) * m + t.y) * m + t.x;
+    double w[3][9];
+    zslice<PAT, SCALED>(w[0], p, t.z0 >= 1, nb, d);
+    zslice<PAT, SCALED>(w[1], p + S, true, nb, d);
+    p += 2 * S;
+    // no early exit: slices past the chunk end load as zeros and their results
+    // are dropped, so the unrolled loop has no data-dependent branch
+#pragma unroll
+    for (int i = 0; i < ZC; ++i) {
+        zslice<PAT, SCALED>(w[2], p, t.z0 + i + 1 < m, nb, d);
+        p += S;
+        if (i < t.zn) f(t.z0 + i, zsum<PAT>(c, w), w[1][4]);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            w[0][q] = w[1][q];
+            w[1][q] = w[2][q];
+        }
+    }
+}
+
+// out[t] = scale_t * S_t in[t] for planes t in [t0, t0 + gridDim.y) (t0 may be -1:
+// ghost planes); table row per plane: tab + 27 * (sid ? sid[t] : 0)
+template <uint32_t PAT>
+__global__ void __launch_bounds__(ZX * ZY)
+    kz_apply(int m, int t0, const double* __restrict__ tab, int tstride,
+             const int* __restrict__ sid, const double* __restrict__ scale,
+             const double* __restrict__ in, double* __restrict__ out) {
+    const ZTile t = ztile(m);
+    if (!t.ok) return;
+    const long long n = (long long)m * m * m;
+    const int pl = t0 + (int)blockIdx.y;
+    const double* tb = tab + (size_t)tstride * (sid ? __ldg(sid + pl) : 0);
+    double c[27];
+    zcoef<PAT>(c, tb);
+    const double sc = scale ? __ldg(scale + pl) : 1.0;
+    const double* v = in + pl * n;
+    double* o = out + pl * n + ((long long)t.y) * m + t.x;
+    zmarch<PAT, false>(t, m, v, c, 1.0, [&](int z, double s, double) {
+        o[(long long)z * m * m] = scale ? sc * s : s;
+    });
+}
+
+// r1 = ((Mu_t - Mu_{t-1}) - s_t A p_t) - f_t   (OP_R1 of k3_timeop, Mu precomputed)
+template <uint32_t PAT>
+__global__ void __launch_bounds__(ZX * ZY)
+    kz_r1(int m, int qmin, const double* __restrict__ ast, const int* __restrict__ asid,
+          const double* __restrict__ ascale, const double* __restrict__ mu,
+          const double* __restrict__ p, const double* __restrict__ f, double* __restrict__ out) {
+    const ZTile t = ztile(m);
+    if (!t.ok) return;
+    const long long n = (long long)m * m * m;
+    const int pl = (int)blockIdx.y;
+    double c[27];
+    zcoef<PAT>(c, ast + 27 * __ldg(asid + pl));
+    const double sc = __ldg(ascale + pl);
+    const long long col = (long long)t.y * m + t.x;
+    const bool hp = pl - 1 >= qmin;
+    zmarch<PAT, false>(t, m, p + pl * n, c, 1.0, [&](int z, double s, double) {
+        const long long gi = pl * n + (long long)z * m * m + col;
+        const double mc = __ldg(mu + gi);
+        const double ku = hp ? mc - __ldg(mu + gi - n) : mc;
+        out[gi] = (ku - sc * s) - __ldg(f + gi);
+    });
+}
+
+// z = (f - K^T p) - ((K u + K^T u) + s_t A u_t)   (OP_Z of k3_timeop, Mu/Mp precomputed)
+template <uint32_t PAT>
+__global__ void __launch_bounds__(ZX * ZY)
+    kz_z(int m, int qmin, int qmax, const double* __restrict__ ast, const int* __restrict__ asid,
+         const double* __restrict__ ascale, const double* __restrict__ mu,
+         const double* __restrict__ mp, const double* __restrict__ u, const double* __restrict__ f,
+         double* __restrict__ out) {
+    const ZTile t = ztile(m);
+    if (!t.ok) return;
+    const long long n = (long long)m * m * m;
+    const int pl = (int)blockIdx.y;
+    double c[27];
+    zcoef<PAT>(c, ast + 27 * __ldg(asid + pl));
+    const double sc = __ldg(ascale + pl);
+    const long long col = (long long)t.y * m + t.x;
+    const bool hp = pl - 1 >= qmin, hn = pl + 1 <= qmax;
+    zmarch<PAT, false>(t, m, u + pl * n, c, 1.0, [&](int z, double s, double) {
+        const long long gi = pl * n + (long long)z * m * m + col;
+        const double mpc = __ldg(mp + gi), muc = __ldg(mu + gi);
+        const double ktp = hn ? mpc - __ldg(mp + gi + n) : mpc;
+        const double ku = hp ? muc - __ldg(mu + gi - n) : muc;
+        const double ktu = hn ? muc - __ldg(mu + gi + n) : muc;
+        out[gi] = (__ldg(f + gi) - ktp) - ((ku + ktu) + sc * s);
+    });
+}
+
+// r = b - S(dinv * b)   (spatial.py:153,156)
+template <uint32_t PAT>
+__global__ void __launch_bounds__(ZX * ZY)
+    kz_residual(int m, const double* __restrict__ tab, const int* __restrict__ sid,
+                const double* __restrict__ b, double* __restrict__ r) {
+    const ZTile t = ztile(m);
+    if (!t.ok) return;
+    const long long n = (long long)m * m * m;
+    const int pl = (int)blockIdx.y;
+    const double* tb = tab + (size_t)__ldg(sid + pl) * 28;
+    double c[27];
+    zcoef<PAT>(c, tb);
+    const double d = __ldg(tb + 27);
+    const double* bp = b + pl * n;
+    const long long col = (long long)t.y * m + t.x;
+    zmarch<PAT, true>(t, m, bp, c, d, [&](int z, double s, double) {
+        const long long li = (long long)z * m * m + col;
+        r[pl * n + li] = __ldg(bp + li) - s;
+    });
+}
+
+// x += dinv*(b - S x) (spatial.py:159-160) + the finest-level epilogues
+template <uint32_t PAT>
+__global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 1 : 3) kz_smooth(Smooth3 a) {
+    const ZTile t = ztile(a.m);
+    const int m = a.m;
+    const long long n = (long long)m * m * m;
+    const int pl = (int)blockIdx.y;
+    double acc = 0.0;
+    if (t.ok) {
+        const double* tb = a.tab + (size_t)__ldg(a.sid + pl) * 28;
+        double c[27];
+        zcoef<PAT>(c, tb);
+        const double d = __ldg(tb + 27);
+        const long long col = (long long)t.y * m + t.x;
+        const double* xp = a.x + pl * n;
+        const double rtau = __ldg(a.rsteps + pl), tau = __ldg(a.steps + pl);
+        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : div_rn(v, tau); };
+        zmarch<PAT, false>(t, m, xp, c, 1.0, [&](int z, double s, double xv) {
+            const long long gi = pl * n + (long long)z * m * m + col;
+            const double bv = __ldg(a.b + gi);
+            const double xn = xv + d * (bv - s);
+            switch (a.epi) {
+                case EPI_PLAIN: a.out[gi] = xn; break;
+                case EPI_DIV_TAU: a.out[gi] = divtau(xn); break;
+                case EPI_UZAWA_P: {
+                    const double dp = divtau(xn);
+                    a.out[gi] = __ldg(a.pin + gi) + dp;
+                    acc = acc + bv * dp;
+                    break;
+                }
+                case EPI_DOT_TAU: acc = acc + bv * divtau(xn); break;
+                case EPI_SCALE: a.out[gi] = a.scale * xn; break;
+                case EPI_SCALE_DOT: {
+                    const double w = a.scale * xn;
+                    a.out[gi] = w;
+                    acc = acc + __ldg(a.aux + gi) * w;
+                    break;
+                }
+                case EPI_SCALE_DOTONLY: acc = acc + __ldg(a.aux + gi) * (a.scale * xn); break;
+            }
+        });
+    }
+    if (a.part) {
+        const double s = block_sum<ZX * ZY>(acc);
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            a.part[(long long)blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+// x = dinv*b + P e  (csr_matvec of the trilinear P over ascending coarse
+// index, spatial.py:149-150,157; e = b_c / a_c on a 1x1x1 coarsest grid).
+// z-marching: the (y, x) interpolation terms of a column are fixed, and each
+// coarse plane's <= 4 values serve the three fine planes 2k, 2k+1, 2k+2.
+template <bool DIRECT>
+__global__ void __launch_bounds__(ZX * ZY)
+    kz_prolong(int m, int mc, const double* __restrict__ tab, const double* __restrict__ tabc,
+               const int* __restrict__ sid, const double* __restrict__ b,
+               const double* __restrict__ ec, double* __restrict__ x) {
+    constexpr bool direct = DIRECT;
+    const ZTile t = ztile(m);
+    if (!t.ok) return;
+    const long long n = (long long)m * m * m, nc = (long long)mc * mc * mc;
+    const int pl = (int)blockIdx.y;
+    const int set = __ldg(sid + pl);
+    const double d = __ldg(tab + (size_t)set * 28 + 27);
+    const double ac = direct ? __ldg(tabc + (size_t)set * 28 + 13) : 1.0;
+    // interpolation terms of one coordinate f: odd -> coarse (f-1)/2, weight 1;
+    // even -> f/2-1 (if >= 0) then f/2 (if < mc), weights 1/2 (pro_terms order)
+    auto terms = [&](int f, int& j0, int& j1, double& w, bool& h0, bool& h1) {
+        if (f & 1) {
+            j0 = (f - 1) >> 1;
+            j1 = j0;
+            w = 1.0;
+            h0 = true;
+            h1 = false;
+        } else {
+            j0 = (f >> 1) - 1;
+            j1 = f >> 1;
+            w = 0.5;
+            h0 = j0 >= 0;
+            h1 = j1 < mc;
+        }
+    };
+    int y0, y1, x0, x1;
+    double wyv, wxv;
+    bool hy0, hy1, hx0, hx1;
+    terms(t.y, y0, y1, wyv, hy0, hy1);
+    terms(t.x, x0, x1, wxv, hx0, hx1);
+    const double* ep = ec + pl * nc;
+    // coarse plane k at the column's (y, x) combinations (zero outside)
+    auto load = [&](int k, double (&g)[2][2]) {
+        const bool kin = k >= 0 && k < mc;
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const bool in = kin && (bb ? hy1 : hy0) && (cc ? hx1 : hx0);
+                double e = in ? __ldg(ep + ((long long)k * mc + (bb ? y1 : y0)) * mc + (cc ? x1 : x0))
+                              : 0.0;
+                if (direct) e = e / ac;
+                g[bb][cc] = e;
+            }
+    };
+    auto accum = [&](double wz, const double (&g)[2][2], double& pe, bool& first) {
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                if (!(bb ? hy1 : hy0) || !(cc ? hx1 : hx0)) continue;
+                const double tterm = ((wz * wyv) * wxv) * g[bb][cc];
+                pe = first ? tterm : pe + tterm;
+                first = false;
+            }
+    };
+    const long long col = (long long)t.y * m + t.x;
+    const int k0 = t.z0 >> 1;  // z0 is even
+    double gp[2][2], gc[2][2];
+    load(k0 - 1, gp);
+    load(k0, gc);
+#pragma unroll
+    for (int i = 0; i < ZC; i += 2) {
+        if (i >= t.zn) break;
+        const int k = k0 + i / 2;
+        {   // even fine plane z = 2k: coarse k-1 (if any) then k (if any), weights 1/2
+            double pe = 0.0;
+            bool first = true;
+            if (k - 1 >= 0) accum(0.5, gp, pe, first);
+            if (k < mc) accum(0.5, gc, pe, first);
+            const long long gi = pl * n + (long long)(2 * k) * m * m + col;
+            x[gi] = d * __ldg(b + gi) + pe;
+        }
+        if (i + 1 < t.zn) {  // odd fine plane 2k+1: coarse k, weight 1
+            double pe = 0.0;
+            bool first = true;
+            accum(1.0, gc, pe, first);
+            const long long gi = pl * n + (long long)(2 * k + 1) * m * m + col;
+            x[gi] = d * __ldg(b + gi) + pe;
+        }
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) gp[bb][cc] = gc[bb][cc];
+        load(k + 1, gc);
+    }
+}
+
+// b_c = P^T r: for coarse (Z, Y, X) the 27 fine nodes (2Z+a, 2Y+bb, 2X+cc) in
+// ascending fine index, weights (wa*wb)*wc with w = (0.5, 1, 0.5) (kron of
+// spatial.py:75-84, same order as k3_restrict).  z-marching over coarse Z:
+// fine plane 2Z+2 is plane 2(Z+1) of the next coarse point.
+__global__ void __launch_bounds__(ZX * ZY)
+    kz_restrict(int m, int mc, const double* __restrict__ r, double* __restrict__ bc) {
+    const ZTile t = ztile(mc);
+    if (!t.ok) return;
+    const long long n = (long long)m * m * m, nc = (long long)mc * mc * mc;
+    const int pl = (int)blockIdx.y;
+    const double* rp = r + pl * n;
+    const double w[3] = {0.5, 1.0, 0.5};
+    auto load = [&](int fz, double (&g)[9]) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+            g[q] = __ldg(rp + ((long long)fz * m + (2 * t.y + q / 3)) * m + (2 * t.x + q % 3));
+    };
+    double g0[9], g1[9], g2[9];
+    load(2 * t.z0, g0);
+    const long long col = (long long)t.y * mc + t.x;
+#pragma unroll
+    for (int i = 0; i < ZC; ++i) {
+        if (i >= t.zn) break;
+        const int Z = t.z0 + i;
+        load(2 * Z + 1, g1);
+        load(2 * Z + 2, g2);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 27; ++k) {
+            const int a = k / 9, q = k % 9;
+            const double v = a == 0 ? g0[q] : a == 1 ? g1[q] : g2[q];
+            const double tterm = ((w[a] * w[q / 3]) * w[q % 3]) * v;
+            s = k == 0 ? tterm : s + tterm;
+        }
+        bc[pl * nc + (long long)Z * mc * mc + col] = s;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) g0[q] = g2[q];
+    }
+}
+
+// run f(std::integral_constant<uint32_t, PAT>) for the smallest compiled pattern covering mask
+template <typename F>
+void zdispatch(uint32_t mask, F&& f) {
+    switch (pattern_pick(mask)) {
+        case PAT_A7: f(std::integral_constant<uint32_t, PAT_A7>{}); break;
+        case PAT_M15: f(std::integral_constant<uint32_t, PAT_M15>{}); break;
+        default: f(std::integral_constant<uint32_t, PAT_F27>{}); break;
+    }
+}
+
 dim3 grid3(int m, int planes) {
     const long long n = (long long)m * m * m;
     return dim3((unsigned)((n + T3 - 1) / T3), (unsigned)planes);
@@ -337,10 +780,57 @@ bool epi_dot(int epi) {
 
 }  // namespace
 
+// M applied to every plane of [qmin, qmax] of src into dst (same plane indexing)
+static void mass_planes3(pint_ctx* c, const double* src, double* dst, int qmin, int qmax) {
+    const uint32_t pm = pattern_of(c->h_mass.data(), 1);
+    zdispatch(pm, [&](auto P) {
+        kz_apply<decltype(P)::value><<<zgrid(c->m, qmax - qmin + 1), dim3(ZX, ZY), 0, c->stream>>>(
+            c->m, qmin, c->d_mass, 0, nullptr, nullptr, src, dst);
+    });
+    PINT_LAUNCHED(c);
+}
+
+static double* mass_buffer3(pint_ctx* c, double*& buf) {
+    // planes -1 .. N (ghost planes of a time partition); returns plane 0
+    if (!buf) {
+        PINT_CUDA_CHECK(cudaMalloc(&buf, (size_t)(c->N + 2) * c->n * sizeof(double) + 16));
+        c->mu3_src = nullptr;
+    }
+    return buf + c->n;
+}
+
 void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                     double* out) {
     const dim3 g((unsigned)(((long long)c->n + T3 - 1) / T3), (unsigned)((c->N + G3 - 1) / G3));
     const int qmin = c->has_prev ? -1 : 0, qmax = c->has_next ? c->N : c->N - 1;
+    if (op == OP_R1 || op == OP_Z) {
+        // z-marching path: M u (and M p) of every plane first, then one fused
+        // pass with the stiffness stencil (same arithmetic as k3_timeop)
+        const uint32_t pa = pattern_of(c->h_ast.data(), c->n_a);
+        double* mu = mass_buffer3(c, c->d_mu3);
+        const int kid = op == OP_R1 ? K_TIMEOP_R1 : K_TIMEOP_Z;
+        ProfScope prof(c, kid, 8.0 * (op == OP_R1 ? 6 : 9) * (double)c->N * c->n);
+        if (op == OP_R1 || !(c->mu3_trust && c->mu3_src == u)) {
+            mass_planes3(c, u, mu, qmin, qmax);
+            c->mu3_src = u;
+        }
+        if (op == OP_R1) {
+            zdispatch(pa, [&](auto P) {
+                kz_r1<decltype(P)::value><<<zgrid(c->m, c->N), dim3(ZX, ZY), 0, c->stream>>>(
+                    c->m, qmin, c->d_ast, c->d_asid, c->d_ascale, mu, p, f, out);
+            });
+        } else {
+            double* mp = mass_buffer3(c, c->d_mp3);
+            mass_planes3(c, p, mp, 0, qmax);
+            zdispatch(pa, [&](auto P) {
+                kz_z<decltype(P)::value><<<zgrid(c->m, c->N), dim3(ZX, ZY), 0, c->stream>>>(
+                    c->m, qmin, qmax, c->d_ast, c->d_asid, c->d_ascale, mu, mp, u, f, out);
+            });
+        }
+        PINT_LAUNCHED(c);
+        PINT_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     static const int passes[] = {2, 2, 2, 4, 4};
     static const int kid[] = {K_TIMEOP_K, K_TIMEOP_KT, K_TIMEOP_ABD, K_TIMEOP_R1, K_TIMEOP_Z};
     ProfScope prof(c, kid[op], 8.0 * passes[op] * (double)c->N * c->n);
@@ -364,7 +854,11 @@ void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const
 
 void launch_apply3(pint_ctx* c, const double* st, const double* in, double* out, int count) {
     ProfScope prof(c, K_AREF, 16.0 * (double)count * c->n);
-    k3_apply<<<grid3(c->m, count), T3, 0, c->stream>>>(c->m, st, in, out);
+    const uint32_t pm = st == c->d_aref ? pattern_of(c->h_aref.data(), 1) : PAT_F27;
+    zdispatch(pm, [&](auto P) {
+        kz_apply<decltype(P)::value><<<zgrid(c->m, count), dim3(ZX, ZY), 0, c->stream>>>(
+            c->m, 0, st, 0, nullptr, nullptr, in, out);
+    });
     PINT_LAUNCHED(c);
     PINT_CUDA_CHECK(cudaGetLastError());
 }
@@ -396,8 +890,12 @@ void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, in
         {
             ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
                            8.0 * count * ((double)m * m * m + (double)mc * mc * mc));
-            k3_residual<<<grid3(m, count), T3, 0, c->stream>>>(m, tab(l), s.sid, bl, c->d_t3a);
-            k3_restrict<<<grid3(mc, count), T3, 0, c->stream>>>(m, mc, c->d_t3a, c->lev_b[l + 1]);
+            zdispatch(s.shape3[l], [&](auto P) {
+                kz_residual<decltype(P)::value><<<zgrid(m, count), dim3(ZX, ZY), 0, c->stream>>>(
+                    m, tab(l), s.sid, bl, c->d_t3a);
+            });
+            kz_restrict<<<zgrid(mc, count), dim3(ZX, ZY), 0, c->stream>>>(m, mc, c->d_t3a,
+                                                                           c->lev_b[l + 1]);
         }
         c->launches += 2;
         bl = c->lev_b[l + 1];
@@ -412,8 +910,12 @@ void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, in
         {
             ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE,
                            8.0 * count * (3.0 * m * m * m + (double)mc * mc * mc));
-            k3_prolong<<<grid3(m, count), T3, 0, c->stream>>>(m, mc, tab(l), tab(l + 1), s.sid,
-                                                              direct ? 1 : 0, bcur, ec, c->d_t3b);
+            if (direct)
+                kz_prolong<true><<<zgrid(m, count), dim3(ZX, ZY), 0, c->stream>>>(
+                    m, mc, tab(l), tab(l + 1), s.sid, bcur, ec, c->d_t3b);
+            else
+                kz_prolong<false><<<zgrid(m, count), dim3(ZX, ZY), 0, c->stream>>>(
+                    m, mc, tab(l), tab(l + 1), s.sid, bcur, ec, c->d_t3b);
             Smooth3 a{};
             a.m = m;
             a.tab = tab(l);
@@ -427,13 +929,15 @@ void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, in
             a.rsteps = c->d_rsteps;
             a.pin = pin;
             a.aux = aux;
-            const dim3 g = grid3(m, count);
+            const dim3 g = zgrid(m, count);
             const bool dot = top && epi_dot(epi);
             if (dot) {
                 ensure_partials(c, (size_t)g.x * g.y);
                 a.part = c->d_part;
             }
-            k3_smooth<<<g, T3, 0, c->stream>>>(a);
+            zdispatch(s.shape3[l], [&](auto P) {
+                kz_smooth<decltype(P)::value><<<g, dim3(ZX, ZY), 0, c->stream>>>(a);
+            });
             if (dot) reduce_partials(c, (int)(g.x * g.y), acc_slot);
         }
         c->launches += 2;

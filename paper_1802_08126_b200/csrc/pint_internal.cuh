@@ -51,6 +51,7 @@ struct MgSet {
     double* tab = nullptr;    // device [levels][n_sets][PINT_TW]
     int* sid = nullptr;       // device [B]
     std::vector<int> shape;   // per level: which stencil positions can be non-zero
+    std::vector<uint32_t> shape3;  // 3D: per level, 27-bit union of non-zero positions
     bool ready = false;
 };
 
@@ -149,6 +150,9 @@ struct pint_ctx {
     double *d_r1 = nullptr, *d_z = nullptr, *d_w1 = nullptr, *d_w2 = nullptr;
     double *d_stage_in = nullptr, *d_stage_out = nullptr, *d_vec = nullptr;
     double *d_t3a = nullptr, *d_t3b = nullptr;  // 3D multigrid work slabs
+    double *d_mu3 = nullptr, *d_mp3 = nullptr;  // 3D: M u, M p of planes -1..N (ops3d.cu)
+    const double* mu3_src = nullptr;            // u that d_mu3 was computed from
+    bool mu3_trust = false;                     // caller guarantees u unchanged since (Uzawa step)
     size_t t3_cap = 0;
 
     // reductions
