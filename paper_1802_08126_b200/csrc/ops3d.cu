@@ -398,11 +398,9 @@ inline dim3 zgrid(int m, int planes) {
     return dim3((unsigned)(tx * ty * tz), (unsigned)planes);
 }
 
-// per-thread neighbourhood of a column: in-domain flags of x-1, x+1, y-1,
-// y+1 and the element offsets of the 9 (dy, dx) positions inside a slice
+// per-thread neighbourhood of a column: in-domain flags of x-1, x+1, y-1, y+1
 struct ZNbr {
     bool xl, xr, yl, yr;
-    int off[9];
 };
 __device__ __forceinline__ ZNbr znbr(int m, int x, int y) {
     ZNbr b;
@@ -410,8 +408,6 @@ __device__ __forceinline__ ZNbr znbr(int m, int x, int y) {
     b.xr = x + 1 < m;
     b.yl = y > 0;
     b.yr = y + 1 < m;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) b.off[q] = (q / 3 - 1) * m + (q % 3 - 1);
     return b;
 }
 __device__ __forceinline__ bool znbr_in(const ZNbr& b, int q) {
@@ -419,17 +415,24 @@ __device__ __forceinline__ bool znbr_in(const ZNbr& b, int q) {
     return (dy < 0 ? b.yl : dy > 0 ? b.yr : true) && (dx < 0 ? b.xl : dx > 0 ? b.xr : true);
 }
 
-// the needed (dy, dx) values of the slice at column pointer p (zero outside
-// the domain or when !zin), times d when SCALED
+// the needed (dy, dx) values of the slice whose column element is v[i]
+// (zero outside the domain or when !zin), times d when SCALED.  32-bit
+// element indices into one plane: a row is one base address, the x
+// neighbours are immediate offsets of it.
 template <uint32_t PAT, bool SCALED>
-__device__ __forceinline__ void zslice(double* w, const double* p, bool zin, const ZNbr& nb,
-                                       double d) {
+__device__ __forceinline__ void zslice(double* w, const double* __restrict__ v, int i, int m,
+                                       bool zin, const ZNbr& nb, double d) {
 #pragma unroll
-    for (int q = 0; q < 9; ++q) {
-        if (!pat_need(PAT, q)) continue;
-        const bool in = zin && znbr_in(nb, q);
-        const double v = in ? __ldg(p + nb.off[q]) : 0.0;
-        w[q] = SCALED ? (in ? d * v : 0.0) : v;
+    for (int dy = -1; dy <= 1; ++dy) {
+        const double* r = v + (i + dy * m);
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            const int q = (dy + 1) * 3 + (dx + 1);
+            if (!pat_need(PAT, q)) continue;
+            const bool in = zin && znbr_in(nb, q);
+            const double val = in ? __ldg(r + dx) : 0.0;
+            w[q] = SCALED ? (in ? d * val : 0.0) : val;
+        }
     }
 }
 
@@ -454,24 +457,25 @@ __device__ __forceinline__ void zcoef(double* c, const double* __restrict__ tb) 
     for (int k = 0; k < 27; ++k) c[k] = pat_has(PAT, k) ? __ldg(tb + k) : 0.0;
 }
 
-// march z over the chunk: f(z, sum, centre value) for every point of the column
+// march z over the chunk: f(z, li, sum, centre value) for every point of the
+// column, li = its element index inside the plane
 template <uint32_t PAT, bool SCALED, typename F>
 __device__ __forceinline__ void zmarch(const ZTile& t, int m, const double* __restrict__ v,
                                        const double* c, double d, F&& f) {
     const ZNbr nb = znbr(m, t.x, t.y);
-    const long long S = (long long)m * m;
-    const double* p = v + ((long long)(t.z0 - 1) * m + t.y) * m + t.x;
+    const int S = m * m;
+    int i = (t.z0 - 1) * S + t.y * m + t.x;  // may be negative for z0 = 0 (not loaded)
     double w[3][9];
-    zslice<PAT, SCALED>(w[0], p, t.z0 >= 1, nb, d);
-    zslice<PAT, SCALED>(w[1], p + S, true, nb, d);
-    p += 2 * S;
+    zslice<PAT, SCALED>(w[0], v, i, m, t.z0 >= 1, nb, d);
+    zslice<PAT, SCALED>(w[1], v, i + S, m, true, nb, d);
+    i += 2 * S;
     // no early exit: slices past the chunk end load as zeros and their results
     // are dropped, so the unrolled loop has no data-dependent branch
 #pragma unroll
-    for (int i = 0; i < ZC; ++i) {
-        zslice<PAT, SCALED>(w[2], p, t.z0 + i + 1 < m, nb, d);
-        p += S;
-        if (i < t.zn) f(t.z0 + i, zsum<PAT>(c, w), w[1][4]);
+    for (int k = 0; k < ZC; ++k) {
+        zslice<PAT, SCALED>(w[2], v, i, m, t.z0 + k + 1 < m, nb, d);
+        if (k < t.zn) f(t.z0 + k, i - S, zsum<PAT>(c, w), w[1][4]);
+        i += S;
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
             w[0][q] = w[1][q];
@@ -496,9 +500,9 @@ __global__ void __launch_bounds__(ZX * ZY)
     zcoef<PAT>(c, tb);
     const double sc = scale ? __ldg(scale + pl) : 1.0;
     const double* v = in + pl * n;
-    double* o = out + pl * n + ((long long)t.y) * m + t.x;
-    zmarch<PAT, false>(t, m, v, c, 1.0, [&](int z, double s, double) {
-        o[(long long)z * m * m] = scale ? sc * s : s;
+    double* o = out + pl * n;
+    zmarch<PAT, false>(t, m, v, c, 1.0, [&](int, int li, double s, double) {
+        o[li] = scale ? sc * s : s;
     });
 }
 
@@ -517,8 +521,8 @@ __global__ void __launch_bounds__(ZX * ZY)
     const double sc = __ldg(ascale + pl);
     const long long col = (long long)t.y * m + t.x;
     const bool hp = pl - 1 >= qmin;
-    zmarch<PAT, false>(t, m, p + pl * n, c, 1.0, [&](int z, double s, double) {
-        const long long gi = pl * n + (long long)z * m * m + col;
+    zmarch<PAT, false>(t, m, p + pl * n, c, 1.0, [&](int, int li, double s, double) {
+        const long long gi = pl * n + li;
         const double mc = __ldg(mu + gi);
         const double ku = hp ? mc - __ldg(mu + gi - n) : mc;
         out[gi] = (ku - sc * s) - __ldg(f + gi);
@@ -541,8 +545,8 @@ __global__ void __launch_bounds__(ZX * ZY)
     const double sc = __ldg(ascale + pl);
     const long long col = (long long)t.y * m + t.x;
     const bool hp = pl - 1 >= qmin, hn = pl + 1 <= qmax;
-    zmarch<PAT, false>(t, m, u + pl * n, c, 1.0, [&](int z, double s, double) {
-        const long long gi = pl * n + (long long)z * m * m + col;
+    zmarch<PAT, false>(t, m, u + pl * n, c, 1.0, [&](int, int li, double s, double) {
+        const long long gi = pl * n + li;
         const double mpc = __ldg(mp + gi), muc = __ldg(mu + gi);
         const double ktp = hn ? mpc - __ldg(mp + gi + n) : mpc;
         const double ku = hp ? muc - __ldg(mu + gi - n) : muc;
@@ -566,8 +570,7 @@ __global__ void __launch_bounds__(ZX * ZY)
     const double d = __ldg(tb + 27);
     const double* bp = b + pl * n;
     const long long col = (long long)t.y * m + t.x;
-    zmarch<PAT, true>(t, m, bp, c, d, [&](int z, double s, double) {
-        const long long li = (long long)z * m * m + col;
+    zmarch<PAT, true>(t, m, bp, c, d, [&](int, int li, double s, double) {
         r[pl * n + li] = __ldg(bp + li) - s;
     });
 }
@@ -589,8 +592,8 @@ __global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 1 : 3) kz_smooth(Smo
         const double* xp = a.x + pl * n;
         const double rtau = __ldg(a.rsteps + pl), tau = __ldg(a.steps + pl);
         auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : div_rn(v, tau); };
-        zmarch<PAT, false>(t, m, xp, c, 1.0, [&](int z, double s, double xv) {
-            const long long gi = pl * n + (long long)z * m * m + col;
+        zmarch<PAT, false>(t, m, xp, c, 1.0, [&](int, int li, double s, double xv) {
+            const long long gi = pl * n + li;
             const double bv = __ldg(a.b + gi);
             const double xn = xv + d * (bv - s);
             switch (a.epi) {
