@@ -183,6 +183,78 @@ def build_solver(load, device):
     return pg, spec, system, at, ht
 
 
+OTHER_CONFIGS = {
+    # BASELINE configs[2]/[4] (G=1)/[3]: MG-compatible meshes
+    "c3": dict(space="3d", cells=64, N=512, T=1.0,
+               workload="c3: 3D heat, unit cube, cells=64 (63^3=250047 interior), N=512, T=1, "
+                        "f~N(0,1) seed 0, u0~U[0,1] seed 0 (drawn after f)"),
+    "c5": dict(space="3d", cells=64, N=1024, T=1.0,
+               workload="c5 (G=1 slice of the weak-scaling series): 3D heat, cells=64, N=1024, "
+                        "T=1, f~N(0,1) seed 0, u0=0"),
+    "c4": dict(space="2d", cells=512, N=4096, T=2.0,
+               workload="c4: 2D -div(a(x,t) grad u), a=1+0.5 sin(2 pi t)(x1^2+x2^2)+0.1 U_cell "
+                        "(seed 0), cells=512 (511^2=261121 interior), N=4096, T=2, "
+                        "f~N(0,1) seed 1, u0=0"),
+}
+
+
+def measure_config(name, steps=3, warm=2):
+    """Per-iteration device time of one more BASELINE config on this GPU
+    (CUDA events on the library stream, state resident in HBM), with the
+    iteration roofline fraction and the per-kernel shares."""
+    import ctypes
+    import gc
+
+    import paper_1802_08126_b200 as pg
+
+    c = OTHER_CONFIGS[name]
+    cells, N, space = c["cells"], c["N"], c["space"]
+    n = (cells - 1) ** (3 if space == "3d" else 2)
+    t0 = time.perf_counter()
+    grid = pg.build_time_grid("uniform", N, c["T"])
+    if name == "c4":
+        load = np.random.default_rng(1).standard_normal((N, n))
+        spec = pg.make_weighted_problem(cells, grid, pg.c4_cell_weights(cells, grid, seed=0),
+                                        load, np.zeros(n), alpha=1.0)
+    else:
+        rng = np.random.default_rng(0)
+        load = rng.standard_normal((N, n))
+        u0 = rng.uniform(0.0, 1.0, n) if name == "c3" else np.zeros(n)
+        spec = pg.problem_from_arrays(space, cells, grid, load, u0, alpha=1.0)
+    system = pg.TimeGlobalSystem(spec)
+    pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy(space, cells))
+    pg.build_schur_preconditioner(spec, "mg")
+    ctx = system._gp.ctx
+    setup = time.perf_counter() - t0
+    f = np.ascontiguousarray(system.rhs)
+    del load
+    ref = ctypes.c_double()
+    ctx.call("pint_uzawa_begin", f.ctypes.data, None, None, ctypes.byref(ref))
+    nums = np.zeros(max(steps, warm, 2))
+    ms = ctypes.c_double()
+    ctx.call("pint_uzawa_run", 0.9, warm, nums.ctypes.data, ctypes.byref(ms))
+    ctx.call("pint_uzawa_run", 0.9, steps, nums.ctypes.data, ctypes.byref(ms))
+    ms_it = ms.value / steps
+    ctx.call("pint_profile", 1)
+    ctx.call("pint_uzawa_run", 0.9, 1, nums.ctypes.data, ctypes.byref(ms))
+    stats = ctx.kernel_stats()
+    ctx.call("pint_profile", 0)
+    hbm, _ = peaks()
+    tot = sum(v[0] for v in stats.values()) or 1.0
+    dom = max(stats.items(), key=lambda kv: kv[1][0])
+    iter_bytes = 224.0 * N * n
+    out = {"workload": c["workload"], "n": n, "N": N, "ms_per_iter": ms_it,
+           "value": N * n / (ms_it / 1e3), "unit": "DoF/s", "setup_s": setup,
+           "iteration_frac": iter_bytes / (ms_it / 1e3) / 1e9 / hbm,
+           "dominant_kernel": {"name": dom[0], "share": dom[1][0] / tot,
+                               "GBps": dom[1][2] / dom[1][0] / 1e6 if dom[1][0] else None},
+           "kernel_shares": {k: round(v[0] / tot, 4) for k, v in
+                             sorted(stats.items(), key=lambda kv: -kv[1][0]) if v[1]}}
+    del system, spec, ctx, f
+    gc.collect()
+    return out
+
+
 def run_gpu_partitioned(args, world, rank, local):
     """N > 1 GPUs (or --partitioned): the c2 time axis split across ranks
     (paper_1802_08126_b200/distributed.py), strong scaling."""
@@ -335,6 +407,19 @@ def run_gpu(args):
     wall = time.perf_counter() - t0
     e2e_val = world * N * n * hist.iterations / wall
 
+    others = {}
+    if rank == 0 and world == 1 and not args.no_other:
+        del system, at, ht, spec, gp, ctx
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        for name in ("c3", "c5", "c4"):
+            try:
+                others[name] = measure_config(name)
+            except Exception as e:  # report, do not lose the headline line
+                others[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            gc.collect()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, dt = cpu_oracle_rate(iters=4)
@@ -364,6 +449,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": launches,
+            "other_configs": others or None,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -377,6 +463,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-other", action="store_true",
+                    help="skip the per-iteration measurements of configs c3, c5 (G=1), c4")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the time-partitioned driver even on one GPU (validation)")
     args = ap.parse_args()
