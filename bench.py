@@ -55,6 +55,22 @@ def c2_load(cells=CELLS, N=NSTEPS, seed=0):
     return g - dinv[None, :] * a.dot(g.T).T
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu launch
+    summary (profiles/*_c2_traffic.json, tools/traffic_summary.py), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_c2_traffic.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as fh:
+            d = json.load(fh)
+        return float(d["kernels"][kernel]["dram_bytes_per_launch"]), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -400,6 +416,7 @@ def run_gpu(args):
                    "GBps": (v[2] / v[0] / 1e6) if v[0] > 0 else None, "launches": v[1]}
                for k, v in stats.items() if v[1] > 0}
     iter_bytes = 224.0 * N * n  # 28 fp64 block-vector passes per iteration
+    traffic, traffic_src = ncu_traffic(dname)
     # ---- end to end through the public API (host numpy in / out) ----------
     t0 = time.perf_counter()
     (p_h, u_h), hist = pg.uzawa_solve(system, at, ht, pg.UzawaConfig(omega=0.9, tol=1e-8,
@@ -442,7 +459,8 @@ def run_gpu(args):
                     "step": "one uzawa_solve call from host arrays to convergence"},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": dbytes / dcnt,
                          "iteration_alg_GBps": iter_bytes / (ms_step / 1e3) / 1e9,
                          "iteration_frac": iter_bytes / (ms_step / 1e3) / 1e9 / hbm},
             "kernels": kernels,
