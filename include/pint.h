@@ -186,6 +186,21 @@ int pint_uzawa(pint_ctx* ctx, const double* f, double* p, double* u, double omeg
                int* converged, double* phase_ms);
 
 /* ---------------------------------------------------------------------------
+ * MINRES building blocks (minres_solve, solvers.py:267-327).  Device pointers.
+ * apply_saddle: top = Abd p - K u, bottom = -Kt p - ((K u + Kt u) + Abd u)
+ *   (TimeGlobalSystem.apply_saddle, operators.py:107-111), bit-identical.
+ * lincomb: out[i] = ((x0[i] + a1*x1[i]) + a2*x2[i]) * (use_scale ? scale : 1),
+ *   x1/x2 may be NULL (term skipped): the operation order of numpy's
+ *   v - a*w1 - b*w2, s*y and x + phi*w in scipy's minres.
+ * dot: sum a[i]*b[i] (deterministic tree order; not numpy's BLAS order).
+ * ------------------------------------------------------------------------- */
+int pint_apply_saddle(pint_ctx* ctx, const double* p, const double* u, double* top,
+                      double* bottom);
+int pint_lincomb(pint_ctx* ctx, double* out, long long count, const double* x0, double a1,
+                 const double* x1, double a2, const double* x2, double scale, int use_scale);
+int pint_dot(pint_ctx* ctx, const double* a, const double* b, long long count, double* out);
+
+/* ---------------------------------------------------------------------------
  * Time-partitioned building blocks (one context per rank).  The
  * driver (paper_1802_08126_b200/distributed.py) moves ghost planes and
  * transposes with torch.distributed; these calls do the arithmetic.  All

@@ -43,6 +43,7 @@ __all__ = [
     "dst_kernel", "dst_forward", "dst_inverse", "dst_forward_T", "dst_inverse_T",
     "frequency_weights", "SchurInv", "BlockInv",
     "UzawaResult", "uzawa", "sequential_euler", "ExactNorms",
+    "MinresResult", "op_saddle", "minres",
 ]
 
 
@@ -671,6 +672,64 @@ def uzawa(pb: Problem, atilde: BlockInv, htilde: SchurInv, omega: float = 0.9,
             converged = True
             break
     return UzawaResult(p, u, res_hist, converged, wall)
+
+
+@dataclass
+class MinresResult:
+    p: np.ndarray
+    u: np.ndarray
+    residual: list
+    converged: bool
+
+
+def op_saddle(pb: Problem, p: np.ndarray, u: np.ndarray, scales=None):
+    """Symmetric indefinite 2x2 block operator (operators.py:107-111)."""
+    top = op_Abd(pb, p, scales) - op_K(pb, u)
+    bottom = -op_Kt(pb, p) - (op_K(pb, u) + op_Kt(pb, u) + op_Abd(pb, u, scales))
+    return top, bottom
+
+
+def minres(pb: Problem, atilde: BlockInv, htilde: SchurInv, tol: float = 1e-8,
+           max_iter: int = 500) -> MinresResult:
+    """Block-diagonally preconditioned MINRES on the saddle-point system
+    (solvers.py:267-327): scipy.sparse.linalg.minres (the reference's own
+    dependency, Paige-Saunders) with the reference's callback, which records
+    the true preconditioned residual of every iterate."""
+    import scipy.sparse.linalg as spla
+
+    f = fold_rhs(pb)
+    scales = stiffness_scales(pb)
+    N, n = pb.N, pb.dim
+    nd = N * n
+    g = np.concatenate([-f.ravel(), -f.ravel()])
+
+    def matvec(w):
+        top, bottom = op_saddle(pb, w[:nd].reshape(N, n), w[nd:].reshape(N, n), scales)
+        return np.concatenate([top.ravel(), bottom.ravel()])
+
+    def precond(w):
+        return np.concatenate([atilde.apply(w[:nd].reshape(N, n)).ravel(),
+                               htilde.apply(w[nd:].reshape(N, n)).ravel()])
+
+    rng = np.random.default_rng(1234)
+    for _ in range(3):
+        w = rng.standard_normal(2 * nd)
+        if w @ precond(w) <= 0.0:
+            raise OracleNotSpd("block preconditioner is not positive definite")
+    op = spla.LinearOperator((2 * nd, 2 * nd), matvec=matvec)
+    mop = spla.LinearOperator((2 * nd, 2 * nd), matvec=precond)
+    res = []
+    ref = float(np.sqrt(g @ precond(g)))
+    if ref == 0.0:
+        z = np.zeros((N, n))
+        return MinresResult(z, z.copy(), res, True)
+
+    def callback(xk):
+        r = g - matvec(xk)
+        res.append(float(np.sqrt(max(r @ precond(r), 0.0))) / ref)
+
+    w, info = spla.minres(op, g, M=mop, rtol=tol, maxiter=max_iter, callback=callback)
+    return MinresResult(w[:nd].reshape(N, n), w[nd:].reshape(N, n), res, info == 0)
 
 
 def sequential_euler(pb: Problem) -> np.ndarray:

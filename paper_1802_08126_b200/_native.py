@@ -54,6 +54,9 @@ _SIGNATURES = {
     "pint_uzawa_step": (_I, [_P, _D, _DP]),
     "pint_uzawa_end": (_I, [_P, _P, _P]),
     "pint_host_prefault": (_I, [_P, _P, ctypes.c_longlong]),
+    "pint_apply_saddle": (_I, [_P, _P, _P, _P, _P]),
+    "pint_lincomb": (_I, [_P, _P, ctypes.c_longlong, _P, _D, _P, _D, _P, _D, _I]),
+    "pint_dot": (_I, [_P, _P, _P, ctypes.c_longlong, _DP]),
     "pint_uzawa": (_I, [_P, _P, _P, _P, _D, _D, _I, _I, _P, _IP, _IP, _P]),
     "pint_set_timing": (_I, [_P, _I]),
     "pint_phase_ms": (_I, [_P, _P]),

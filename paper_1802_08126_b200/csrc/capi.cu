@@ -841,6 +841,56 @@ int pint_axpy(pint_ctx* c, double* u, const double* y, double omega, long long c
     });
 }
 
+int pint_dot(pint_ctx* c, const double* a, const double* b, long long count, double* out) {
+    return guarded(c, [&] {
+        require_device(a, "a");
+        require_device(b, "b");
+        if (!out || count < 0) pint_throw(PINT_INPUT, "bad dot arguments");
+        pint::launch_dot(c, a, b, count, 3);
+        PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc + 3, c->d_acc + 3, sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream));
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        *out = c->h_acc[3];
+    });
+}
+
+int pint_lincomb(pint_ctx* c, double* out, long long count, const double* x0, double a1,
+                 const double* x1, double a2, const double* x2, double scale, int use_scale) {
+    return guarded(c, [&] {
+        require_device(out, "out");
+        require_device(x0, "x0");
+        if (x1) require_device(x1, "x1");
+        if (x2) require_device(x2, "x2");
+        if (count < 0) pint_throw(PINT_INPUT, "bad count");
+        pint::launch_lincomb(c, out, x0, a1, x1, a2, x2, scale, use_scale != 0, count);
+    });
+}
+
+int pint_apply_saddle(pint_ctx* c, const double* p, const double* u, double* top,
+                      double* bottom) {
+    return guarded(c, [&] {
+        require_problem(c);
+        require_device(p, "p");
+        require_device(u, "u");
+        require_device(top, "top");
+        require_device(bottom, "bottom");
+        ensure_uzawa_buffers(c);
+        const long long S = (long long)slab(c);
+        // top = Abd p - K u ;  bottom = -Kt p - ((K u + Kt u) + Abd u)   (operators.py:107-111)
+        double *ku = c->d_r1, *ktp = c->d_z, *au = c->d_w1;
+        pint::launch_timeop(c, pint::OP_K, u, nullptr, nullptr, ku);
+        pint::launch_timeop(c, pint::OP_ABD, p, nullptr, nullptr, top);
+        pint::launch_lincomb(c, top, top, -1.0, ku, 0.0, nullptr, 1.0, false, S);
+        pint::launch_timeop(c, pint::OP_KT, p, nullptr, nullptr, ktp);
+        pint::launch_timeop(c, pint::OP_KT, u, nullptr, nullptr, bottom);
+        pint::launch_timeop(c, pint::OP_ABD, u, nullptr, nullptr, au);
+        // s = (Ku + Ktu) + Au ; bottom = (-Ktp) - s
+        pint::launch_lincomb(c, bottom, ku, 1.0, bottom, 1.0, au, 1.0, false, S);
+        pint::launch_lincomb(c, bottom, bottom, 0.0, nullptr, 0.0, nullptr, -1.0, true, S);
+        pint::launch_lincomb(c, bottom, bottom, -1.0, ktp, 0.0, nullptr, 1.0, false, S);
+    });
+}
+
 int pint_uzawa_begin(pint_ctx* c, const double* f, const double* p0, const double* u0,
                      double* ref_out) {
     return guarded(c, [&] {

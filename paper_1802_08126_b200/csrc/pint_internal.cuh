@@ -197,6 +197,9 @@ void launch_timeop(pint_ctx* c, int op, const double* u, const double* p, const 
 void launch_fold_rhs(pint_ctx* c, const double* load, const double* u_init, double* f);
 void launch_aref(pint_ctx* c, const double* in, double* out, int count);
 void launch_axpy(pint_ctx* c, double* u, const double* y, double omega, long long count);
+void launch_lincomb(pint_ctx* c, double* out, const double* x0, double a1, const double* x1,
+                    double a2, const double* x2, double sc, bool use_sc, long long count);
+void launch_dot(pint_ctx* c, const double* a, const double* b, long long count, int slot);
 // TMA band versions (timeop_band.cu), used for 64 <= m <= 512
 bool band_timeop_supported(const pint_ctx* c);
 void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p, const double* f,

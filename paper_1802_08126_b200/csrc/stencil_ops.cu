@@ -157,6 +157,52 @@ __global__ void __launch_bounds__(256) k_axpy(double* __restrict__ u, const doub
         u[i] = u[i] + omega * y[i];
 }
 
+// out = ((x0 + a1 x1) + a2 x2) * sc, absent terms skipped: the exact
+// operation sequence of numpy's  v - a*w1 - b*w2  /  s*y  /  x + phi*w
+// (no FMA in this file), used by the MINRES driver (solvers.py:267-327)
+__global__ void __launch_bounds__(256)
+    k_lincomb(double* __restrict__ out, const double* __restrict__ x0, double a1,
+              const double* __restrict__ x1, double a2, const double* __restrict__ x2, double sc,
+              int use_sc, long long count) {
+    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < count;
+         i += (long long)gridDim.x * 256) {
+        double v = x0[i];
+        if (x1) v = v + a1 * x1[i];
+        if (x2) v = v + a2 * x2[i];
+        out[i] = use_sc ? v * sc : v;
+    }
+}
+
+// per-CTA partial sums of a.b (grid-stride, fixed grid: deterministic)
+__global__ void __launch_bounds__(256)
+    k_dot_partials(const double* __restrict__ a, const double* __restrict__ b, long long count,
+                   double* __restrict__ part) {
+    double s = 0.0;
+    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < count;
+         i += (long long)gridDim.x * 256)
+        s += a[i] * b[i];
+    s = block_sum<256>(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+void launch_lincomb(pint_ctx* c, double* out, const double* x0, double a1, const double* x1,
+                    double a2, const double* x2, double sc, bool use_sc, long long count) {
+    const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 16);
+    k_lincomb<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, c->stream>>>(
+        out, x0, a1, x1, a2, x2, sc, use_sc ? 1 : 0, count);
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_dot(pint_ctx* c, const double* a, const double* b, long long count, int slot) {
+    constexpr int kParts = 148 * 8;
+    ensure_partials(c, kParts);
+    k_dot_partials<<<kParts, 256, 0, c->stream>>>(a, b, count, c->d_part);
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+    reduce_partials(c, kParts, slot);
+}
+
 void launch_axpy(pint_ctx* c, double* u, const double* y, double omega, long long count) {
     const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 16);
     k_axpy<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, c->stream>>>(u, y, omega, count);

@@ -14,7 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from ._device import gpu_problem
-from ._native import as_buffer, empty_like_kind, ptr_of
+from ._native import _is_tensor, as_buffer, empty_like_kind, ptr_of
 from .errors import DiagnosticModeRequiredError
 
 
@@ -74,9 +74,36 @@ class TimeGlobalSystem:
         return self.apply_Kt(u) + self.apply_Abd(u)
 
     def apply_saddle(self, p, u):
-        """Symmetric indefinite 2x2 block operator (operators.py:107-111)."""
-        top = self.apply_Abd(p) - self.apply_K(u)
-        bottom = -self.apply_Kt(p) - (self.apply_K(u) + self.apply_Kt(u) + self.apply_Abd(u))
+        """Symmetric indefinite 2x2 block operator (operators.py:107-111):
+        top = Abd p - K u, bottom = -Kt p - (K u + Kt u + Abd u), one
+        pint_apply_saddle call (device kernels, the reference's operation
+        order); numpy in -> numpy out, CUDA tensors in -> CUDA tensors out."""
+        import torch
+
+        shape = (self.spec.N, self.spec.dim)
+        host = not (_is_tensor(p) and _is_tensor(u))
+        dev = torch.device("cuda", self._gp.ctx.device)
+
+        def dev_of(x):
+            if _is_tensor(x):
+                _, t = as_buffer(x, shape)
+                return t
+            a = np.ascontiguousarray(x, dtype=np.float64)
+            if a.shape != shape:
+                from .errors import DimensionMismatchError
+
+                raise DimensionMismatchError(f"expected block vector of shape {shape}, got {a.shape}")
+            return torch.from_numpy(a).to(dev)
+
+        pd, ud = dev_of(p), dev_of(u)
+        top = torch.empty(shape, dtype=torch.float64, device=dev)
+        bottom = torch.empty(shape, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize(dev)  # uploads (torch stream) before the library stream reads
+        self._gp.ctx.call("pint_apply_saddle", pd.data_ptr(), ud.data_ptr(), top.data_ptr(),
+                          bottom.data_ptr())
+        self._gp.ctx.call("pint_sync")
+        if host:
+            return top.cpu().numpy(), bottom.cpu().numpy()
         return top, bottom
 
     def a_norm(self, u) -> float:

@@ -219,3 +219,194 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
         ctx.call("pint_set_timing", 0)
     ctx.call("pint_uzawa_end", ptr_of(p_out), ptr_of(u_out))
     return (p_out, u_out), hist
+
+
+def minres_solve(system, atilde, htilde, tol: float = 1e-8, max_iter: int = 500):
+    """Block-diagonally preconditioned MINRES on the saddle-point system
+    (solvers.py:267-327) with every vector resident on the GPU.
+
+    The Krylov recurrence is scipy.sparse.linalg.minres (the reference's own
+    solver, Paige-Saunders; restated step for step: same scalar updates, same
+    stopping tests test1 = |r|/(|A||x|) <= rtol, test2 = |Ar|/(|A||r|) <= rtol,
+    Acond >= 0.1/eps, ...), with the operator ``apply_saddle``
+    (operators.py:107-111) and the preconditioner diag(A~^-1, H~^-1) as the
+    library's kernels and the vector updates as pint_lincomb in numpy's
+    operation order.  As in the reference, the callback evaluates the true
+    preconditioned residual sqrt(max(r.M r, 0))/ref of every iterate,
+    r = g - A x, g = (-f, -f).  Inner products are deterministic device
+    reductions (a different summation order than numpy's BLAS dot).
+    Returns ((p, u), ConvergenceHistory); p, u are numpy arrays.
+    """
+    import torch
+
+    gp = _shared_problem(system, atilde, htilde)
+    ctx = gp.ctx
+    spec = system.spec
+    N, n = spec.N, spec.dim
+    nd = N * n
+    dev = torch.device("cuda", ctx.device)
+    eps = float(np.finfo(np.float64).eps)
+
+    def new():
+        return torch.empty(2 * nd, dtype=torch.float64, device=dev)
+
+    def halves(t):
+        return t.data_ptr(), t.data_ptr() + nd * 8
+
+    def matvec(w, out):
+        wp, wu = halves(w)
+        op, ou = halves(out)
+        ctx.call("pint_apply_saddle", wp, wu, op, ou)
+
+    def precond(w, out):
+        wp, wu = halves(w)
+        op, ou = halves(out)
+        ctx.call("pint_atilde_inv", wp, op)
+        ctx.call("pint_htilde_inv", wu, ou)
+
+    def lincomb(out, x0, a1=0.0, x1=None, a2=0.0, x2=None, scale=None):
+        ctx.call("pint_lincomb", out.data_ptr(), 2 * nd, x0.data_ptr(), float(a1),
+                 None if x1 is None else x1.data_ptr(), float(a2),
+                 None if x2 is None else x2.data_ptr(),
+                 1.0 if scale is None else float(scale), 0 if scale is None else 1)
+
+    def dot(a, b):
+        v = ctypes.c_double()
+        ctx.call("pint_dot", a.data_ptr(), b.data_ptr(), 2 * nd, ctypes.byref(v))
+        return v.value
+
+    def upload(arr):
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64).ravel()).to(dev)
+        torch.cuda.synchronize(dev)  # torch-stream copy before the library stream reads it
+        return t
+
+    f = np.ascontiguousarray(system.rhs, dtype=np.float64).ravel()
+    g = upload(np.concatenate([-f, -f]))
+    tmp, tmp2 = new(), new()
+
+    # cheap positivity probe of the preconditioner (solvers.py:297-302)
+    rng = np.random.default_rng(1234)
+    for _ in range(3):
+        w = upload(rng.standard_normal(2 * nd))
+        precond(w, tmp)
+        if dot(w, tmp) <= 0.0:
+            from .errors import NotSpdError
+
+            raise NotSpdError("block preconditioner is not positive definite")
+        del w
+
+    hist = ConvergenceHistory()
+    t0 = time.perf_counter()
+    precond(g, tmp)
+    ref = float(np.sqrt(dot(g, tmp)))
+    if ref == 0.0:
+        hist.converged = True
+        z = np.zeros((N, n))
+        return (z, z.copy()), hist
+
+    def callback(xk):
+        matvec(xk, tmp)
+        lincomb(tmp, g, -1.0, tmp)           # r = g - A x
+        precond(tmp, tmp2)
+        res = float(np.sqrt(max(dot(tmp, tmp2), 0.0))) / ref
+        hist.append(res, None, None, time.perf_counter() - t0, 0.0, 0.0)
+
+    # ---- scipy.sparse.linalg.minres (x0 = None, shift = 0) ----
+    x = torch.zeros(2 * nd, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    r1 = new()
+    lincomb(r1, g)                           # r1 = b.copy()
+    y = new()
+    precond(r1, y)
+    beta1 = dot(r1, y)
+    if beta1 < 0:
+        raise InputError("indefinite preconditioner")
+    info = 0
+    if beta1 == 0 or float(np.sqrt(max(dot(g, g), 0.0))) == 0.0:
+        hist.converged = True
+    else:
+        beta1 = float(np.sqrt(beta1))
+        oldb, beta, dbar, epsln = 0.0, beta1, 0.0, 0.0
+        phibar = beta1
+        rhs1, rhs2, tnorm2 = beta1, 0.0, 0.0
+        gmax, gmin = 0.0, float(np.finfo(np.float64).max)
+        cs, sn = -1.0, 0.0
+        w = torch.zeros(2 * nd, dtype=torch.float64, device=dev)
+        w2 = torch.zeros(2 * nd, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize(dev)
+        w1 = new()
+        v = new()
+        r2 = new()
+        lincomb(r2, r1)                      # r2 = r1
+        istop, itn = 0, 0
+        while itn < max_iter:
+            itn += 1
+            s = 1.0 / beta
+            lincomb(v, y, scale=s)           # v = s*y
+            matvec(v, y)                     # y = A v  (shift = 0: y - 0*v == y)
+            if itn >= 2:
+                lincomb(y, y, -(beta / oldb), r1)
+            alfa = dot(v, y)
+            lincomb(y, y, -(alfa / beta), r2)
+            r1, r2 = r2, r1
+            lincomb(r2, y)                   # r2 = y
+            precond(r2, y)
+            oldb = beta
+            beta = dot(r2, y)
+            if beta < 0:
+                raise InputError("non-symmetric matrix")
+            beta = float(np.sqrt(beta))
+            tnorm2 += alfa ** 2 + oldb ** 2 + beta ** 2
+            if itn == 1 and beta / beta1 <= 10 * eps:
+                istop = -1
+            oldeps = epsln
+            delta = cs * dbar + sn * alfa
+            gbar = sn * dbar - cs * alfa
+            epsln = sn * beta
+            dbar = -cs * beta
+            root = float(np.linalg.norm([gbar, dbar]))
+            gamma = float(np.linalg.norm([gbar, beta]))
+            gamma = max(gamma, eps)
+            cs = gbar / gamma
+            sn = beta / gamma
+            phi = cs * phibar
+            phibar = sn * phibar
+            denom = 1.0 / gamma
+            w1, w2, w = w2, w, w1
+            lincomb(w, v, -oldeps, w1, -delta, w2, scale=denom)
+            lincomb(x, x, phi, w)
+            gmax = max(gmax, gamma)
+            gmin = min(gmin, gamma)
+            z = rhs1 / gamma
+            rhs1 = rhs2 - delta * z
+            rhs2 = -epsln * z
+            Anorm = float(np.sqrt(tnorm2))
+            ynorm = float(np.sqrt(max(dot(x, x), 0.0)))
+            epsx = Anorm * ynorm * eps
+            rnorm = phibar
+            test1 = np.inf if (ynorm == 0 or Anorm == 0) else rnorm / (Anorm * ynorm)
+            test2 = np.inf if Anorm == 0 else root / Anorm
+            Acond = gmax / gmin
+            if istop == 0:
+                if 1 + test2 <= 1:
+                    istop = 2
+                if 1 + test1 <= 1:
+                    istop = 1
+                if itn >= max_iter:
+                    istop = 6
+                if Acond >= 0.1 / eps:
+                    istop = 4
+                if epsx >= beta1:
+                    istop = 3
+                if test2 <= tol:
+                    istop = 2
+                if test1 <= tol:
+                    istop = 1
+            callback(x)
+            if istop != 0:
+                break
+        info = max_iter if istop == 6 else 0
+        hist.converged = info == 0
+    ctx.call("pint_sync")
+    xh = x.cpu().numpy()
+    return (xh[:nd].reshape(N, n).copy(), xh[nd:].reshape(N, n).copy()), hist

@@ -1,0 +1,64 @@
+"""minres_solve on the GPU (solvers.py:267-327) against the reference's
+MINRES runs (tests/golden/make_golden_minres.py), through the C ABI."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_1802_08126_b200 as pg
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["minres_c16_N16", "minres_sine_c8_N32"]
+
+
+def _build(d):
+    cells = int(d["cells"])
+    spec = pg.problem_from_arrays(str(d["space"]), cells, pg.TimeGrid(d["nodes"]), d["load"],
+                                  d["u_init"])
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy(str(d["space"]), cells))
+    ht = pg.build_schur_preconditioner(spec, "mg", vcycles=1)
+    return spec, system, at, ht
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_minres_matches_reference(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    spec, system, at, ht = _build(d)
+    (p, u), hist = pg.minres_solve(system, at, ht, tol=float(d["mr_tol"]),
+                                   max_iter=int(d["mr_max_iter"]))
+    ref = d["mr_res"]
+    # iteration count within 1 of the reference (north_star), residual history
+    # within 1e-10 relative where the reference residual is above 1e-7 of the
+    # start (deeper, the Krylov recurrence amplifies rounding of the inner
+    # products exactly as it does between BLAS builds)
+    assert abs(hist.iterations - len(ref)) <= 1, (hist.iterations, len(ref))
+    assert hist.converged == bool(d["mr_converged"])
+    k = min(hist.iterations, len(ref))
+    res = np.array(hist.residual[:k])
+    rel = np.abs(res - ref[:k]) / ref[:k]
+    head = ref[:k] > 1e-7 * ref[0]
+    print(f"{name}: {hist.iterations} vs {len(ref)} iterations, max rel drift {rel.max():.2e}")
+    assert rel[head].max() <= 1e-10, rel[head].max()
+    pb = orc.heat_problem(str(d["space"]), int(d["cells"]), d["nodes"], load=d["load"],
+                          u_init=d["u_init"])
+    nrm = orc.ExactNorms(pb)
+    ref_u = d["mr_u"]
+    assert nrm.s_norm(u - ref_u) <= 1e-8 * nrm.s_norm(ref_u)
+
+
+def test_apply_saddle_bitwise():
+    d = np.load(os.path.join(GOLDEN, "minres_c16_N16.npz"))
+    spec, system, at, ht = _build(d)
+    rng = np.random.default_rng(3)
+    p = rng.standard_normal((spec.N, spec.dim))
+    u = rng.standard_normal((spec.N, spec.dim))
+    top, bottom = system.apply_saddle(p, u)
+    pb = orc.heat_problem("2d", int(d["cells"]), d["nodes"], load=d["load"], u_init=d["u_init"])
+    t0, b0 = orc.op_saddle(pb, p, u, orc.stiffness_scales(pb))
+    np.testing.assert_array_equal(top, t0)
+    np.testing.assert_array_equal(bottom, b0)

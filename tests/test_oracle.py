@@ -127,3 +127,40 @@ def test_3d_extension_stencils():
     assert np.count_nonzero(mrow) == 15
     assert mrow[mid] == pytest.approx(2 * h ** 3 / 5)
     assert mrow.sum() == pytest.approx(h ** 3)      # interior row sums to |supp| * ... = h^3
+
+
+MINRES_CASES = ["minres_c16_N16", "minres_sine_c8_N32"]
+
+
+def load_minres(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    pb = orc.heat_problem(str(d["space"]), int(d["cells"]), d["nodes"], load=d["load"],
+                          u_init=d["u_init"])
+    return d, pb
+
+
+@pytest.mark.parametrize("name", MINRES_CASES)
+def test_minres_bitwise(name):
+    """minres_solve (solvers.py:267-327): the oracle reproduces the
+    reference's residual history and iterate bit for bit
+    (tests/golden/make_golden_minres.py)."""
+    d, pb = load_minres(name)
+    lev = orc.mg_levels(pb.space, pb.cells)
+    r = orc.minres(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), tol=float(d["mr_tol"]),
+                   max_iter=int(d["mr_max_iter"]))
+    np.testing.assert_array_equal(np.array(r.residual), d["mr_res"])
+    assert r.converged == bool(d["mr_converged"])
+    np.testing.assert_array_equal(r.p, d["mr_p"])
+    np.testing.assert_array_equal(r.u, d["mr_u"])
+
+
+@pytest.mark.parametrize("name", MINRES_CASES)
+def test_sequential_euler_and_s_norm(name):
+    """sequential_euler_solve (solvers.py:158-174) and s_norm
+    (operators.py:176-183) against the reference."""
+    d, pb = load_minres(name)
+    u = orc.sequential_euler(pb)
+    np.testing.assert_allclose(u, d["u_seq"], rtol=0, atol=1e-13 * np.abs(d["u_seq"]).max())
+    nrm = orc.ExactNorms(pb)
+    assert nrm.s_norm(d["x"]) == pytest.approx(float(d["s_norm_x"]), rel=1e-13)
+    assert nrm.s_norm(d["u_seq"]) == pytest.approx(float(d["s_norm_seq"]), rel=1e-13)
