@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(ZX * ZY)
 
 // x += dinv*(b - S x) (spatial.py:159-160) + the finest-level epilogues
 template <uint32_t PAT>
-__global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 1 : 3) kz_smooth(Smooth3 a) {
+__global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 2 : 3) kz_smooth(Smooth3 a) {
     const ZTile t = ztile(a.m);
     const int m = a.m;
     const long long n = (long long)m * m * m;
