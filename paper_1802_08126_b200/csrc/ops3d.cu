@@ -484,6 +484,43 @@ __device__ __forceinline__ void zmarch(const ZTile& t, int m, const double* __re
     }
 }
 
+// zmarch with one-point-ahead prefetch: the window slice of z+2 and the
+// point values pre(li, valid) of the next point are loaded before the
+// current point is computed, so every thread keeps two iterations of loads
+// in flight (the smoother / residual kernels are latency bound otherwise).
+// post(li, sum, centre, pv) consumes the point values pre returned.
+template <uint32_t PAT, bool SCALED, typename Pre, typename Post>
+__device__ __forceinline__ void zmarch_pf(const ZTile& t, int m, const double* __restrict__ v,
+                                          const double* c, double d, Pre&& pre, Post&& post) {
+    const ZNbr nb = znbr(m, t.x, t.y);
+    const int S = m * m;
+    const int i0 = t.z0 * S + t.y * m + t.x;  // element index of the chunk's first point
+    double w[3][9];
+    zslice<PAT, SCALED>(w[0], v, i0 - S, m, t.z0 >= 1, nb, d);
+    zslice<PAT, SCALED>(w[1], v, i0, m, true, nb, d);
+    zslice<PAT, SCALED>(w[2], v, i0 + S, m, t.z0 + 1 < m, nb, d);
+    auto pv = pre(i0, true);
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) {
+        double wn[9];
+        decltype(pv) pn = pv;
+        if (k + 1 < ZC) {
+            zslice<PAT, SCALED>(wn, v, i0 + (k + 2) * S, m, t.z0 + k + 2 < m, nb, d);
+            pn = pre(i0 + (k + 1) * S, k + 1 < t.zn);
+        }
+        if (k < t.zn) post(i0 + k * S, zsum<PAT>(c, w), w[1][4], pv);
+        if (k + 1 < ZC) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                w[0][q] = w[1][q];
+                w[1][q] = w[2][q];
+                w[2][q] = wn[q];
+            }
+            pv = pn;
+        }
+    }
+}
+
 // out[t] = scale_t * S_t in[t] for planes t in [t0, t0 + gridDim.y) (t0 may be -1:
 // ghost planes); table row per plane: tab + 27 * (sid ? sid[t] : 0)
 template <uint32_t PAT>
@@ -521,12 +558,21 @@ __global__ void __launch_bounds__(ZX * ZY)
     const double sc = __ldg(ascale + pl);
     const long long col = (long long)t.y * m + t.x;
     const bool hp = pl - 1 >= qmin;
-    zmarch<PAT, false>(t, m, p + pl * n, c, 1.0, [&](int, int li, double s, double) {
-        const long long gi = pl * n + li;
-        const double mc = __ldg(mu + gi);
-        const double ku = hp ? mc - __ldg(mu + gi - n) : mc;
-        out[gi] = (ku - sc * s) - __ldg(f + gi);
-    });
+    const double* mup = mu + pl * n;
+    const double* fp = f + pl * n;
+    zmarch_pf<PAT, false>(
+        t, m, p + pl * n, c, 1.0,
+        [&](int li, bool ok) {
+            double3 r;
+            r.x = ok ? __ldg(mup + li) : 0.0;
+            r.y = ok && hp ? __ldg(mup + li - n) : 0.0;
+            r.z = ok ? __ldg(fp + li) : 0.0;
+            return r;
+        },
+        [&](int li, double s, double, double3 pv) {
+            const double ku = hp ? pv.x - pv.y : pv.x;
+            out[pl * n + li] = (ku - sc * s) - pv.z;
+        });
 }
 
 // z = (f - K^T p) - ((K u + K^T u) + s_t A u_t)   (OP_Z of k3_timeop, Mu/Mp precomputed)
@@ -577,7 +623,7 @@ __global__ void __launch_bounds__(ZX * ZY)
 
 // x += dinv*(b - S x) (spatial.py:159-160) + the finest-level epilogues
 template <uint32_t PAT>
-__global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 2 : 3) kz_smooth(Smooth3 a) {
+__global__ void __launch_bounds__(ZX * ZY, 2) kz_smooth(Smooth3 a) {
     const ZTile t = ztile(a.m);
     const int m = a.m;
     const long long n = (long long)m * m * m;
@@ -592,16 +638,26 @@ __global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 2 : 3) kz_smooth(Smo
         const double* xp = a.x + pl * n;
         const double rtau = __ldg(a.rsteps + pl), tau = __ldg(a.steps + pl);
         auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : div_rn(v, tau); };
-        zmarch<PAT, false>(t, m, xp, c, 1.0, [&](int, int li, double s, double xv) {
+        const double* bpl = a.b + pl * n;
+        const double* epl = a.epi == EPI_UZAWA_P ? a.pin + pl * n
+                            : (a.epi == EPI_SCALE_DOT || a.epi == EPI_SCALE_DOTONLY) ? a.aux + pl * n
+                                                                                      : nullptr;
+        auto pre = [&](int li, bool ok) {
+            double2 r;
+            r.x = ok ? __ldg(bpl + li) : 0.0;
+            r.y = ok && epl ? __ldg(epl + li) : 0.0;
+            return r;
+        };
+        auto post = [&](int li, double s, double xv, double2 pv) {
             const long long gi = pl * n + li;
-            const double bv = __ldg(a.b + gi);
+            const double bv = pv.x;
             const double xn = xv + d * (bv - s);
             switch (a.epi) {
                 case EPI_PLAIN: a.out[gi] = xn; break;
                 case EPI_DIV_TAU: a.out[gi] = divtau(xn); break;
                 case EPI_UZAWA_P: {
                     const double dp = divtau(xn);
-                    a.out[gi] = __ldg(a.pin + gi) + dp;
+                    a.out[gi] = pv.y + dp;
                     acc = acc + bv * dp;
                     break;
                 }
@@ -610,12 +666,20 @@ __global__ void __launch_bounds__(ZX * ZY, PAT == PAT_F27 ? 2 : 3) kz_smooth(Smo
                 case EPI_SCALE_DOT: {
                     const double w = a.scale * xn;
                     a.out[gi] = w;
-                    acc = acc + __ldg(a.aux + gi) * w;
+                    acc = acc + pv.y * w;
                     break;
                 }
-                case EPI_SCALE_DOTONLY: acc = acc + __ldg(a.aux + gi) * (a.scale * xn); break;
+                case EPI_SCALE_DOTONLY: acc = acc + pv.y * (a.scale * xn); break;
             }
-        });
+        };
+        if constexpr (PAT == PAT_F27) {
+            // coarse levels: no prefetch (register budget of the 27-point window)
+            zmarch<PAT, false>(t, m, xp, c, 1.0, [&](int, int li, double s, double xv) {
+                post(li, s, xv, pre(li, true));
+            });
+        } else {
+            zmarch_pf<PAT, false>(t, m, xp, c, 1.0, pre, post);
+        }
     }
     if (a.part) {
         const double s = block_sum<ZX * ZY>(acc);
