@@ -192,6 +192,10 @@ __global__ void __launch_bounds__(FX* FY)
 }
 
 // ---- multigrid -----------------------------------------------------------------------
+// x / y out of line, so a select with v * (1/tau) is not if-converted into an
+// unconditional division
+__device__ __noinline__ double fdiv_rn(double x, double y) { return x / y; }
+
 // x0 = dinv * b with dinv = damping / diag  (spatial.py:142, 153)
 template <int MODE>
 __global__ void __launch_bounds__(FT)
@@ -234,9 +238,13 @@ __global__ void __launch_bounds__(FT)
 
 // x = x0 + P e (csr_matvec of P, ascending coarse index); on the last
 // level above the 1x1 coarsest grid e = b_c / a_c (spatial.py:149-150, 157)
+template <bool DIRECT>
 __global__ void __launch_bounds__(FT)
-    k_f_prolong(int m, int mc, const double* __restrict__ ac9, size_t ac_stride, int direct,
+    k_f_prolong(int m, int mc, const double* __restrict__ ac9, size_t ac_stride,
                 const double* __restrict__ ec, double* __restrict__ x) {
+    // DIRECT is a template parameter: a runtime flag lets the compiler
+    // evaluate e / 1.0 speculatively for every term
+    constexpr bool direct = DIRECT;
     const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)n) return;
@@ -297,10 +305,8 @@ __global__ void __launch_bounds__(FT) k_f_smooth(Src A, FSmooth P) {
         const double d = P.damping / coef<MODE>(A, t, 4, m, x, y);
         const double bv = __ldg(P.b + gi);
         const double xn = __ldg(P.x + gi) + d * (bv - frow<MODE>(A, t, P.x + (size_t)t * n, m, x, y));
-        auto divtau = [&](double v) {
-            const double r = __ldg(P.rsteps + t);
-            return r > 0.0 ? v * r : v / __ldg(P.steps + t);
-        };
+        const double rtau = __ldg(P.rsteps + t);
+        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : fdiv_rn(v, __ldg(P.steps + t)); };
         switch (P.epi) {
             case EPI_PLAIN: P.out[gi] = xn; break;
             case EPI_DIV_TAU: P.out[gi] = divtau(xn); break;
@@ -515,8 +521,12 @@ void post_level(pint_ctx* c, const Src& S, const FieldMg& F, int l, int count, c
     const double* ec = direct ? c->lev_b[l + 1] : c->lev_x[l + 1];
     ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE,
                    8.0 * count * (4.0 * m * m + (double)mc * mc));
-    k_f_prolong<<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(
-        m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, direct ? 1 : 0, ec, x);
+    if (direct)
+        k_f_prolong<true><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(
+            m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, ec, x);
+    else
+        k_f_prolong<false><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(
+            m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, ec, x);
     FSmooth P{};
     P.m = m;
     P.b = b;
