@@ -33,6 +33,10 @@
 
 namespace pint {
 
+// x / y out of line: a select between v * (1/tau) and v / tau is otherwise
+// if-converted and the division evaluated for every point
+__device__ __noinline__ double band_div(double x, double y) { return x / y; }
+
 constexpr int BT = 256;       // threads of the band kernels
 constexpr int TT = 512;       // threads of the tail kernel
 
@@ -623,7 +627,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
         const BandView vq = band_view(sq(s), pq, m, y0, y0);
         const double tau = meta[s][PINT_TW];
         const double rtau = meta[s][PINT_TW + 1];  // > 0: tau is a power of two
-        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : v / tau; };
+        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : band_div(v, tau); };
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
             const int x = tid + j * NT;
@@ -818,7 +822,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
         const BandView vq = band_view(sq(s), pq, m, y0, y0);
         const double tau = meta[s][PINT_TW];
         const double rtau = meta[s][PINT_TW + 1];
-        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : v / tau; };
+        auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : band_div(v, tau); };
         if (active) {
             // x += dinv * (b - A x) on rows y0 .. y1-1; padded columns 2t-1 .. 2t+2
             const double* col = sx + 2 * t;
