@@ -306,3 +306,39 @@ def test_band_uzawa_matches_oracle():
     rel = np.abs(np.array(hist.residual) - ref.residual) / np.array(ref.residual)
     assert rel.max() <= 1e-12, rel
     assert np.max(np.abs(u - ref.u)) <= 1e-12 * np.max(np.abs(ref.u))
+
+
+@pytest.mark.parametrize("method", ["uzawa", "minres"])
+def test_cli_solve_problem_file(method, tmp_path):
+    """python -m paper_1802_08126_b200 solve --problem-file (cli.py:131-155)
+    against the reference CLI's CSV on the same reference-written file."""
+    from paper_1802_08126_b200.cli import main
+
+    out = tmp_path / "h.csv"
+    omega = float(np.load(os.path.join(GOLDEN, "problem_c8_N4_omega.npy")))
+    rc = main(["solve", "--problem-file", os.path.join(GOLDEN, "problem_c8_N4.txt"),
+               "--solver", "mg", "--method", method, "--tol", "1e-10", "--max-iter", "300",
+               "--omega", repr(omega), "--out", str(out)])
+    assert rc == 0
+    ours = np.loadtxt(out, delimiter=",", skiprows=1, usecols=(0, 1), ndmin=2)
+    ref = np.loadtxt(os.path.join(GOLDEN, f"problem_c8_N4_{method}.csv"), delimiter=",",
+                     skiprows=1, usecols=(0, 1), ndmin=2)
+    assert abs(len(ours) - len(ref)) <= 1
+    k = min(len(ours), len(ref))
+    rel = np.abs(ours[:k, 1] - ref[:k, 1]) / ref[:k, 1]
+    head = ref[:k, 1] > 1e-7 * ref[0, 1]
+    # bar: 1e-10, or 5x the reference's own FFT-vs-dense DST drift on this case
+    d = np.load(os.path.join(GOLDEN, "problem_c8_N4.npz"))
+    pb = orc.heat_problem("2d", 8, d["nodes"], coeff=lambda t: 1.0 + t, load=d["load"],
+                          u_init=d["u_init"])
+    lev = orc.mg_levels("2d", 8)
+    dense = orc.SchurInv(pb, lev, dense_dst=True)
+    if method == "minres":
+        alt = orc.minres(pb, orc.BlockInv(pb, lev), dense, tol=1e-10, max_iter=300).residual
+    else:
+        alt = orc.uzawa(pb, orc.BlockInv(pb, lev), dense, omega, 1e-10, 300).residual
+    kk = min(k, len(alt))
+    floor = float((np.abs(np.array(alt[:kk]) - ref[:kk, 1]) / ref[:kk, 1])[head[:kk]].max())
+    print(f"{method}: {len(ours)} vs {len(ref)} iterations, drift {rel[head].max():.2e}, "
+          f"reference floor {floor:.2e}")
+    assert rel[head].max() <= max(1e-10, 5 * floor), (rel[head].max(), floor)

@@ -1,0 +1,49 @@
+"""Problem-file I/O (problems.py:300-395) and the CLI entry point against
+files written by the unmodified reference (tests/golden/make_golden_problem_io.py).
+CPU only."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1802_08126_b200 as pg
+from conftest import GOLDEN
+
+FILE = os.path.join(GOLDEN, "problem_c8_N4.txt")
+
+
+def test_load_reference_file():
+    d = np.load(os.path.join(GOLDEN, "problem_c8_N4.npz"))
+    spec = pg.load_problem(FILE)
+    np.testing.assert_array_equal(spec.grid.nodes, d["nodes"])
+    np.testing.assert_array_equal(spec.load, d["load"])
+    np.testing.assert_array_equal(spec.u_init, d["u_init"])
+    assert spec.tau_ref == float(d["tau_ref"]) and spec.alpha == float(d["alpha"])
+    np.testing.assert_array_equal(spec.mass.todense(), d["mass"])
+    np.testing.assert_array_equal(spec.a_ref.todense(), d["a_ref"])
+    np.testing.assert_array_equal(np.stack([a.todense() for a in spec.stiffness]), d["stiff"])
+    assert spec.meta == {"space": "2d", "mesh": 8}
+
+
+def test_save_is_byte_identical(tmp_path):
+    """Our writer reproduces the reference's file byte for byte."""
+    spec = pg.load_problem(FILE)
+    out = tmp_path / "p.txt"
+    pg.save_problem(spec, str(out))
+    assert out.read_bytes() == open(FILE, "rb").read()
+
+
+def test_bad_header(tmp_path):
+    bad = tmp_path / "bad.txt"
+    bad.write_text("not-a-problem\n")
+    with pytest.raises(pg.InputError):
+        pg.load_problem(str(bad))
+
+
+def test_cli_rejects_non_gpu_options():
+    from paper_1802_08126_b200.cli import main
+
+    assert main(["solve", "--solver", "direct"]) == 1
+    assert main(["solve", "--method", "sequential"]) == 1
+    assert main(["solve", "--problem-file", "/nonexistent/file"]) == 1
