@@ -119,6 +119,7 @@ struct DstArgs {
     int debug;  // diagnostic: 1 skip FFT, 2 skip FFT and fold
     const double2* tw;
     const double2* tq;
+    const double2* twp[3];  // k_dst_reg: per-pass twiddles, [s-1][j] contiguous in j
     const double* in;
     double* out;
     const double* base;   // out = base + alpha*T(in) when non-null
@@ -414,10 +415,10 @@ __device__ __forceinline__ void mid_pass(double2* buf, const double2* __restrict
 #pragma unroll
             for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = x[s];
         } else {
-            const double2* w = tw + (j << (LG - LGL));
-            const int dw = j << (LG - LGL);
+            // table [s-1][j]: a warp's lanes read consecutive j (one sector run)
+            const double2* w = tw + j;
 #pragma unroll
-            for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + (s - 1) * dw));
+            for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + ((s - 1) << lgB)));
         }
     }
 }
@@ -522,20 +523,20 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
 #pragma unroll
             for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = x[s];
         } else {
-            const double2* w = a.tw + j;
+            const double2* w = a.twp[0] + j;  // [s-1][j], j < N/16
 #pragma unroll
-            for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + (s - 1) * j));
+            for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + ((s - 1) << lgB)));
         }
     }
     __syncthreads();
     // ---- middle passes ----
     if constexpr (S::np >= 3) {
         constexpr int L2 = LG - 4;
-        mid_pass<S::r1, L2, LG, P, NT>(buf, a.tw);
+        mid_pass<S::r1, L2, LG, P, NT>(buf, a.twp[1]);
         __syncthreads();
         if constexpr (S::np == 4) {
             constexpr int L3 = L2 - ilog2(S::r1);
-            mid_pass<S::r2, L3, LG, P, NT>(buf, a.tw);
+            mid_pass<S::r2, L3, LG, P, NT>(buf, a.twp[2]);
             __syncthreads();
         }
     }
@@ -664,6 +665,7 @@ void dst_plan_free(DstPlan& d) {
     cudaFree(d.tq);
     cudaFree(d.rev);
     cudaFree(d.dense);
+    for (auto* p : d.twp) cudaFree(p);
     d = DstPlan{};
 }
 
@@ -718,6 +720,25 @@ void dst_plan_build(DstPlan& d, int N) {
         // register-radix kernel (k_dst_reg) for 2^8 <= N <= 2^13
         d.reg_lg = (lg >= 8 && lg <= 13 && !getenv("PINT_DST_OLD")) ? lg : 0;
         if (d.reg_lg) {
+            // per-pass twiddle tables W_L^{j s}, stored [s-1][j] (j fastest):
+            // pass 1 L = N, R = 16; middle passes L = N/16 (R = r1), N/(16 r1) (R = r2)
+            const int np = dstreg::sched_np(lg);
+            int L = N, lgL = lg;
+            for (int ps = 0; ps + 1 < np; ++ps) {
+                const int R = dstreg::sched_r(lg, ps);
+                const int B = L / R;
+                std::vector<double2> t((size_t)(R - 1) * B);
+                for (int sidx = 1; sidx < R; ++sidx)
+                    for (int j = 0; j < B; ++j) {
+                        const long double ang = -2.0L * PI * (long double)((long long)j * sidx) / L;
+                        t[(size_t)(sidx - 1) * B + j] = make_double2((double)cosl(ang), (double)sinl(ang));
+                    }
+                PINT_CUDA_CHECK(cudaMalloc(&d.twp[ps], t.size() * sizeof(double2)));
+                PINT_CUDA_CHECK(cudaMemcpy(d.twp[ps], t.data(), t.size() * sizeof(double2),
+                                           cudaMemcpyHostToDevice));
+                L = B;
+                (void)lgL;
+            }
             d.reg_p = dst_reg_pairs(lg);
             if (const char* e = getenv("PINT_DST_P")) {
                 const int want = atoi(e);
@@ -777,6 +798,7 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
     }
     a.n = (int)ncols;
     a.tw = d.tw;
+    for (int q = 0; q < 3; ++q) a.twp[q] = d.twp[q];
     a.tq = d.tq;
     a.in = in;
     a.out = out;

@@ -77,6 +77,7 @@ struct DstPlan {
     int pairs = 0;            // column pairs per CTA
     int reg_lg = 0;           // log2 N when the register-radix kernel runs (0: k_dst_fft)
     int reg_p = 0;            // its column pairs per CTA
+    double2* twp[3] = {nullptr, nullptr, nullptr};  // its per-pass twiddle tables
 };
 
 // kernel families timed individually in profiling mode (pint_profile)
