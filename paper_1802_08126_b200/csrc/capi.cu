@@ -263,8 +263,13 @@ void schur_mode_space(pint_ctx* c, const double* z, double* scratch, int epi, do
     pint::dst_apply(c, 1, z, c->d_w1, nullptr, 1.0);
     rec(c, 2);
     pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w1, c->d_w2, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
-    pint::launch_aref(c, c->d_w2, scratch, c->N);
-    pint::vcycle(c, PINT_MG_HTILDE, c->N, scratch, wout, epi, s, nullptr, c->d_w1, slot);
+    if (pint::vcycle_aref_fusable(c, PINT_MG_HTILDE)) {
+        // b2 = A_ref y1 formed inside the second V-cycle's finest kernels (schur.py:72-73)
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w2, wout, epi, s, nullptr, c->d_w1, slot, true);
+    } else {
+        pint::launch_aref(c, c->d_w2, scratch, c->N);
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, scratch, wout, epi, s, nullptr, c->d_w1, slot);
+    }
     rec(c, 3);
 }
 
@@ -824,9 +829,14 @@ int pint_htilde_modes(pint_ctx* c, const double* zh, double* w, double* dot) {
         const int Ng = c->N_global > 0 ? c->N_global : c->N;
         const double s = 2.0 * c->tau_ref / Ng;  // schur.py:67 with the global N
         pint::vcycle(c, PINT_MG_HTILDE, c->N, zh, c->d_w2, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
-        pint::launch_aref(c, c->d_w2, c->d_z, c->N);
-        pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_z, w, w ? EPI_SCALE_DOT : EPI_SCALE_DOTONLY, s,
-                     nullptr, zh, 1);
+        if (pint::vcycle_aref_fusable(c, PINT_MG_HTILDE)) {
+            pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w2, w, w ? EPI_SCALE_DOT : EPI_SCALE_DOTONLY,
+                         s, nullptr, zh, 1, true);
+        } else {
+            pint::launch_aref(c, c->d_w2, c->d_z, c->N);
+            pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_z, w, w ? EPI_SCALE_DOT : EPI_SCALE_DOTONLY,
+                         s, nullptr, zh, 1);
+        }
         const double v = read_acc(c, 1);
         if (dot) *dot = v;
     });

@@ -157,6 +157,8 @@ constexpr int MAXSTAGE = 4;
 struct PreParams {
     int m, mc, B, Hc, nbands, stages;
     int words_b, words_r;  // smem words: stage b, residual rows
+    int aref;              // b = A_ref y formed on the fly from y = P.b (k_band_pre2<.., AR = 1>)
+    double ar[9];          // A_ref stencil (CSR order), by value
     const double* b;
     double* bc;
     const double* tab;  // level table [n_sets][10]
@@ -188,6 +190,19 @@ __device__ __forceinline__ double win_sum(const double* ca, double a0, double a1
     PINT_W(8, c2)
 #undef PINT_W
     return s;
+}
+
+// 5-point A_ref row sum for the fused mode right-hand side b2 = A_ref y1
+// (schur.py:72) with fused multiply-adds: 5 fp64 instructions instead of 9.
+// Not bit-identical to the separate CSR-order pass (k_band_apply); H~^{-1}
+// carries the sine transforms' rounding anyway (parity bar 1e-12).
+__device__ __forceinline__ double aref5(const double* ar, double s_, double w_, double c_,
+                                        double e_, double n_) {
+    double v = ar[1] * s_;
+    v = __fma_rn(ar[3], w_, v);
+    v = __fma_rn(ar[4], c_, v);
+    v = __fma_rn(ar[5], e_, v);
+    return __fma_rn(ar[7], n_, v);
 }
 
 template <int SH, int NT, int CPT, int HC>
@@ -326,7 +341,13 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
 // x0 = dinv*b (one multiply per loaded value instead of three), stores the
 // pair as one 16-byte word of the padded residual tile, and then restricts
 // coarse column t from padded columns 2t+1 .. 2t+3.
-template <int SH, int NT, int HC>
+//
+// AR = 1 (schur.py:72-73 fused): the right-hand side is b = A_ref y (y = the
+// first mode V-cycle's output) and is never stored.  The stage holds y on one
+// more halo row per side and every b value of the window is the 5-point
+// A_ref row sum (aref5, zero fill as k_band_apply) of a rolling 3-row window
+// of y; k_band_post2<AR = 1> forms the identical values.
+template <int SH, int NT, int HC, int AR = 0>
 __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
@@ -363,8 +384,8 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
                 int plane, Y0, Y1;
                 unit_rows(u, plane, Y0, Y1);
                 const long long pb = plane * n + bob;
-                const int first = 2 * Y0 - 1;
-                const int lo = max(0, first), hi = min(m, 2 * Y1 + 2);
+                const int first = 2 * Y0 - 1 - AR;  // AR: y on one more halo row per side
+                const int lo = max(0, first), hi = min(m, 2 * Y1 + 2 + AR);
                 const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
 #pragma unroll
                 for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
@@ -393,14 +414,52 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
         const double d = meta[s][9];
-        const BandView vb = band_view(smem + s * P.words_b, pb, m, first, lo);
+        const BandView vb = AR ? band_view(smem + s * P.words_b, pb, m, first - 1, max(0, first - 1))
+                               : band_view(smem + s * P.words_b, pb, m, first, lo);
         if (active) {
             // window columns: 0 = 2t-2, 1 = 2t-1 (xa), 2 = 2t (xb), 3 = 2t+1
             const double* bcol = vb.p + 2 * t;
+            // AR: y rows (slot 0 = plane row first-1) at columns 2t-3 .. 2t+2, zero outside
+            double ya[6], yb[6], yc[6];
+            auto yrow = [&](int ys, double* v) {
+                const int gy = first - 1 + ys;
+                const bool in = gy >= 0 && gy < m;
+                const double* row = bcol + ys * m;
+                v[0] = (in && t >= 2) ? row[-3] : 0.0;
+                v[1] = (in && has_l) ? row[-2] : 0.0;
+                v[2] = (in && has_a) ? row[-1] : 0.0;
+                v[3] = in ? row[0] : 0.0;
+                v[4] = (in && has_r) ? row[1] : 0.0;
+                v[5] = (in && has_r) ? row[2] : 0.0;
+            };
+            if (AR) {
+                yrow(0, ya);
+                yrow(1, yb);
+            }
             auto ld = [&](int slot, double& w0, double& w1, double& w2, double& w3, double& ra,
                           double& rb) {
                 const int gy = first + slot;
                 const bool in = gy >= 0 && gy < m;
+                if (AR) {
+                    // b row `slot` from y slots slot .. slot+2 (5-point A_ref, k_band_apply order)
+                    yrow(slot + 2, yc);
+                    double bq[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        bq[i] = aref5(P.ar, ya[i + 1], yb[i], yb[i + 1], yb[i + 2], yc[i + 1]);
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        ya[i] = yb[i];
+                        yb[i] = yc[i];
+                    }
+                    ra = (in && has_a) ? bq[1] : 0.0;
+                    rb = in ? bq[2] : 0.0;
+                    w0 = (in && has_l) ? d * bq[0] : 0.0;
+                    w1 = d * ra;
+                    w2 = d * rb;
+                    w3 = (in && has_r) ? d * bq[3] : 0.0;
+                    return;
+                }
                 const double* row = bcol + slot * m;
                 ra = (in && has_a) ? row[-1] : 0.0;
                 rb = in ? row[0] : 0.0;
@@ -476,6 +535,8 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
 struct PostBandParams {
     int m, mc, B, H, nbands, stages;
     int words_b, words_e, words_q, words_x;  // stage: b, e, pin|aux ; work: padded x
+    int aref;                                // b = A_ref y formed on the fly from y = P.b
+    double ar[9];
     const double* b;
     const double* ec;
     const double* tab;
@@ -687,7 +748,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
 // leaves every sum bit-identical to the ascending-coarse-index csr_matvec of P.
 // The smoothing window is 3 rows x 4 padded columns in registers, reading one
 // 16-byte pair plus two scalars of the padded x tile per row.
-template <int SH, int EPI, int NT, int H>
+// AR = 1: b = A_ref y formed on the fly (see k_band_pre2); the stage holds y
+// on rows y0-2 .. y1+1 and the b values of rows y0-1 .. y1 are kept in
+// registers between the prolongation and the smoothing sweep.
+template <int SH, int EPI, int NT, int H, int AR = 0>
 __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
@@ -736,7 +800,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
                 int plane, y0, y1;
                 unit_rows(u, plane, y0, y1);
                 const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
-                const int fb = y0 - 1, lob = max(0, fb), hib = min(m, y1 + 1);
+                const int fb = y0 - 1 - AR, lob = max(0, fb), hib = min(m, y1 + 1 + AR);
                 const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
                 uint32_t bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
                 if (HAS_Q) bytes += band_bytes(pq, m, y0, y1);
@@ -754,6 +818,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
         return;
     }
     const int t = tid;
+    double bsa[AR ? H + 2 : 1], bsb[AR ? H + 2 : 1];  // AR: b at xa, xb of tile rows 0 .. H+1
     const bool active = t <= mc;
     const bool has_a = t >= 1 && active;   // column xa = 2t-1 exists (and coarse column t-1)
     const bool has_cb = t < mc;            // coarse column t exists
@@ -773,21 +838,50 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
         const double d = meta[s][9];
-        const BandView vb = band_view(sb(s), pb, m, fb, lob);
+        const BandView vb = AR ? band_view(sb(s), pb, m, fb - 1, max(0, fb - 1))
+                               : band_view(sb(s), pb, m, fb, lob);
         const BandView ve = band_view(se(s), pc, mc, fe, loe);
         if (active) {
             // x = dinv*b + P e on tile rows 0 .. nrow+1 (fine rows y0-1 .. y1)
-            const double* brow = vb.p + xb;       // slot r at brow + r*m
+            const double* brow = vb.p + xb;       // slot r at brow + r*m (AR: y slot r+1)
             const double* erow = ve.p + (t - 1);  // coarse column t-1 of slot 0
+            // AR: y rows at columns 2t-2 .. 2t+1 (y slot 0 = fine row y0-2), zero outside
+            double ya[4], yb[4], yc[4];
+            auto yrow = [&](int ys, double* v) {
+                const int gy = fb - 1 + ys;
+                const bool in = gy >= 0 && gy < m;
+                const double* row = brow + ys * m;
+                v[0] = (in && has_a) ? row[-2] : 0.0;
+                v[1] = (in && has_a) ? row[-1] : 0.0;
+                v[2] = in ? row[0] : 0.0;
+                v[3] = (in && has_cb) ? row[1] : 0.0;
+            };
+            if (AR) {
+                yrow(0, ya);
+                yrow(1, yb);
+            }
 #pragma unroll
             for (int r = 0; r < H + 2; ++r) {
                 if (r > nrow + 1) continue;
                 const int gy = fb + r;
                 double xva = 0.0, xvb = 0.0;
+                double b2a = 0.0, b2b = 0.0;
+                if (AR) {
+                    yrow(r + 2, yc);
+                    b2a = aref5(P.ar, ya[1], yb[0], yb[1], yb[2], yc[1]);
+                    b2b = aref5(P.ar, ya[2], yb[1], yb[2], yb[3], yc[2]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        ya[i] = yb[i];
+                        yb[i] = yc[i];
+                    }
+                    bsa[AR ? r : 0] = b2a;
+                    bsb[AR ? r : 0] = b2b;
+                }
                 if (gy >= 0 && gy < m) {
                     const double* bp = brow + r * m;
-                    const double bva = has_a ? bp[-1] : 0.0;
-                    const double bvb = bp[0];
+                    const double bva = has_a ? (AR ? b2a : bp[-1]) : 0.0;
+                    const double bvb = AR ? b2b : bp[0];
                     double pa, pbv;
                     if ((r & 1) == 0) {
                         // odd fine row: one coarse row, slot r/2
@@ -845,8 +939,8 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
                 if (r < nrow) {
                     double c0, c1, c2, c3;
                     ldrow(r + 2, c0, c1, c2, c3);
-                    const double bvb = brow[r * m];
-                    const double bva = has_a ? brow[r * m - 1] : 0.0;
+                    const double bvb = AR ? bsb[AR ? r + 1 : 0] : brow[r * m];
+                    const double bva = has_a ? (AR ? bsa[AR ? r + 1 : 0] : brow[r * m - 1]) : 0.0;
                     const double xna =
                         b1 + d * (bva - win_sum<SH>(ca, a0, a1, a2, b0, b1, b2, c0, c1, c2));
                     const double xnb =
@@ -1154,16 +1248,27 @@ static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int& gr
         launch_pre_h<SH, NT, CPT, 4>(c, P, smem, grid);
 }
 
-template <int SH, int NT, int HC>
-static void launch_pre2_h(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+template <int SH, int NT, int HC, int AR>
+static void launch_pre2_ar(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre2<SH, NT, HC>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre2<SH, NT, HC, AR>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    grid = occupancy_grid(k_band_pre2<SH, NT, HC>, NT + 32, smem, grid);
-    k_band_pre2<SH, NT, HC><<<grid, NT + 32, smem, c->stream>>>(P);
+    grid = occupancy_grid(k_band_pre2<SH, NT, HC, AR>, NT + 32, smem, grid);
+    k_band_pre2<SH, NT, HC, AR><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int NT, int HC>
+static void launch_pre2_h(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+    if (P.aref) {
+        // fused A_ref input: only the mode operators' shapes (mu M + tau A is 7- or 9-point)
+        if constexpr (SH != SH_FIVE) launch_pre2_ar<SH, NT, HC, 1>(c, P, smem, grid);
+        else pint_throw(PINT_INPUT, "fused A_ref input needs a mode-operator level");
+        return;
+    }
+    launch_pre2_ar<SH, NT, HC, 0>(c, P, smem, grid);
 }
 
 template <int SH, int NT>
@@ -1228,16 +1333,30 @@ static int band_rows(int m) {
     return m > 300 ? 4 : 8;
 }
 
-template <int SH, int EPI, int NT, int H>
-static void launch_post2_h(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
+template <int SH, int EPI, int NT, int H, int AR>
+static void launch_post2_ar(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post2<SH, EPI, NT, H>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post2<SH, EPI, NT, H, AR>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    grid = occupancy_grid(k_band_post2<SH, EPI, NT, H>, NT + 32, smem, grid);
-    k_band_post2<SH, EPI, NT, H><<<grid, NT + 32, smem, c->stream>>>(P);
+    grid = occupancy_grid(k_band_post2<SH, EPI, NT, H, AR>, NT + 32, smem, grid);
+    k_band_post2<SH, EPI, NT, H, AR><<<grid, NT + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int EPI, int NT, int H>
+static void launch_post2_h(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
+    if (P.aref) {
+        // fused A_ref input: the second mode V-cycle (schur.py:73) epilogues only
+        if constexpr (SH != SH_FIVE &&
+                      (EPI == EPI_SCALE || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY))
+            launch_post2_ar<SH, EPI, NT, H, 1>(c, P, smem, grid);
+        else
+            pint_throw(PINT_INPUT, "fused A_ref input needs a mode-operator level");
+        return;
+    }
+    launch_post2_ar<SH, EPI, NT, H, 0>(c, P, smem, grid);
 }
 
 // consumer threads of the paired kernel: mc + 1 rounded up to warps
@@ -1315,8 +1434,20 @@ static int blocks_per_sm(size_t smem) {
     return k;
 }
 
+bool vcycle_aref_fusable(const pint_ctx* c, int which) {
+    if (c->dims != 2 || c->field || getenv("PINT_AREF_SEPARATE")) return false;
+    if (!use_pre2() || !use_post2()) return false;
+    const MgSet& s = c->mg[which];
+    if (!s.ready || s.levels < 2 || s.m[0] <= TAIL_MAX_M || s.shape[0] == SH_FIVE) return false;
+    if (c->h_aref.size() != 9) return false;
+    const double* z = c->h_aref.data();
+    return z[0] == 0.0 && z[2] == 0.0 && z[6] == 0.0 && z[8] == 0.0;  // 5-point A_ref
+}
+
 void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
-            double scale, const double* pin, const double* aux, int acc_slot) {
+            double scale, const double* pin, const double* aux, int acc_slot, bool aref_in) {
+    if (aref_in && !vcycle_aref_fusable(c, which))
+        pint_throw(PINT_INPUT, "fused A_ref V-cycle input is not available for this problem");
     if (c->dims == 3) {
         vcycle3(c, which, count, b, out, epi, scale, pin, aux, acc_slot);
         return;
@@ -1342,7 +1473,10 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.B = count;
         P.Hc = band_rows(P.m) / 2;  // coarse rows per unit
         P.nbands = (P.mc + P.Hc - 1) / P.Hc;
-        P.words_b = band_words(2 * P.Hc + 3, P.m);
+        P.aref = (aref_in && l == 0) ? 1 : 0;
+        if (P.aref)
+            for (int q = 0; q < 9; ++q) P.ar[q] = c->h_aref[q];
+        P.words_b = band_words(2 * P.Hc + 3 + 2 * P.aref, P.m);
         P.words_r = use_pre2() ? (2 * P.Hc + 1) * (P.m + 3) : ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
         P.stages = env_int("PINT_STAGES", pick_stages(P.words_b, P.words_r));
         P.b = bl;
@@ -1443,7 +1577,10 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.epi = top ? epi : EPI_PLAIN;
         const bool has_q = P.epi == EPI_UZAWA_P || P.epi == EPI_SCALE_DOT ||
                            P.epi == EPI_SCALE_DOTONLY;
-        P.words_b = band_words(P.H + 2, P.m);
+        P.aref = (aref_in && top) ? 1 : 0;
+        if (P.aref)
+            for (int q = 0; q < 9; ++q) P.ar[q] = c->h_aref[q];
+        P.words_b = band_words(P.H + 2 + 2 * P.aref, P.m);
         P.words_e = band_words(P.H / 2 + 2, P.mc);
         P.words_q = has_q ? band_words(P.H, P.m) : 0;
         P.words_x = (P.H + 2) * (use_post2() ? P.m + 3 : P.m + 2);

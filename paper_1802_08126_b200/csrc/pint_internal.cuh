@@ -211,8 +211,12 @@ void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host,
 // multigrid (mg.cu)
 // V-cycle over planes [0,count) of set `which`; finest post kernel uses `epi`.
 // pin: EPI_UZAWA_P input p;  aux: EPI_SCALE_DOT partner vector; acc_slot: d_acc index
+// aref_in: the right-hand side is A_ref * b, formed inside the finest pre / post
+// kernels (only when vcycle_aref_fusable)
 void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
-            double scale, const double* pin, const double* aux, int acc_slot);
+            double scale, const double* pin, const double* aux, int acc_slot,
+            bool aref_in = false);
+bool vcycle_aref_fusable(const pint_ctx* c, int which);
 void mg_compute_shapes(MgSet& set, const double* tables);
 // 3D (ops3d.cu)
 void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const double* f,

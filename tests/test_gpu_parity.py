@@ -289,6 +289,42 @@ def test_band_levels_bitwise(cells, N):
     assert np.max(np.abs(ht.apply_inverse(x) - href)) <= 1e-12 * np.max(np.abs(href))
 
 
+@pytest.mark.parametrize("cells,N", [(64, 4), (128, 6), (256, 3), (512, 2)])
+def test_fused_aref_vcycle_bitwise(cells, N, monkeypatch):
+    """schur.py:71-73 with b2 = A_ref y1 formed inside the second V-cycle's
+    finest band kernels (k_band_pre2 / k_band_post2 with AR = 1, fused
+    multiply-adds) agrees with the separate CSR-order A_ref pass followed by
+    the V-cycle (PINT_AREF_SEPARATE=1) to 1e-13 relative, output and fused
+    sum zh.w alike (the H~^{-1} bar against the oracle is 1e-12)."""
+    import ctypes
+
+    import torch
+
+    n = (cells - 1) ** 2
+    rng = np.random.default_rng(7 * cells + N)
+    nodes = orc.time_nodes("uniform", N, 0.37)
+    load = rng.standard_normal((N, n))
+    spec = pg.problem_from_arrays("2d", cells, pg.TimeGrid(nodes), load, np.zeros(n),
+                                  coeff=lambda t: 1.0 + t)
+    system = pg.TimeGlobalSystem(spec)
+    pg.build_schur_preconditioner(spec, "mg")
+    ctx = system._gp.ctx
+    zh = torch.from_numpy(rng.standard_normal((N, n))).to("cuda")
+    outs = []
+    for separate in (False, True):
+        if separate:
+            monkeypatch.setenv("PINT_AREF_SEPARATE", "1")
+        w = torch.empty_like(zh)
+        d = ctypes.c_double()
+        ctx.call("pint_htilde_modes", zh.data_ptr(), w.data_ptr(), ctypes.byref(d))
+        torch.cuda.synchronize()
+        outs.append((w.cpu().numpy(), d.value))
+    scale = np.abs(outs[1][0]).max()
+    assert scale > 0 and np.all(np.isfinite(outs[0][0]))
+    assert np.abs(outs[0][0] - outs[1][0]).max() <= 1e-13 * scale
+    assert abs(outs[0][1] - outs[1][1]) <= 1e-13 * abs(outs[1][1])
+
+
 def test_band_uzawa_matches_oracle():
     """A few Uzawa iterations on a band-kernel grid (cells=128) against the oracle."""
     cells, N = 128, 8
