@@ -65,6 +65,15 @@ int pint_sync(pint_ctx* ctx);
  * torch stream; 0 = the legacy default stream); own != 0 restores the
  * context's own stream. */
 int pint_set_stream(pint_ctx* ctx, void* stream, int own);
+/* Arithmetic of the 2D band kernels (time operators, multigrid):
+ * exact != 0: no FMA contraction, every stencil / V-cycle row sum in scipy's
+ *             CSR order, bit-identical to the reference (linalg.py:96-97,
+ *             spatial.py:148-161);
+ * exact == 0: FMA-contracted (the default; <= 1e-15 relative per operator,
+ *             Uzawa histories within the reference's own DST-path noise).
+ * The initial value is taken from the environment variable PINT_EXACT. */
+int pint_set_arith(pint_ctx* ctx, int exact);
+int pint_get_arith(const pint_ctx* ctx);
 
 /* ---------------------------------------------------------------------------
  * Problem: the spatial stencils, step sizes and stiffness scales of one

@@ -23,6 +23,26 @@ from .errors import (
 LIB_PATH = os.environ.get("PINT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpint.so")
 
 PINT_OK, PINT_INPUT, PINT_DIMENSION, PINT_NOT_SPD, PINT_DIVERGED, PINT_CUDA = range(6)
+
+# Arithmetic of the band kernels for contexts created from now on
+# (include/pint.h pint_set_arith): "fast" (FMA, the default) or "exact"
+# (bit-identical to the reference's CSR products).  PINT_ARITH sets the
+# process default.
+_ARITH = os.environ.get("PINT_ARITH", "fast")
+
+
+def set_arithmetic(mode: str) -> str:
+    """Select "fast" or "exact" band-kernel arithmetic for new contexts;
+    returns the previous mode."""
+    global _ARITH
+    if mode not in ("fast", "exact"):
+        raise InputError(f"arithmetic must be 'fast' or 'exact', not {mode!r}")
+    prev, _ARITH = _ARITH, mode
+    return prev
+
+
+def get_arithmetic() -> str:
+    return _ARITH
 MG_ATILDE, MG_HTILDE = 0, 1
 
 _P = ctypes.c_void_p
@@ -38,6 +58,8 @@ _SIGNATURES = {
     "pint_ctx_destroy": (_I, [_P]),
     "pint_last_error": (ctypes.c_char_p, [_P]),
     "pint_sync": (_I, [_P]),
+    "pint_set_arith": (_I, [_P, _I]),
+    "pint_get_arith": (_I, [_P]),
     "pint_set_stream": (_I, [_P, _P, _I]),
     "pint_problem_set": (_I, [_P, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _D]),
     "pint_fold_rhs": (_I, [_P, _P, _P, _P]),
@@ -162,6 +184,8 @@ class Context:
             )
         self.h = h
         self.device = int(device)
+        self.arith = _ARITH
+        self.call("pint_set_arith", 1 if _ARITH == "exact" else 0)
 
     def close(self):
         if getattr(self, "h", None):

@@ -38,33 +38,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 
+// Waits suspend in hardware until the phase completes (suspend-time hint
+// PINT_MBAR_SUSPEND_NS) instead of re-polling: ncu showed the polling loops
+// (try_wait + nanosleep + branch) at 20-30 % of the issued instructions of
+// the band kernels, taken from the compute warps' issue slots.
+#ifndef PINT_MBAR_SUSPEND_NS
+#define PINT_MBAR_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(
         "{\n\t"
         ".reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t"
         "}" ::"r"(smem_u32(bar)),
-        "r"(phase)
+        "r"(phase), "n"(PINT_MBAR_SUSPEND_NS)
         : "memory");
 }
 
-// producer-side wait: back off between polls so a lone producer thread does
-// not take issue slots from the compute warps of its SM sub-partition
+// producer-side wait (same suspend-until-complete wait)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-    uint32_t ok = 0;
-    while (true) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-        if (ok) return;
-        __nanosleep(64);
-    }
+    mbar_wait(bar, phase);
 }
 
 // global -> shared bulk copy completing `bytes` of transaction on `bar`

@@ -316,6 +316,7 @@ int pint_ctx_create(int device, int rank, int world, const void* nccl_id, pint_c
         return PINT_CUDA;
     }
     pint_ctx* c = new pint_ctx();
+    if (const char* e = getenv("PINT_EXACT")) c->exact = atoi(e) != 0;
     c->dev = device;
     c->rank = rank;
     c->world = world;
@@ -367,6 +368,15 @@ int pint_set_stream(pint_ctx* c, void* stream, int own) {
         c->stream = own ? c->own_stream : static_cast<cudaStream_t>(stream);
     });
 }
+
+int pint_set_arith(pint_ctx* c, int exact) {
+    return guarded(c, [&] {
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        c->exact = exact != 0;
+    });
+}
+
+int pint_get_arith(const pint_ctx* c) { return c ? c->exact : -1; }
 
 int pint_profile(pint_ctx* c, int on) {
     return guarded(c, [&] {

@@ -31,7 +31,12 @@
 #include "pint_device.cuh"
 #include "pint_internal.cuh"
 
+#ifndef PINT_VARIANT
+#define PINT_VARIANT exact
+#endif
+
 namespace pint {
+namespace PINT_VARIANT {  // compiled as pint::exact (-fmad=false) and pint::fast (FMA)
 
 // x / y out of line: a select between v * (1/tau) and v / tau is otherwise
 // if-converted and the division evaluated for every point
@@ -1622,4 +1627,5 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
     }
 }
 
+}  // namespace PINT_VARIANT
 }  // namespace pint

@@ -105,6 +105,7 @@ struct HostXfer;
 
 struct pint_ctx {
     int dev = 0, rank = 0, world = 1;
+    int exact = 0;  // 1: bit-exact (no FMA) band kernels; 0: FMA-contracted (pint_set_arith)
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;  // created by the context; `stream` may be a caller's
     std::string err;
@@ -218,6 +219,27 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
             bool aref_in = false);
 bool vcycle_aref_fusable(const pint_ctx* c, int which);
 void mg_compute_shapes(MgSet& set, const double* tables);
+// The 2D band kernels (timeop_band.cu, mg_band.cu) are compiled twice
+// (Makefile): `exact` with -fmad=false (every row sum bit-identical to
+// scipy's CSR products) and `fast` with FMA contraction (<= 1e-15 relative
+// per operator; the default arithmetic, pint_set_arith).  The functions above
+// dispatch on pint_ctx::exact (variant.cu).
+#define PINT_VARIANT_API                                                                          \
+    bool band_timeop_supported(const pint_ctx* c);                                                \
+    void launch_band_timeop(pint_ctx* c, int op, const double* u, const double* p,               \
+                            const double* f, double* out);                                       \
+    void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host,             \
+                           const double* in, double* out, int count);                            \
+    void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,         \
+                double scale, const double* pin, const double* aux, int acc_slot, bool aref_in); \
+    bool vcycle_aref_fusable(const pint_ctx* c, int which);                                      \
+    void mg_compute_shapes(MgSet& set, const double* tables);
+namespace exact {
+PINT_VARIANT_API
+}
+namespace fast {
+PINT_VARIANT_API
+}
 // 3D (ops3d.cu)
 void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                     double* out);

@@ -21,7 +21,12 @@
 #include "pint_device.cuh"
 #include "pint_internal.cuh"
 
+#ifndef PINT_VARIANT
+#define PINT_VARIANT exact
+#endif
+
 namespace pint {
+namespace PINT_VARIANT {  // compiled as pint::exact (-fmad=false) and pint::fast (FMA)
 
 namespace {
 
@@ -766,4 +771,5 @@ void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host,
     PINT_CUDA_CHECK(cudaGetLastError());
 }
 
+}  // namespace PINT_VARIANT
 }  // namespace pint

@@ -1,0 +1,4 @@
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_gpu.log | grep -E "passed|failed|FAILED|Error" 
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 300 python tools/kstats_c2.py 2>&1 | tail -1
+PINT_ARITH=exact timeout 300 python tools/kstats_c2.py 2>&1 | tail -1
