@@ -203,7 +203,13 @@ void free_field(pint_ctx* c) {
     c->fref_ready = false;
 }
 
+void graph_reset(pint_ctx* c) {
+    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+    c->g_exec = nullptr;
+}
+
 void free_problem(pint_ctx* c) {
+    graph_reset(c);
     dfree(c->d_steps);
     dfree(c->d_rsteps);
     c->d_rsteps = nullptr;
@@ -245,7 +251,15 @@ void ensure_levels(pint_ctx* c, const std::vector<int>& m) {
 }
 
 void rec(pint_ctx* c, int i) {
-    if (c->timing) PINT_CUDA_CHECK(cudaEventRecord(c->ev[i], c->stream));
+    // External: inside a captured Uzawa step this becomes a real event-record
+    // node of the graph (a plain record would only be a capture dependency)
+    if (!c->timing) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    PINT_CUDA_CHECK(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+        PINT_CUDA_CHECK(cudaEventRecordWithFlags(c->ev[i], c->stream, cudaEventRecordExternal));
+    else
+        PINT_CUDA_CHECK(cudaEventRecord(c->ev[i], c->stream));
 }
 
 float elapsed(pint_ctx* c, int a, int b) {
@@ -262,11 +276,15 @@ void schur_mode_space(pint_ctx* c, const double* z, double* scratch, int epi, do
     rec(c, 1);
     pint::dst_apply(c, 1, z, c->d_w1, nullptr, 1.0);
     rec(c, 2);
-    pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w1, c->d_w2, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
-    if (pint::vcycle_aref_fusable(c, PINT_MG_HTILDE)) {
-        // b2 = A_ref y1 formed inside the second V-cycle's finest kernels (schur.py:72-73)
-        pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w2, wout, epi, s, nullptr, c->d_w1, slot, true);
+    if (pint::vcycle_aref_fusable(c, PINT_MG_HTILDE) && scratch != wout) {
+        // b2 = A_ref y1 formed inside the second V-cycle's finest kernels
+        // (schur.py:72-73).  y1 is read on halo rows by every band of the
+        // second V-cycle, so it must not share a buffer with that V-cycle's
+        // output: y1 goes to `scratch`, w to `wout`.
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w1, scratch, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, scratch, wout, epi, s, nullptr, c->d_w1, slot, true);
     } else {
+        pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_w1, c->d_w2, EPI_PLAIN, 1.0, nullptr, nullptr, 0);
         pint::launch_aref(c, c->d_w2, scratch, c->N);
         pint::vcycle(c, PINT_MG_HTILDE, c->N, scratch, wout, epi, s, nullptr, c->d_w1, slot);
     }
@@ -366,6 +384,7 @@ int pint_set_stream(pint_ctx* c, void* stream, int own) {
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         // stream 0 is the legacy default stream (torch's default): a valid choice
         c->stream = own ? c->own_stream : static_cast<cudaStream_t>(stream);
+        graph_reset(c);
     });
 }
 
@@ -373,6 +392,7 @@ int pint_set_arith(pint_ctx* c, int exact) {
     return guarded(c, [&] {
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         c->exact = exact != 0;
+        graph_reset(c);
     });
 }
 
@@ -490,6 +510,7 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
                 const double* tables, const int* sid) {
     return guarded(c, [&] {
         require_problem(c);
+        graph_reset(c);
         if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE)
             pint_throw(PINT_INPUT, "unknown multigrid set");
         if (levels < 2 || !level_m || !tables || !sid || n_sets < 1)
@@ -922,6 +943,7 @@ int pint_uzawa_begin(pint_ctx* c, const double* f, const double* p0, const doubl
         dfree(c->d_stage_in);
         dfree(c->d_stage_out);
         c->d_stage_in = c->d_stage_out = nullptr;
+        if (!c->d_f || !c->d_r1 || !c->d_w2) graph_reset(c);  // buffers (re)allocated below
         ensure_uzawa_buffers(c);
         const size_t S = slab(c), bytes = S * sizeof(double);
         copy_in(c, c->d_f, f, bytes);
@@ -943,29 +965,79 @@ int pint_uzawa_begin(pint_ctx* c, const double* f, const double* p0, const doubl
         const double q = c->h_acc[0] + c->h_acc[1];
         c->ref = std::sqrt(q > 0.0 ? q : 0.0);
         c->uz_ready = true;
+        c->uz_steps = 0;
         c->ms_dst = c->ms_mg = c->ms_other = 0.0;
         if (ref_out) *ref_out = c->ref;
     });
 }
 
+// one Uzawa iteration (solvers.py:224-233), stream-ordered, no host sync
+void uzawa_step_enqueue(pint_ctx* c, double omega) {
+    rec(c, 0);
+    // u is not written between the two residuals: the 3D path may reuse M u
+    c->mu3_trust = true;
+    pint::launch_timeop(c, pint::OP_R1, c->d_u, c->d_p, c->d_f, c->d_r1);
+    rec(c, 4);
+    pint::vcycle(c, PINT_MG_ATILDE, c->N, c->d_r1, c->d_p, EPI_UZAWA_P, 1.0, c->d_p, nullptr, 0);
+    rec(c, 5);
+    pint::launch_timeop(c, pint::OP_Z, c->d_u, c->d_p, c->d_f, c->d_z);
+    c->mu3_trust = false;
+    schur_mode_space(c, c->d_z, c->d_z, EPI_SCALE_DOT, c->d_w2, 1);
+    pint::dst_apply(c, 0, c->d_w2, c->d_u, c->d_u, omega);
+    rec(c, 6);
+    PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc, c->d_acc, 2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, c->stream));
+}
+
+bool graphs_enabled() {
+    static const int v = getenv("PINT_NO_GRAPH") ? 0 : 1;
+    return v != 0;
+}
+
+// The ~30 launches of a step are replayed as one CUDA graph: the first step
+// of a solve runs eagerly (it sizes every lazily allocated buffer), the
+// second is captured; the graph lives until the problem, the multigrid
+// tables, the stream or the arithmetic change (graph_reset).
+void uzawa_step_launch(pint_ctx* c, double omega) {
+    const bool want = graphs_enabled() && !c->profile;
+    if (want && c->g_exec && c->g_omega == omega && c->g_timing == c->timing &&
+        c->g_stream == c->stream) {
+        PINT_CUDA_CHECK(cudaGraphLaunch(c->g_exec, c->stream));
+        c->launches += c->g_launches;
+        return;
+    }
+    if (!want || c->uz_steps < 1) {
+        uzawa_step_enqueue(c, omega);
+        return;
+    }
+    graph_reset(c);
+    const long long l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    PINT_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        uzawa_step_enqueue(c, omega);
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+    }
+    PINT_CUDA_CHECK(cudaStreamEndCapture(c->stream, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&c->g_exec, g, 0);
+    cudaGraphDestroy(g);
+    PINT_CUDA_CHECK(ie);
+    c->g_launches = c->launches - l0;
+    c->g_omega = omega;
+    c->g_timing = c->timing;
+    c->g_stream = c->stream;
+    PINT_CUDA_CHECK(cudaGraphLaunch(c->g_exec, c->stream));
+}
+
 int pint_uzawa_step(pint_ctx* c, double omega, double* res_num_out) {
     return guarded(c, [&] {
         if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
-        rec(c, 0);
-        // u is not written between the two residuals: the 3D path may reuse M u
-        c->mu3_trust = true;
-        pint::launch_timeop(c, pint::OP_R1, c->d_u, c->d_p, c->d_f, c->d_r1);
-        rec(c, 4);
-        pint::vcycle(c, PINT_MG_ATILDE, c->N, c->d_r1, c->d_p, EPI_UZAWA_P, 1.0, c->d_p,
-                     nullptr, 0);
-        rec(c, 5);
-        pint::launch_timeop(c, pint::OP_Z, c->d_u, c->d_p, c->d_f, c->d_z);
-        c->mu3_trust = false;
-        schur_mode_space(c, c->d_z, c->d_z, EPI_SCALE_DOT, c->d_w2, 1);
-        pint::dst_apply(c, 0, c->d_w2, c->d_u, c->d_u, omega);
-        rec(c, 6);
-        PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc, c->d_acc, 2 * sizeof(double),
-                                        cudaMemcpyDeviceToHost, c->stream));
+        uzawa_step_launch(c, omega);
+        ++c->uz_steps;
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         pint_prof_drain(c);
         if (c->timing) {

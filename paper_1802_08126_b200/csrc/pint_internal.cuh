@@ -165,6 +165,14 @@ struct pint_ctx {
 
     double ref = 0.0;
     bool uz_ready = false;
+    // CUDA graph of one Uzawa step (pint_uzawa_step), captured on the second
+    // step and replayed while its key (omega, timing, stream) holds
+    cudaGraphExec_t g_exec = nullptr;
+    double g_omega = 0.0;
+    bool g_timing = false;
+    cudaStream_t g_stream = nullptr;
+    long long g_launches = 0;
+    int uz_steps = 0;
 
     // phase timing
     bool timing = false;

@@ -351,6 +351,29 @@ def test_fused_aref_vcycle_bitwise(cells, N, monkeypatch):
     assert abs(outs[0][1] - outs[1][1]) <= 1e-13 * abs(outs[1][1])
 
 
+def test_fused_aref_uzawa_history(monkeypatch):
+    """A full Uzawa solve on a band-kernel grid with the fused A_ref product
+    takes the same iterations as with the separate A_ref pass, residuals
+    within 1e-10 (a regression test: y1 must not share a buffer with the
+    second V-cycle's output, which every band reads on its halo rows)."""
+    cells, N = 256, 128
+    n = (cells - 1) ** 2
+    load = np.random.default_rng(11).standard_normal((N, n))
+    runs = []
+    for separate in (False, True):
+        if separate:
+            monkeypatch.setenv("PINT_AREF_SEPARATE", "1")
+        spec = pg.problem_from_arrays("2d", cells, pg.build_time_grid("uniform", N, 1.0), load,
+                                      np.zeros(n))
+        system = pg.TimeGlobalSystem(spec)
+        at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("2d", cells))
+        ht = pg.build_schur_preconditioner(spec, "mg")
+        _, hist = pg.uzawa_solve(system, at, ht, pg.UzawaConfig(omega=0.9, tol=1e-8))
+        runs.append(np.array(hist.residual))
+    assert len(runs[0]) == len(runs[1]), (len(runs[0]), len(runs[1]))
+    assert np.max(np.abs(runs[0] - runs[1]) / runs[1]) <= 1e-10
+
+
 def test_band_uzawa_matches_oracle():
     """A few Uzawa iterations on a band-kernel grid (cells=128) against the oracle."""
     cells, N = 128, 8
