@@ -163,6 +163,7 @@ struct PreParams {
     int m, mc, B, Hc, nbands, stages;
     int words_b, words_r;  // smem words: stage b, residual rows
     int aref;              // b = A_ref y formed on the fly from y = P.b (k_band_pre2<.., AR = 1>)
+    int ppu;               // planes per unit (k_band_pre2 PPU; 1 or 128 / NT)
     double ar[9];          // A_ref stencil (CSR order), by value
     const double* b;
     double* bc;
@@ -352,23 +353,32 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
 // more halo row per side and every b value of the window is the 5-point
 // A_ref row sum (aref5, zero fill as k_band_apply) of a rolling 3-row window
 // of y; k_band_post2<AR = 1> forms the identical values.
-template <int SH, int NT, int HC, int AR = 0>
-__global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
+//
+// PPU > 1 (narrow levels, NT <= 64 column pairs): one unit is the same band
+// of PPU consecutive planes, consumer warp group pl of the CTA owning plane
+// g*PPU + pl, so a stage carries PPU bands and the per-unit barrier and
+// mbarrier latency is paid once for PPU planes.
+template <int SH, int NT, int HC, int AR = 0, int PPU = 1>
+__global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
-    __shared__ double meta[MAXSTAGE][PINT_TW];
+    __shared__ double meta[MAXSTAGE][PPU][PINT_TW];
     constexpr int RR = 2 * HC + 1;  // residual rows per unit
+    constexpr int NC = NT * PPU;    // consumer threads
     const int m = P.m, mc = P.mc, S = P.stages;
     const int mp = m + 3;           // padded residual pitch (even): fine x at index x+1
     const long long n = (long long)m * m, nc = (long long)mc * mc;
-    double* sr = smem + S * P.words_b;  // RR x mp
-    const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
+    const int pl = tid < NC ? tid / NT : 0;  // plane of the unit this consumer works on
+    double* sr = smem + S * PPU * P.words_b + pl * P.words_r;  // RR x mp
+    const int groups = (P.B + PPU - 1) / PPU;
+    const int units = groups * P.nbands;
     const int bob = (int)((reinterpret_cast<uintptr_t>(P.b) >> 3) & 1);
     const double* gb = P.b - bob;
-    auto unit_rows = [&](int u, int& plane, int& Y0, int& Y1) {
-        plane = u / P.nbands;
-        const int j = u - plane * P.nbands;
+    auto stage_b = [&](int s, int q) { return smem + (s * PPU + q) * P.words_b; };
+    auto unit_rows = [&](int u, int& g, int& Y0, int& Y1) {
+        g = u / P.nbands;
+        const int j = u - g * P.nbands;
         Y0 = j * HC;
         Y1 = min(mc, Y0 + HC);
     };
@@ -380,36 +390,48 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
         fence_barrier_init();
     }
     __syncthreads();
-    if (tid >= NT) {  // ---- producer warp (as k_band_pre) ----
-        if (tid == NT) {
+    if (tid >= NC) {  // ---- producer warp (as k_band_pre) ----
+        if (tid == NC) {
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
                 if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
-                int plane, Y0, Y1;
-                unit_rows(u, plane, Y0, Y1);
-                const long long pb = plane * n + bob;
+                int g, Y0, Y1;
+                unit_rows(u, g, Y0, Y1);
                 const int first = 2 * Y0 - 1 - AR;  // AR: y on one more halo row per side
                 const int lo = max(0, first), hi = min(m, 2 * Y1 + 2 + AR);
-                const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+                uint32_t bytes = 0;
+                for (int q = 0; q < PPU; ++q) {
+                    const int plane = g * PPU + q;
+                    if (plane >= P.B) break;
+                    const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
 #pragma unroll
-                for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
-                mbar_expect_tx(&full[s], band_bytes(pb, m, lo, hi));
-                band_issue(smem + s * P.words_b, gb, pb, m, first, lo, hi, &full[s]);
+                    for (int w = 0; w < PINT_TW; ++w) meta[s][q][w] = __ldg(tb + w);
+                    bytes += band_bytes(plane * n + bob, m, lo, hi);
+                }
+                mbar_expect_tx(&full[s], bytes);
+                for (int q = 0; q < PPU; ++q) {
+                    const int plane = g * PPU + q;
+                    if (plane >= P.B) break;
+                    band_issue(stage_b(s, q), gb, plane * n + bob, m, first, lo, hi, &full[s]);
+                }
             }
         }
         return;
     }
-    const int t = tid;
-    const bool active = t <= mc;
+    const int t = tid - pl * NT;
+    const bool tcol = t <= mc;
     const bool has_a = t >= 1;          // fine column 2t-1 exists
     const bool has_l = t >= 1;          // fine column 2t-2 exists
     const bool has_r = t < mc;          // fine column 2t+1 exists
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
         const int s = k % S;
-        int plane, Y0, Y1;
-        unit_rows(u, plane, Y0, Y1);
+        int g, Y0, Y1;
+        unit_rows(u, g, Y0, Y1);
+        const int plane = g * PPU + pl;
+        const bool pok = PPU == 1 || plane < P.B;
+        const bool active = tcol && pok;
         const long long pb = plane * n + bob;
         const int first = 2 * Y0 - 1;
         const int lo = max(0, first);
@@ -417,10 +439,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
         mbar_wait(&full[s], (k / S) & 1);
         double ca[9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
-        const double d = meta[s][9];
-        const BandView vb = AR ? band_view(smem + s * P.words_b, pb, m, first - 1, max(0, first - 1))
-                               : band_view(smem + s * P.words_b, pb, m, first, lo);
+        for (int q = 0; q < 9; ++q) ca[q] = meta[s][pl][q];
+        const double d = meta[s][pl][9];
+        const BandView vb = AR ? band_view(stage_b(s, pl), pb, m, first - 1, max(0, first - 1))
+                               : band_view(stage_b(s, pl), pb, m, first, lo);
         if (active) {
             // window columns: 0 = 2t-2, 1 = 2t-1 (xa), 2 = 2t (xb), 3 = 2t+1
             const double* bcol = vb.p + 2 * t;
@@ -493,12 +515,12 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
                 }
             }
         }
-        consumer_sync<NT>();
+        consumer_sync<NC>();
         if (tid == 0) mbar_arrive(&empty[s]);  // stage s fully consumed
         // restriction: P^T r, ascending fine index (csc_matvec order);
         // coarse X = t reads fine columns 2X .. 2X+2 = padded 2X+1 .. 2X+3
         const int ncr = Y1 - Y0;
-        if (t < mc) {
+        if (t < mc && pok) {
             const double* col = sr + 2 * t;
             auto ld3 = [&](int row, double& v0, double& v1, double& v2) {
                 const double* q = col + row * mp;
@@ -530,7 +552,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre2(PreParams P) {
                 }
             }
         }
-        consumer_sync<NT>();
+        consumer_sync<NC>();
     }
 }
 
@@ -541,6 +563,7 @@ struct PostBandParams {
     int m, mc, B, H, nbands, stages;
     int words_b, words_e, words_q, words_x;  // stage: b, e, pin|aux ; work: padded x
     int aref;                                // b = A_ref y formed on the fly from y = P.b
+    int ppu;                                 // planes per unit (k_band_post2 PPU)
     double ar[9];
     const double* b;
     const double* ec;
@@ -756,20 +779,23 @@ __global__ void __launch_bounds__(NT + 32) k_band_post(PostBandParams P) {
 // AR = 1: b = A_ref y formed on the fly (see k_band_pre2); the stage holds y
 // on rows y0-2 .. y1+1 and the b values of rows y0-1 .. y1 are kept in
 // registers between the prolongation and the smoothing sweep.
-template <int SH, int EPI, int NT, int H, int AR = 0>
-__global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
+// PPU > 1: PPU planes per unit, as in k_band_pre2.
+template <int SH, int EPI, int NT, int H, int AR = 0, int PPU = 1>
+__global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) {
+    constexpr int NC = NT * PPU;  // consumer threads
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
-    __shared__ double meta[MAXSTAGE][PINT_TW + 2];
-    __shared__ double red[NT / 32 > 0 ? NT / 32 : 1];
+    __shared__ double meta[MAXSTAGE][PPU][PINT_TW + 2];
+    __shared__ double red[NC / 32 > 0 ? NC / 32 : 1];
     static_assert(H % 2 == 0, "bands start at even rows");
     const int m = P.m, mc = P.mc, S = P.stages;
     const int mp = m + 3;  // even pitch: padded column c sits at index c, pairs are 16-byte aligned
     const long long n = (long long)m * m, nc = (long long)mc * mc;
     const int wstage = P.words_b + P.words_e + P.words_q;
-    double* sx = smem + S * wstage;  // (H+2) x mp, zero-padded columns 0 and m+1
-    const int units = P.B * P.nbands;
     const int tid = threadIdx.x;
+    const int pl = tid < NC ? tid / NT : 0;  // plane of the unit this consumer works on
+    double* sx = smem + S * PPU * wstage + pl * P.words_x;  // (H+2) x mp, zero-padded columns 0 and m+1
+    const int units = (P.B + PPU - 1) / PPU * P.nbands;
     const double* qsrc0 = EPI == EPI_UZAWA_P ? P.pin : P.aux;
     const int bob = (int)((reinterpret_cast<uintptr_t>(P.b) >> 3) & 1);
     const int boe = (int)((reinterpret_cast<uintptr_t>(P.ec) >> 3) & 1);
@@ -778,12 +804,12 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
     constexpr bool HAS_DOT =
         EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU || EPI == EPI_SCALE_DOT || EPI == EPI_SCALE_DOTONLY;
     constexpr bool HAS_TAU = EPI == EPI_DIV_TAU || EPI == EPI_UZAWA_P || EPI == EPI_DOT_TAU;
-    auto sb = [&](int s) { return smem + s * wstage; };
-    auto se = [&](int s) { return smem + s * wstage + P.words_b; };
-    auto sq = [&](int s) { return smem + s * wstage + P.words_b + P.words_e; };
-    auto unit_rows = [&](int u, int& plane, int& y0, int& y1) {
-        plane = u / P.nbands;
-        const int j = u - plane * P.nbands;
+    auto sb = [&](int s, int q) { return smem + (s * PPU + q) * wstage; };
+    auto se = [&](int s, int q) { return smem + (s * PPU + q) * wstage + P.words_b; };
+    auto sq = [&](int s, int q) { return smem + (s * PPU + q) * wstage + P.words_b + P.words_e; };
+    auto unit_rows = [&](int u, int& g, int& y0, int& y1) {
+        g = u / P.nbands;
+        const int j = u - g * P.nbands;
         y0 = j * H;
         y1 = min(m, y0 + H);
     };
@@ -794,46 +820,61 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
         }
         fence_barrier_init();
     }
-    for (int i = tid; i < P.words_x; i += NT + 32) sx[i] = 0.0;
+    {
+        double* sx0 = smem + S * PPU * wstage;
+        for (int i = tid; i < PPU * P.words_x; i += NC + 32) sx0[i] = 0.0;
+    }
     __syncthreads();
-    if (tid >= NT) {  // ---- producer warp (as k_band_post) ----
-        if (tid == NT) {
+    if (tid >= NC) {  // ---- producer warp (as k_band_post) ----
+        if (tid == NC) {
             int k = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
                 const int s = k % S;
                 if (k >= S) mbar_wait_sleep(&empty[s], ((k / S) - 1) & 1);
-                int plane, y0, y1;
-                unit_rows(u, plane, y0, y1);
-                const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
+                int g, y0, y1;
+                unit_rows(u, g, y0, y1);
                 const int fb = y0 - 1 - AR, lob = max(0, fb), hib = min(m, y1 + 1 + AR);
                 const int fe = y0 / 2 - 1, loe = max(0, fe), hie = min(mc, y1 / 2 + 1);
-                uint32_t bytes = band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
-                if (HAS_Q) bytes += band_bytes(pq, m, y0, y1);
-                const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
+                uint32_t bytes = 0;
+                for (int q = 0; q < PPU; ++q) {
+                    const int plane = g * PPU + q;
+                    if (plane >= P.B) break;
+                    const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
+                    bytes += band_bytes(pb, m, lob, hib) + band_bytes(pc, mc, loe, hie);
+                    if (HAS_Q) bytes += band_bytes(pq, m, y0, y1);
+                    const double* tb = P.tab + (size_t)__ldg(P.sid + plane) * PINT_TW;
 #pragma unroll
-                for (int q = 0; q < PINT_TW; ++q) meta[s][q] = __ldg(tb + q);
-                meta[s][PINT_TW] = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
-                meta[s][PINT_TW + 1] = HAS_TAU ? __ldg(P.rsteps + plane) : 0.0;
+                    for (int w = 0; w < PINT_TW; ++w) meta[s][q][w] = __ldg(tb + w);
+                    meta[s][q][PINT_TW] = HAS_TAU ? __ldg(P.steps + plane) : 1.0;
+                    meta[s][q][PINT_TW + 1] = HAS_TAU ? __ldg(P.rsteps + plane) : 0.0;
+                }
                 mbar_expect_tx(&full[s], bytes);
-                band_issue(sb(s), P.b - bob, pb, m, fb, lob, hib, &full[s]);
-                band_issue(se(s), P.ec - boe, pc, mc, fe, loe, hie, &full[s]);
-                if (HAS_Q) band_issue(sq(s), qsrc0 - boq, pq, m, y0, y0, y1, &full[s]);
+                for (int q = 0; q < PPU; ++q) {
+                    const int plane = g * PPU + q;
+                    if (plane >= P.B) break;
+                    const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
+                    band_issue(sb(s, q), P.b - bob, pb, m, fb, lob, hib, &full[s]);
+                    band_issue(se(s, q), P.ec - boe, pc, mc, fe, loe, hie, &full[s]);
+                    if (HAS_Q) band_issue(sq(s, q), qsrc0 - boq, pq, m, y0, y0, y1, &full[s]);
+                }
             }
         }
         return;
     }
-    const int t = tid;
+    const int t = tid - pl * NT;
     double bsa[AR ? H + 2 : 1], bsb[AR ? H + 2 : 1];  // AR: b at xa, xb of tile rows 0 .. H+1
-    const bool active = t <= mc;
-    const bool has_a = t >= 1 && active;   // column xa = 2t-1 exists (and coarse column t-1)
+    const bool tcol = t <= mc;
     const bool has_cb = t < mc;            // coarse column t exists
     const int xa = 2 * t - 1, xb = 2 * t;
     double acc = 0.0;
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
         const int s = k % S;
-        int plane, y0, y1;
-        unit_rows(u, plane, y0, y1);
+        int g, y0, y1;
+        unit_rows(u, g, y0, y1);
+        const int plane = g * PPU + pl;
+        const bool active = tcol && (PPU == 1 || plane < P.B);
+        const bool has_a = t >= 1 && active;   // column xa = 2t-1 exists (and coarse column t-1)
         const long long pb = plane * n + bob, pc = plane * nc + boe, pq = plane * n + boq;
         const int fb = y0 - 1, lob = max(0, fb);
         const int fe = y0 / 2 - 1, loe = max(0, fe);
@@ -841,11 +882,11 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
         mbar_wait(&full[s], (k / S) & 1);
         double ca[9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) ca[q] = meta[s][q];
-        const double d = meta[s][9];
-        const BandView vb = AR ? band_view(sb(s), pb, m, fb - 1, max(0, fb - 1))
-                               : band_view(sb(s), pb, m, fb, lob);
-        const BandView ve = band_view(se(s), pc, mc, fe, loe);
+        for (int q = 0; q < 9; ++q) ca[q] = meta[s][pl][q];
+        const double d = meta[s][pl][9];
+        const BandView vb = AR ? band_view(sb(s, pl), pb, m, fb - 1, max(0, fb - 1))
+                               : band_view(sb(s, pl), pb, m, fb, lob);
+        const BandView ve = band_view(se(s, pl), pc, mc, fe, loe);
         if (active) {
             // x = dinv*b + P e on tile rows 0 .. nrow+1 (fine rows y0-1 .. y1)
             const double* brow = vb.p + xb;       // slot r at brow + r*m (AR: y slot r+1)
@@ -917,10 +958,10 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
                 *reinterpret_cast<double2*>(sx + r * mp + 2 * t) = make_double2(xva, xvb);
             }
         }
-        consumer_sync<NT>();
-        const BandView vq = band_view(sq(s), pq, m, y0, y0);
-        const double tau = meta[s][PINT_TW];
-        const double rtau = meta[s][PINT_TW + 1];
+        consumer_sync<NC>();
+        const BandView vq = band_view(sq(s, pl), pq, m, y0, y0);
+        const double tau = meta[s][pl][PINT_TW];
+        const double rtau = meta[s][pl][PINT_TW + 1];
         auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : band_div(v, tau); };
         if (active) {
             // x += dinv * (b - A x) on rows y0 .. y1-1; padded columns 2t-1 .. 2t+2
@@ -980,11 +1021,11 @@ __global__ void __launch_bounds__(NT + 32) k_band_post2(PostBandParams P) {
                 }
             }
         }
-        consumer_sync<NT>();
+        consumer_sync<NC>();
         if (tid == 0) mbar_arrive(&empty[s]);
     }
     if (HAS_DOT) {
-        const double sum = consumer_sum<NT>(acc, red);
+        const double sum = consumer_sum<NC>(acc, red);
         if (tid == 0) P.part[blockIdx.x] = sum;
     }
 }
@@ -1197,7 +1238,7 @@ static int num_sms() {
     return g_num_sms;
 }
 
-constexpr int TAIL_MAX_M = 31;  // m = 63 runs through the band kernels
+constexpr int TAIL_MAX_M_DEFAULT = 31;  // m = 63 runs through the band kernels
 
 // shapes of the level tables: a position is skipped only if it is exactly 0
 // for every set of the level
@@ -1219,6 +1260,12 @@ void mg_compute_shapes(MgSet& set, const double* tab) {
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return v ? atoi(v) : dflt;
+}
+
+// largest level handled by the shared-memory tail kernel (PINT_TAIL_MAX_M)
+static int tail_max_m() {
+    static const int v = env_int("PINT_TAIL_MAX_M", TAIL_MAX_M_DEFAULT);
+    return v;
 }
 
 // persistent grid: as many CTAs as are co-resident (registers and shared
@@ -1253,16 +1300,34 @@ static void launch_pre_cfg(pint_ctx* c, const PreParams& P, size_t smem, int& gr
         launch_pre_h<SH, NT, CPT, 4>(c, P, smem, grid);
 }
 
-template <int SH, int NT, int HC, int AR>
-static void launch_pre2_ar(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+// planes per unit of the narrow band levels (k_band_pre2 / k_band_post2, PPU);
+// PINT_PPU=1 restores one plane per unit
+static int planes_per_unit(int nt) {
+    static const int off = getenv("PINT_PPU") ? atoi(getenv("PINT_PPU")) == 1 : 0;
+    return (nt <= 64 && !off) ? 128 / nt : 1;
+}
+
+template <int SH, int NT, int HC, int AR, int PPU>
+static void launch_pre2_ppu(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre2<SH, NT, HC, AR>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_pre2<SH, NT, HC, AR, PPU>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    grid = occupancy_grid(k_band_pre2<SH, NT, HC, AR>, NT + 32, smem, grid);
-    k_band_pre2<SH, NT, HC, AR><<<grid, NT + 32, smem, c->stream>>>(P);
+    grid = occupancy_grid(k_band_pre2<SH, NT, HC, AR, PPU>, NT * PPU + 32, smem, grid);
+    k_band_pre2<SH, NT, HC, AR, PPU><<<grid, NT * PPU + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int NT, int HC, int AR>
+static void launch_pre2_ar(pint_ctx* c, const PreParams& P, size_t smem, int& grid) {
+    if constexpr (NT <= 64) {
+        if (P.ppu > 1) {
+            launch_pre2_ppu<SH, NT, HC, AR, 128 / NT>(c, P, smem, grid);
+            return;
+        }
+    }
+    launch_pre2_ppu<SH, NT, HC, AR, 1>(c, P, smem, grid);
 }
 
 template <int SH, int NT, int HC>
@@ -1338,16 +1403,27 @@ static int band_rows(int m) {
     return m > 300 ? 4 : 8;
 }
 
-template <int SH, int EPI, int NT, int H, int AR>
-static void launch_post2_ar(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
+template <int SH, int EPI, int NT, int H, int AR, int PPU>
+static void launch_post2_ppu(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
     static bool attr = false;
     if (!attr) {
-        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post2<SH, EPI, NT, H, AR>,
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(k_band_post2<SH, EPI, NT, H, AR, PPU>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    grid = occupancy_grid(k_band_post2<SH, EPI, NT, H, AR>, NT + 32, smem, grid);
-    k_band_post2<SH, EPI, NT, H, AR><<<grid, NT + 32, smem, c->stream>>>(P);
+    grid = occupancy_grid(k_band_post2<SH, EPI, NT, H, AR, PPU>, NT * PPU + 32, smem, grid);
+    k_band_post2<SH, EPI, NT, H, AR, PPU><<<grid, NT * PPU + 32, smem, c->stream>>>(P);
+}
+
+template <int SH, int EPI, int NT, int H, int AR>
+static void launch_post2_ar(pint_ctx* c, const PostBandParams& P, size_t smem, int& grid) {
+    if constexpr (NT <= 64) {
+        if (P.ppu > 1) {
+            launch_post2_ppu<SH, EPI, NT, H, AR, 128 / NT>(c, P, smem, grid);
+            return;
+        }
+    }
+    launch_post2_ppu<SH, EPI, NT, H, AR, 1>(c, P, smem, grid);
 }
 
 template <int SH, int EPI, int NT, int H>
@@ -1443,7 +1519,7 @@ bool vcycle_aref_fusable(const pint_ctx* c, int which) {
     if (c->dims != 2 || c->field || getenv("PINT_AREF_SEPARATE")) return false;
     if (!use_pre2() || !use_post2()) return false;
     const MgSet& s = c->mg[which];
-    if (!s.ready || s.levels < 2 || s.m[0] <= TAIL_MAX_M || s.shape[0] == SH_FIVE) return false;
+    if (!s.ready || s.levels < 2 || s.m[0] <= tail_max_m() || s.shape[0] == SH_FIVE) return false;
     if (c->h_aref.size() != 9) return false;
     const double* z = c->h_aref.data();
     return z[0] == 0.0 && z[2] == 0.0 && z[6] == 0.0 && z[8] == 0.0;  // 5-point A_ref
@@ -1466,7 +1542,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
     const int L = s.levels;
     auto lvl_tab = [&](int l) { return s.tab + (size_t)l * s.n_sets * PINT_TW; };
     int lt = 0;
-    while (lt < L && s.m[lt] > TAIL_MAX_M) ++lt;
+    while (lt < L && s.m[lt] > tail_max_m()) ++lt;
     const int sms = num_sms();
     const bool dot = epi_has_dot(epi);
     // ---- descend through the band levels ----
@@ -1484,13 +1560,14 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_b = band_words(2 * P.Hc + 3 + 2 * P.aref, P.m);
         P.words_r = use_pre2() ? (2 * P.Hc + 1) * (P.m + 3) : ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
         P.stages = env_int("PINT_STAGES", pick_stages(P.words_b, P.words_r));
+        P.ppu = use_pre2() ? planes_per_unit(pair_threads(P.m)) : 1;
         P.b = bl;
         P.bc = c->lev_b[l + 1];
         P.tab = lvl_tab(l);
         P.sid = s.sid;
-        const size_t smem = sizeof(double) * (P.stages * P.words_b + P.words_r);
-        const int units = P.B * P.nbands;
-        int grid = std::min(units, sms * 8);
+        const size_t smem = sizeof(double) * P.ppu * (P.stages * P.words_b + P.words_r);
+        const int units = (P.B + P.ppu - 1) / P.ppu * P.nbands;
+        int grid = std::min(units, sms * (l == 0 ? 8 : env_int("PINT_COARSE_CTAS", 8)));
         ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
                        8.0 * count * ((double)P.m * P.m + (double)P.mc * P.mc));
         switch (s.shape[l]) {
@@ -1590,6 +1667,7 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.words_q = has_q ? band_words(P.H, P.m) : 0;
         P.words_x = (P.H + 2) * (use_post2() ? P.m + 3 : P.m + 2);
         P.stages = env_int("PINT_STAGES", pick_stages(P.words_b + P.words_e + P.words_q, P.words_x));
+        P.ppu = use_post2() ? planes_per_unit(post2_threads(P.m)) : 1;
         P.b = top ? b : c->lev_b[l];
         P.ec = c->lev_x[l + 1];
         P.tab = lvl_tab(l);
@@ -1601,9 +1679,9 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.pin = pin;
         P.aux = aux;
         const size_t smem =
-            sizeof(double) * (P.stages * (P.words_b + P.words_e + P.words_q) + P.words_x);
-        const int units = P.B * P.nbands;
-        int grid = std::min(units, sms * 8);
+            sizeof(double) * P.ppu * (P.stages * (P.words_b + P.words_e + P.words_q) + P.words_x);
+        const int units = (P.B + P.ppu - 1) / P.ppu * P.nbands;
+        int grid = std::min(units, sms * (l == 0 ? 8 : env_int("PINT_COARSE_CTAS", 8)));
         const bool dl = top && dot;
         if (dl) {
             ensure_partials(c, grid);
