@@ -5,8 +5,9 @@
 ``apply_saddle``) with the arithmetic done by the sm_100a kernels of
 csrc/stencil_ops.cu: block vectors of shape (N, dim), numpy (host) or CUDA
 float64 torch tensors (device), results of the same kind.  Diagnostic-mode
-operators (exact per-step inverses, S-norm, P, S; operators.py:51-214) need
-sparse factorisations and are not on the GPU path.
+operators (exact per-step inverses, S-norm, P, S; operators.py:51-214) are
+the reference's host-side SuperLU computations (diagnostics.py); they serve
+error measurement, never the iteration.
 """
 
 from __future__ import annotations
@@ -16,6 +17,10 @@ import numpy as np
 from ._device import gpu_problem
 from ._native import _is_tensor, as_buffer, empty_like_kind, ptr_of
 from .errors import DiagnosticModeRequiredError
+
+
+def _host(x) -> np.ndarray:
+    return x.detach().cpu().numpy() if _is_tensor(x) else np.asarray(x, dtype=np.float64)
 
 
 def fold_rhs(spec) -> np.ndarray:
@@ -32,21 +37,59 @@ class TimeGlobalSystem:
     """The time-global implicit-Euler system of one ProblemSpec, on the GPU."""
 
     def __init__(self, spec, diagnostic: bool = False, device=None):
-        if diagnostic:
-            raise DiagnosticModeRequiredError(
-                "exact per-step factorizations are not part of the GPU path")
         self.spec = spec
         self._gp = gpu_problem(spec, device)
         self.rhs = fold_rhs(spec)
         self._scales = self._gp.scales
+        self._exact = None
+        if diagnostic:
+            self.build_exact_solvers()
 
     @property
     def diagnostic(self) -> bool:
-        return False
+        return self._exact is not None
 
     def build_exact_solvers(self) -> None:
-        raise DiagnosticModeRequiredError(
-            "exact per-step factorizations are not part of the GPU path")
+        """Exact per-step factorisations on the host (operators.py:51-61)."""
+        if self._exact is None:
+            from .diagnostics import ExactNorms
+
+            self._exact = ExactNorms(self.spec)
+
+    def _need_exact(self):
+        if self._exact is None:
+            raise DiagnosticModeRequiredError(
+                "exact per-step factorizations not built; pass diagnostic=True")
+        return self._exact
+
+    # --- diagnostic-mode operators and norms (operators.py:113-183) --------
+    def apply_Abd_inv(self, b):
+        return self._need_exact().apply_Abd_inv(_host(b))
+
+    def apply_P(self, u):
+        """Optimal-test-function map (operators.py:124-126)."""
+        return self.apply_Abd_inv(self.apply_K(_host(u))) + _host(u)
+
+    def apply_Pt(self, u):
+        return self.apply_Kt(self.apply_Abd_inv(_host(u))) + _host(u)
+
+    def apply_S(self, u):
+        """Schur complement operator (operators.py:131-139)."""
+        u = _host(u)
+        ku = self.apply_K(u)
+        return self.apply_Kt(self.apply_Abd_inv(ku)) + ku + self.apply_Kt(u) + self.apply_Abd(u)
+
+    def a_norm(self, u) -> float:
+        return self._need_exact().a_norm(_host(u))
+
+    def jump_form(self, u, v) -> float:
+        return self._need_exact().jump_form(_host(u), _host(v))
+
+    def s_bilinear(self, u, v) -> float:
+        return self._need_exact().s_bilinear(_host(u), _host(v))
+
+    def s_norm(self, u) -> float:
+        return self._need_exact().s_norm(_host(u))
 
     def _apply(self, name: str, u):
         shape = (self.spec.N, self.spec.dim)

@@ -14,8 +14,11 @@ The iteration itself is one call per iteration into libpint
 (pint_uzawa_step); the state (f, p, u and all work slabs) stays in HBM and
 only the two partial sums come back.  ``fft_seconds`` / ``spatial_seconds``
 are cumulative device time of the DST and multigrid phases (CUDA events).
-Diagnostic mode (exact S-norm error per iteration, stopping='s_norm_error')
-needs sparse factorisations and is not on the GPU path.
+Diagnostic mode (exact S-norm error per iteration, stopping='s_norm_error',
+solvers.py:201-244) keeps the iteration on the device and measures the error
+on the host against the sequential implicit-Euler solution with the
+reference's SuperLU factorisations (diagnostics.py): u is copied back once
+per iteration, as the reference's bench.run_table2 needs it.
 """
 
 from __future__ import annotations
@@ -28,7 +31,7 @@ import numpy as np
 
 from ._device import gpu_problem
 from ._native import as_buffer, empty_like_kind, ptr_of
-from .errors import DiagnosticModeRequiredError, InputError
+from .errors import InputError
 from .spatial import MgHierarchy, _check_mg_options
 
 
@@ -168,9 +171,7 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
     Returns ((p, u), ConvergenceHistory) with p, u numpy arrays (or CUDA
     tensors when ``initial`` holds CUDA tensors).
     """
-    if cfg.diagnostics or cfg.stopping == "s_norm_error":
-        raise DiagnosticModeRequiredError(
-            "diagnostic error norms need exact factorizations; not on the GPU path")
+    diagnostics = cfg.diagnostics or cfg.stopping == "s_norm_error"
     gp = _shared_problem(system, atilde, htilde)
     ctx = gp.ctx
     shape = (system.spec.N, system.spec.dim)
@@ -183,6 +184,17 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
         p_ptr = u_ptr = None
         like = f_keep
     hist = ConvergenceHistory()
+    # diagnostic mode (solvers.py:201-210): exact solution and its S-norm on
+    # the host (diagnostics.py); the iterate u comes back once per iteration
+    u_star = s_norm_ref = None
+    if diagnostics:
+        from .diagnostics import sequential_euler_solve
+
+        system.build_exact_solvers()
+        u_star = np.asarray(u_oracle, dtype=np.float64) if u_oracle is not None \
+            else sequential_euler_solve(system.spec)
+        s_norm_ref = system.s_norm(u_star)
+        u_host = np.empty(shape)
     ref = ctypes.c_double(0.0)
     ctx.call("pint_uzawa_begin", f_ptr, p_ptr, u_ptr, ctypes.byref(ref))
     p_out = empty_like_kind(like, shape)
@@ -207,12 +219,19 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
             if first is None:
                 first = max(res, 1e-300)
             ctx.call("pint_phase_ms", ms.ctypes.data)
-            hist.append(res, None, None, time.perf_counter() - t0, ms[0] / 1e3, ms[1] / 1e3)
+            s_err = None
+            if diagnostics:
+                ctx.call("pint_uzawa_end", None, u_host.ctypes.data)  # copy u, keep iterating
+                s_err = system.s_norm(u_host - u_star) / s_norm_ref
+            hist.append(res, s_err, None, time.perf_counter() - t0, ms[0] / 1e3, ms[1] / 1e3)
             if res > 1e6 * first:
                 from .errors import SolverDivergenceError
 
                 raise SolverDivergenceError(f"residual grew to {res:.3e} from {first:.3e}")
-            if res < cfg.tol:
+            if cfg.stopping == "preconditioned_residual" and res < cfg.tol:
+                hist.converged = True
+                break
+            if cfg.stopping == "s_norm_error" and s_err < cfg.tol:
                 hist.converged = True
                 break
     finally:

@@ -45,5 +45,25 @@ def test_cli_rejects_non_gpu_options():
     from paper_1802_08126_b200.cli import main
 
     assert main(["solve", "--solver", "direct"]) == 1
-    assert main(["solve", "--method", "sequential"]) == 1
     assert main(["solve", "--problem-file", "/nonexistent/file"]) == 1
+
+
+def test_cli_sequential_matches_oracle(tmp_path):
+    """--method sequential: the time-stepping oracle's first node per step in
+    the reference's CSV format (cli.py:142-145), host SuperLU (diagnostics.py)."""
+    import numpy as np
+
+    import oracle as orc
+    from paper_1802_08126_b200.cli import main
+
+    out = tmp_path / "seq.csv"
+    assert main(["solve", "--method", "sequential", "--space", "2d", "--h", "8", "--N", "5",
+                 "--out", str(out)]) == 0
+    lines = out.read_text().splitlines()
+    assert lines[0] == "step,node" and len(lines) == 6
+    spec = pg.make_heat_problem("2d", 8, pg.build_time_grid("uniform", 5, 1.0), data="sine")
+    opb = orc.heat_problem("2d", 8, orc.time_nodes("uniform", 5, 1.0), load=spec.load,
+                           u_init=spec.u_init)
+    ref = orc.sequential_euler(opb)
+    got = np.array([float(ln.split(",")[1]) for ln in lines[1:]])
+    assert np.max(np.abs(got - ref[:, 0])) <= 1e-15 * np.max(np.abs(ref[:, 0])) + 1e-300
