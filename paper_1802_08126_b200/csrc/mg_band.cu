@@ -1060,12 +1060,15 @@ __device__ __forceinline__ double row_sum_any(const double* c, const double* v, 
     return row_sum<SH_FULL>(c, r0 - m, r0, r0 + m, x, hs, hn, w, e);
 }
 
+// barrier over the GT threads of one plane group (named barrier 1 + group)
 template <int GT, int GPB>
 __device__ __forceinline__ void group_sync() {
-    if (GT == 32)
+    if constexpr (GT == 32)
         __syncwarp();
+    else if constexpr (GPB == 1)
+        __syncthreads();
     else
-        group_sync<GT, GPB>();
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / GT)), "n"(GT) : "memory");
 }
 
 // GT threads cooperate on one plane; GPB planes per CTA (GT = 32: one warp
@@ -1620,15 +1623,27 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
             PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail<32, 8>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  220 * 1024));
+            PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail<64, 4>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 220 * 1024));
+            PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail<128, 4>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 220 * 1024));
             PINT_CUDA_CHECK(cudaFuncSetAttribute(k_mg_tail<TT, 1>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  220 * 1024));
             attr = true;
         }
         if (smem > 220 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
-        const int per_cta = warp_mode ? 8 : 1;
+        // plane groups of the warp-mode tail: GT threads per plane, GPB planes per CTA
+        // (PINT_TAIL_GT = 32 / 64 / 128 for A/B runs)
+        const int tail_gt = warp_mode ? env_int("PINT_TAIL_GT", 64) : TT;
+        const int per_cta = !warp_mode ? 1 : tail_gt == 32 ? 8 : 4;
         const int ctas_needed = (count + per_cta - 1) / per_cta;
-        const int grid = std::min(ctas_needed, sms * (warp_mode ? 1 : blocks_per_sm(smem)));
+        const size_t smem_cta = sizeof(double) * (size_t)T.words_plane * per_cta;
+        int occ_tail = 1;
+        if (warp_mode) occ_tail = std::max(1, (int)((227 * 1024) / (smem_cta + 1024)));
+        const int grid = std::min(ctas_needed, sms * (warp_mode ? occ_tail : blocks_per_sm(smem)));
         if (top && dot) {
             ensure_partials(c, grid);
             T.part = c->d_part;
@@ -1636,10 +1651,10 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         const double fine = (double)s.m[lt] * s.m[lt];
         ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_TAIL, 8.0 * count * 2.0 * fine);
         if (warp_mode) {
-            // 8 warps per CTA, each owning planes; smem sized for 8 groups
-            const size_t smem8 = sizeof(double) * (size_t)T.words_plane * 8;
-            if (smem8 > 220 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
-            k_mg_tail<32, 8><<<grid, 256, smem8, c->stream>>>(T);
+            if (smem_cta > 220 * 1024) pint_throw(PINT_INPUT, "multigrid tail does not fit shared memory");
+            if (tail_gt == 128) k_mg_tail<128, 4><<<grid, 512, smem_cta, c->stream>>>(T);
+            else if (tail_gt == 64) k_mg_tail<64, 4><<<grid, 256, smem_cta, c->stream>>>(T);
+            else k_mg_tail<32, 8><<<grid, 256, smem_cta, c->stream>>>(T);
         } else {
             k_mg_tail<TT, 1><<<grid, TT, smem, c->stream>>>(T);
         }
