@@ -623,16 +623,24 @@ __global__ void __launch_bounds__(ZX * ZY)
 
 // x += dinv*(b - S x) (spatial.py:159-160) + the finest-level epilogues
 template <uint32_t PAT>
-__global__ void __launch_bounds__(ZX * ZY, 2) kz_smooth(Smooth3 a) {
+__global__ void __launch_bounds__(ZX * ZY, 3) kz_smooth(Smooth3 a) {
     const ZTile t = ztile(a.m);
     const int m = a.m;
     const long long n = (long long)m * m * m;
     const int pl = (int)blockIdx.y;
     double acc = 0.0;
+    // the plane's stencil in shared memory (broadcast reads) instead of 2 x 15..27
+    // registers: the smoother is latency bound, registers buy resident warps
+    __shared__ double cs[27];
+    {
+        const double* tb = a.tab + (size_t)__ldg(a.sid + pl) * 28;
+        const int q = threadIdx.y * ZX + threadIdx.x;
+        if (q < 27) cs[q] = pat_has(PAT, q) ? __ldg(tb + q) : 0.0;
+        __syncthreads();
+    }
     if (t.ok) {
         const double* tb = a.tab + (size_t)__ldg(a.sid + pl) * 28;
-        double c[27];
-        zcoef<PAT>(c, tb);
+        const double* c = cs;
         const double d = __ldg(tb + 27);
         const long long col = (long long)t.y * m + t.x;
         const double* xp = a.x + pl * n;
