@@ -1558,8 +1558,11 @@ void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int
         P.Hc = band_rows(P.m) / 2;  // coarse rows per unit
         P.nbands = (P.mc + P.Hc - 1) / P.Hc;
         P.aref = (aref_in && l == 0) ? 1 : 0;
-        if (P.aref)
+        if (P.aref) {
             for (int q = 0; q < 9; ++q) P.ar[q] = c->h_aref[q];
+            P.Hc = env_int("PINT_AR_HC", P.Hc) <= 2 ? 2 : 4;
+            P.nbands = (P.mc + P.Hc - 1) / P.Hc;
+        }
         P.words_b = band_words(2 * P.Hc + 3 + 2 * P.aref, P.m);
         P.words_r = use_pre2() ? (2 * P.Hc + 1) * (P.m + 3) : ((2 * P.Hc + 1) * P.m + 1) / 2 * 2;
         P.stages = env_int("PINT_STAGES", pick_stages(P.words_b, P.words_r));
