@@ -16,6 +16,7 @@
 // the Schur preconditioner (schur.py:72) uses the same machinery.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "band.cuh"
 #include "pint_device.cuh"
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(TB_NT + 32, 2) k_band_timeop(TopParams P) {
 // sharing a 4-column register window of u and p (2 loads per point instead
 // of 3) and interleaving two independent CSR-order sums.
 template <int OP, int NT, int H, int SHM, int SHA, int ONEA>
-__global__ void __launch_bounds__(NT + 32) k_band_timeop2(TopParams P) {
+__global__ void __launch_bounds__(NT + 32, 2) k_band_timeop2(TopParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[TB_MAXSTAGE], empty[TB_MAXSTAGE];
     __shared__ double meta[TB_MAXSTAGE][10];
@@ -371,24 +372,35 @@ __global__ void __launch_bounds__(NT + 32) k_band_timeop2(TopParams P) {
         qrange(n0, n1, qs, qe);
         const int first = y0 - 1, lo = max(0, first);
         const int nrow = y1 - y0;
+        // interior band: H rows with both halo rows inside the plane (no row predicates)
+        const bool interior = nrow == H && y0 > 0 && y1 < m;
+        // carried state, zero-initialised: a missing previous plane enters as
+        // x - (+0) == x, bit-identical to the reference's one-sided first step
         double mu_prev[2][H], mu_cur[2][H], mp_cur[2][H], au_cur[2][H];
-        const int qlast = OP == 0 ? qe - 1 : qe;
-        for (int q = qs; q <= qlast; ++q) {
-            const bool staged = q < qe;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+                mu_prev[c][r] = 0.0;
+                mu_cur[c][r] = 0.0;
+                mp_cur[c][r] = 0.0;
+                au_cur[c][r] = 0.0;
+            }
+        // one staged plane q; IN: interior band, EM: plane q completes output step t
+        // (r1: t = q >= n0; z: t = q-1 >= n0, the first one or two planes only warm up)
+        auto step = [&](auto in_tag, auto em_tag, int q) {
+            constexpr bool IN = decltype(in_tag)::value;
+            constexpr bool EM = decltype(em_tag)::value;
             const int s = k % S;
             const long long pb = q * n;
-            double ca[9];
-            double sc = 0.0;
             const int t = OP == 0 ? q : q - 1;
-            const bool emit = t >= n0 && t < n1;
-            if (staged) {
-                mbar_wait(&full[s], (k / S) & 1);
-                if (!ONEA) {
+            double ca[9];
+            mbar_wait(&full[s], (k / S) & 1);
+            if (!ONEA) {
 #pragma unroll
-                    for (int t2 = 0; t2 < 9; ++t2) ca[t2] = meta[s][t2];
-                }
-                sc = meta[s][9];
+                for (int t2 = 0; t2 < 9; ++t2) ca[t2] = meta[s][t2];
             }
+            const double sc = meta[s][9];
             const double* A = ONEA ? P.a0 : ca;
             if (act) {
                 const double* us = ustage(s) + tb_shift(pb + bou, m, first, lo) + t0c;
@@ -401,36 +413,31 @@ __global__ void __launch_bounds__(NT + 32) k_band_timeop2(TopParams P) {
                     v[2] = (in && hb) ? row[1] : 0.0;
                     v[3] = (in && hr) ? row[2] : 0.0;
                 };
+                constexpr bool NEED_P = OP == 1 || EM;  // r1 reads p of the emitted steps only
                 double ua[4], ub[4], uc[4], pa[4], pbv[4], pc[4];
-                const bool need_p = OP == 1 || q >= n0;
-                if (staged) {
-                    wr4(us, first >= 0, ua);
-                    wr4(us + m, true, ub);
-                    if (need_p) {
-                        wr4(ps, first >= 0, pa);
-                        wr4(ps + m, true, pbv);
-                    }
+                wr4(us, IN || first >= 0, ua);
+                wr4(us + m, true, ub);
+                if (NEED_P) {
+                    wr4(ps, IN || first >= 0, pa);
+                    wr4(ps + m, true, pbv);
                 }
 #pragma unroll
                 for (int r = 0; r < H; ++r) {
-                    if (r >= nrow) continue;
+                    if (!IN && r >= nrow) continue;
                     const int gy = y0 + r;
-                    double mu[2] = {0.0, 0.0}, mp[2] = {0.0, 0.0}, au[2] = {0.0, 0.0},
-                           ap[2] = {0.0, 0.0};
-                    if (staged) {
-                        wr4(us + (r + 2) * m, gy + 1 < m, uc);
+                    double mu[2], mp[2] = {0.0, 0.0}, au[2] = {0.0, 0.0}, ap[2] = {0.0, 0.0};
+                    wr4(us + (r + 2) * m, IN || gy + 1 < m, uc);
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        mu[c] = wsum<SHM>(cm, ua + c, ub + c, uc + c);
+                        if (OP == 1) au[c] = sc * wsum<SHA>(A, ua + c, ub + c, uc + c);
+                    }
+                    if (NEED_P) {
+                        wr4(ps + (r + 2) * m, IN || gy + 1 < m, pc);
 #pragma unroll
                         for (int c = 0; c < 2; ++c) {
-                            mu[c] = wsum<SHM>(cm, ua + c, ub + c, uc + c);
-                            if (OP == 1) au[c] = sc * wsum<SHA>(A, ua + c, ub + c, uc + c);
-                        }
-                        if (need_p) {
-                            wr4(ps + (r + 2) * m, gy + 1 < m, pc);
-#pragma unroll
-                            for (int c = 0; c < 2; ++c) {
-                                if (OP == 1) mp[c] = wsum<SHM>(cm, pa + c, pbv + c, pc + c);
-                                else ap[c] = sc * wsum<SHA>(A, pa + c, pbv + c, pc + c);
-                            }
+                            if (OP == 1) mp[c] = wsum<SHM>(cm, pa + c, pbv + c, pc + c);
+                            else ap[c] = sc * wsum<SHA>(A, pa + c, pbv + c, pc + c);
                         }
                     }
                     double* o = P.out + t * n + (long long)gy * m + t0c;
@@ -438,22 +445,15 @@ __global__ void __launch_bounds__(NT + 32) k_band_timeop2(TopParams P) {
                     for (int c = 0; c < 2; ++c) {
                         const bool ok = c == 0 || hb;
                         if (OP == 0) {
-                            if (emit && ok) {
-                                const double ku = t - 1 >= P.qmin ? mu[c] - mu_prev[c][r] : mu[c];
-                                o[c] = (ku - ap[c]) - fs[r * m + c];
-                            }
+                            if (EM && ok) o[c] = ((mu[c] - mu_prev[c][r]) - ap[c]) - fs[r * m + c];
                             mu_prev[c][r] = mu[c];
                         } else {
-                            if (emit && ok) {
-                                const bool has_next = t + 1 <= P.qmax;
-                                const double ktp = has_next ? mp_cur[c][r] - mp[c] : mp_cur[c][r];
-                                const double ku =
-                                    t - 1 >= P.qmin ? mu_cur[c][r] - mu_prev[c][r] : mu_cur[c][r];
-                                const double ktu = has_next ? mu_cur[c][r] - mu[c] : mu_cur[c][r];
-                                const double fval =
-                                    staged ? fs[r * m + c]
-                                           : __ldg(P.f + t * n + (long long)gy * m + t0c + c);
-                                o[c] = (fval - ktp) - ((ku + ktu) + au_cur[c][r]);
+                            if (EM && ok) {
+                                // a staged plane q = t+1 always exists here (has_next)
+                                const double ktp = mp_cur[c][r] - mp[c];
+                                const double ku = mu_cur[c][r] - mu_prev[c][r];
+                                const double ktu = mu_cur[c][r] - mu[c];
+                                o[c] = (fs[r * m + c] - ktp) - ((ku + ktu) + au_cur[c][r]);
                             }
                             mu_prev[c][r] = mu_cur[c][r];
                             mu_cur[c][r] = mu[c];
@@ -461,21 +461,49 @@ __global__ void __launch_bounds__(NT + 32) k_band_timeop2(TopParams P) {
                             au_cur[c][r] = au[c];
                         }
                     }
-                    if (staged) {
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            ua[i] = ub[i];
-                            ub[i] = uc[i];
-                            pa[i] = pbv[i];
-                            pbv[i] = pc[i];
-                        }
+                    for (int i = 0; i < 4; ++i) {
+                        ua[i] = ub[i];
+                        ub[i] = uc[i];
+                        pa[i] = pbv[i];
+                        pbv[i] = pc[i];
                     }
                 }
             }
-            if (staged) {
-                consumer_sync<NT>();
-                if (tid == 0) mbar_arrive(&empty[s]);
-                ++k;
+            consumer_sync<NT>();
+            if (tid == 0) mbar_arrive(&empty[s]);
+            ++k;
+        };
+        using TT = std::integral_constant<bool, true>;
+        using FF = std::integral_constant<bool, false>;
+        const int qem = min(qe, OP == 0 ? n0 : n0 + 1);
+        int q = qs;
+        for (; q < qem; ++q) {
+            if (interior) step(TT{}, FF{}, q);
+            else step(FF{}, FF{}, q);
+        }
+        for (; q < qe; ++q) {
+            if (interior) step(TT{}, TT{}, q);
+            else step(FF{}, TT{}, q);
+        }
+        if (OP == 1 && act) {
+            // last step of the time axis (t = qe-1 = qmax, no plane t+1): K^T has
+            // no next-step term
+            const int t = qe - 1;
+            if (t >= n0 && t < n1 && qe > P.qmax) {
+#pragma unroll
+                for (int r = 0; r < H; ++r) {
+                    if (r >= nrow) continue;
+                    const int gy = y0 + r;
+                    double* o = P.out + t * n + (long long)gy * m + t0c;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        if (!(c == 0 || hb)) continue;
+                        const double ku = mu_cur[c][r] - mu_prev[c][r];
+                        const double fval = __ldg(P.f + t * n + (long long)gy * m + t0c + c);
+                        o[c] = (fval - mp_cur[c][r]) - ((ku + mu_cur[c][r]) + au_cur[c][r]);
+                    }
+                }
             }
         }
     }
