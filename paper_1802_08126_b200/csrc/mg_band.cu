@@ -24,6 +24,7 @@
 // exact zero on every plane (the SE/NW entries of the P1 diagonal split, the
 // four diagonal entries of the stiffness) are skipped, which adds +-0 and so
 // cannot change a non-zero sum.
+#include <type_traits>
 #include <algorithm>
 #include <cstdlib>
 
@@ -436,6 +437,11 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
         const int first = 2 * Y0 - 1;
         const int lo = max(0, first);
         const int nr = 2 * (Y1 - Y0) + 1;
+        // interior band: HC coarse rows whose fine rows (and the A_ref halo) are
+        // all inside the plane, so the row loops carry no boundary predicates
+        const bool interior = Y1 - Y0 == HC && Y0 >= 1 && 2 * Y1 + 2 < m;
+        auto unit_body = [&](auto in_tag) {
+        constexpr bool IN = decltype(in_tag)::value;
         mbar_wait(&full[s], (k / S) & 1);
         double ca[9];
 #pragma unroll
@@ -450,7 +456,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
             double ya[6], yb[6], yc[6];
             auto yrow = [&](int ys, double* v) {
                 const int gy = first - 1 + ys;
-                const bool in = gy >= 0 && gy < m;
+                const bool in = IN || (gy >= 0 && gy < m);
                 const double* row = bcol + ys * m;
                 v[0] = (in && t >= 2) ? row[-3] : 0.0;
                 v[1] = (in && has_l) ? row[-2] : 0.0;
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
             auto ld = [&](int slot, double& w0, double& w1, double& w2, double& w3, double& ra,
                           double& rb) {
                 const int gy = first + slot;
-                const bool in = gy >= 0 && gy < m;
+                const bool in = IN || (gy >= 0 && gy < m);
                 if (AR) {
                     // b row `slot` from y slots slot .. slot+2 (5-point A_ref, k_band_apply order)
                     yrow(slot + 2, yc);
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
             double* out = sr + 2 * t;  // padded columns 2t, 2t+1 = fine 2t-1, 2t
 #pragma unroll
             for (int rho = 0; rho < RR; ++rho) {
-                if (rho < nr) {
+                if (IN || rho < nr) {
                     double c0, c1, c2, c3, cra, crb;
                     ld(rho + 2, c0, c1, c2, c3, cra, crb);
                     const double ra = has_a ? bra - win_sum<SH>(ca, a0, a1, a2, b0, b1, b2, c0, c1, c2)
@@ -534,7 +540,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
             double* outc = P.bc + plane * nc + (long long)Y0 * mc + t;
 #pragma unroll
             for (int r = 0; r < HC; ++r) {
-                if (r < ncr) {
+                if (IN || r < ncr) {
                     double q0, q1, q2, t0, t1, t2;
                     ld3(2 * r + 1, q0, q1, q2);
                     ld3(2 * r + 2, t0, t1, t2);
@@ -553,6 +559,9 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
             }
         }
         consumer_sync<NC>();
+        };
+        if (interior) unit_body(std::true_type{});
+        else unit_body(std::false_type{});
     }
 }
 
@@ -879,6 +888,11 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
         const int fb = y0 - 1, lob = max(0, fb);
         const int fe = y0 / 2 - 1, loe = max(0, fe);
         const int nrow = y1 - y0;
+        // interior band: H rows whose prolongation and halo rows are all inside
+        // the plane, so the row loops carry no boundary predicates
+        const bool interior = nrow == H && y0 >= 2 && y1 <= m - 2;
+        auto unit_body = [&](auto in_tag) {
+        constexpr bool IN = decltype(in_tag)::value;
         mbar_wait(&full[s], (k / S) & 1);
         double ca[9];
 #pragma unroll
@@ -895,7 +909,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
             double ya[4], yb[4], yc[4];
             auto yrow = [&](int ys, double* v) {
                 const int gy = fb - 1 + ys;
-                const bool in = gy >= 0 && gy < m;
+                const bool in = IN || (gy >= 0 && gy < m);
                 const double* row = brow + ys * m;
                 v[0] = (in && has_a) ? row[-2] : 0.0;
                 v[1] = (in && has_a) ? row[-1] : 0.0;
@@ -908,7 +922,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
             }
 #pragma unroll
             for (int r = 0; r < H + 2; ++r) {
-                if (r > nrow + 1) continue;
+                if (!IN && r > nrow + 1) continue;
                 const int gy = fb + r;
                 double xva = 0.0, xvb = 0.0;
                 double b2a = 0.0, b2b = 0.0;
@@ -924,7 +938,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
                     bsa[AR ? r : 0] = b2a;
                     bsb[AR ? r : 0] = b2b;
                 }
-                if (gy >= 0 && gy < m) {
+                if (IN || (gy >= 0 && gy < m)) {
                     const double* bp = brow + r * m;
                     const double bva = has_a ? (AR ? b2a : bp[-1]) : 0.0;
                     const double bvb = AR ? b2b : bp[0];
@@ -939,7 +953,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
                         pbv = pbv + (1.0 * 0.5) * e1;
                     } else {
                         // even fine row gy: coarse rows gy/2-1 (slot (r-1)/2) and gy/2 (slot (r+1)/2)
-                        const bool va = gy >= 2, vbr = (gy >> 1) < mc;
+                        const bool va = IN || gy >= 2, vbr = IN || (gy >> 1) < mc;
                         const double* e = erow + ((r - 1) >> 1) * mc;
                         const double a0 = (va && has_a) ? e[0] : 0.0;
                         const double a1 = (va && has_cb) ? e[1] : 0.0;
@@ -982,7 +996,7 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
             const double* qrow = vq.p + xb;
 #pragma unroll
             for (int r = 0; r < H; ++r) {
-                if (r < nrow) {
+                if (IN || r < nrow) {
                     double c0, c1, c2, c3;
                     ldrow(r + 2, c0, c1, c2, c3);
                     const double bvb = AR ? bsb[AR ? r + 1 : 0] : brow[r * m];
@@ -1023,6 +1037,9 @@ __global__ void __launch_bounds__(NT * PPU + 32) k_band_post2(PostBandParams P) 
         }
         consumer_sync<NC>();
         if (tid == 0) mbar_arrive(&empty[s]);
+        };
+        if (interior) unit_body(std::true_type{});
+        else unit_body(std::false_type{});
     }
     if (HAS_DOT) {
         const double sum = consumer_sum<NC>(acc, red);
