@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(NT + 32) k_band_pre(PreParams P) {
 // g*PPU + pl, so a stage carries PPU bands and the per-unit barrier and
 // mbarrier latency is paid once for PPU planes.
 template <int SH, int NT, int HC, int AR = 0, int PPU = 1>
-__global__ void __launch_bounds__(NT * PPU + 32) k_band_pre2(PreParams P) {
+__global__ void __launch_bounds__(NT * PPU + 32, (AR && NT * PPU <= 128) ? 3 : 1) k_band_pre2(PreParams P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) uint64_t full[MAXSTAGE], empty[MAXSTAGE];
     __shared__ double meta[MAXSTAGE][PPU][PINT_TW];

@@ -24,7 +24,7 @@ def family(name, grid):
     if "k_band_pre2" in name:
         return "mg_pre_fine" if ", 128," in name or "<2, 128" in name or "<1, 128" in name else "mg_pre_coarse"
     if "k_band_post2" in name:
-        return "mg_post_fine" if re.search(r", 128, 8(, [01])?>", name) else "mg_post_coarse"
+        return "mg_post_fine" if re.search(r", 128, 8(, [01]){0,2}>", name) else "mg_post_coarse"
     if "k_mg_tail" in name:
         return "mg_tail"
     if "k_reduce" in name:
