@@ -591,14 +591,30 @@ __global__ void __launch_bounds__(ZX * ZY)
     const double sc = __ldg(ascale + pl);
     const long long col = (long long)t.y * m + t.x;
     const bool hp = pl - 1 >= qmin, hn = pl + 1 <= qmax;
-    zmarch<PAT, false>(t, m, u + pl * n, c, 1.0, [&](int, int li, double s, double) {
-        const long long gi = pl * n + li;
-        const double mpc = __ldg(mp + gi), muc = __ldg(mu + gi);
-        const double ktp = hn ? mpc - __ldg(mp + gi + n) : mpc;
-        const double ku = hp ? muc - __ldg(mu + gi - n) : muc;
-        const double ktu = hn ? muc - __ldg(mu + gi + n) : muc;
-        out[gi] = (__ldg(f + gi) - ktp) - ((ku + ktu) + sc * s);
-    });
+    // the six point operands of the next z are requested one point ahead
+    // (zmarch_pf), like kz_r1: the kernel is latency bound otherwise
+    struct Pv {
+        double mp, mpn, mu, mup, mun, f;
+    };
+    zmarch_pf<PAT, false>(
+        t, m, u + pl * n, c, 1.0,
+        [&](int li, bool ok) {
+            const long long gi = pl * n + li;
+            Pv r;
+            r.mp = ok ? __ldg(mp + gi) : 0.0;
+            r.mu = ok ? __ldg(mu + gi) : 0.0;
+            r.mpn = ok && hn ? __ldg(mp + gi + n) : 0.0;
+            r.mun = ok && hn ? __ldg(mu + gi + n) : 0.0;
+            r.mup = ok && hp ? __ldg(mu + gi - n) : 0.0;
+            r.f = ok ? __ldg(f + gi) : 0.0;
+            return r;
+        },
+        [&](int li, double s, double, Pv pv) {
+            const double ktp = hn ? pv.mp - pv.mpn : pv.mp;
+            const double ku = hp ? pv.mu - pv.mup : pv.mu;
+            const double ktu = hn ? pv.mu - pv.mun : pv.mu;
+            out[pl * n + li] = (pv.f - ktp) - ((ku + ktu) + sc * s);
+        });
 }
 
 // r = b - S(dinv * b)   (spatial.py:153,156)
