@@ -779,6 +779,13 @@ __global__ void __launch_bounds__(ZX * ZY)
     };
     const long long col = (long long)t.y * m + t.x;
     const int k0 = t.z0 >> 1;  // z0 is even
+    // the chunk's ZC values of b are requested up front (one exposed latency)
+    double bv[ZC];
+    {
+        const double* bp = b + pl * n + (long long)t.z0 * m * m + col;
+#pragma unroll
+        for (int i = 0; i < ZC; ++i) bv[i] = i < t.zn ? __ldg(bp + (long long)i * m * m) : 0.0;
+    }
     double gp[2][2], gc[2][2];
     load(k0 - 1, gp);
     load(k0, gc);
@@ -792,14 +799,14 @@ __global__ void __launch_bounds__(ZX * ZY)
             if (k - 1 >= 0) accum(0.5, gp, pe, first);
             if (k < mc) accum(0.5, gc, pe, first);
             const long long gi = pl * n + (long long)(2 * k) * m * m + col;
-            x[gi] = d * __ldg(b + gi) + pe;
+            x[gi] = d * bv[i] + pe;
         }
         if (i + 1 < t.zn) {  // odd fine plane 2k+1: coarse k, weight 1
             double pe = 0.0;
             bool first = true;
             accum(1.0, gc, pe, first);
             const long long gi = pl * n + (long long)(2 * k + 1) * m * m + col;
-            x[gi] = d * __ldg(b + gi) + pe;
+            x[gi] = d * bv[i + 1] + pe;
         }
 #pragma unroll
         for (int bb = 0; bb < 2; ++bb)
