@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(NT + 32, 2) k_band_timeop2(TopParams P) {
         const int first = y0 - 1, lo = max(0, first);
         const int nrow = y1 - y0;
         // interior band: H rows with both halo rows inside the plane (no row predicates)
-        const bool interior = nrow == H && y0 > 0 && y1 < m;
+        // (r1 is at the HBM roofline: it keeps one row-predicated body, smaller code)
+        const bool interior = OP == 1 && nrow == H && y0 > 0 && y1 < m;
         // carried state, zero-initialised: a missing previous plane enters as
         // x - (+0) == x, bit-identical to the reference's one-sided first step
         double mu_prev[2][H], mu_cur[2][H], mp_cur[2][H], au_cur[2][H];
