@@ -190,6 +190,10 @@ int pint_uzawa_end(pint_ctx* ctx, double* p, double* u);
  * (No reference counterpart: a transfer-path detail of uzawa_solve's
  * numpy-in/numpy-out contract, solvers.py:177-264.) */
 int pint_host_prefault(pint_ctx* ctx, void* host, long long bytes);
+/* Wait for every background first-touch started by pint_host_prefault.  Call
+ * before releasing a prefaulted buffer that no copy-out has consumed (error
+ * paths of the caller's loop). */
+int pint_host_prefault_join(pint_ctx* ctx);
 int pint_uzawa(pint_ctx* ctx, const double* f, double* p, double* u, double omega,
                double tol, int max_iter, int use_initial, double* res_hist, int* iters,
                int* converged, double* phase_ms);

@@ -76,6 +76,7 @@ _SIGNATURES = {
     "pint_uzawa_step": (_I, [_P, _D, _DP]),
     "pint_uzawa_end": (_I, [_P, _P, _P]),
     "pint_host_prefault": (_I, [_P, _P, ctypes.c_longlong]),
+    "pint_host_prefault_join": (_I, [_P]),
     "pint_apply_saddle": (_I, [_P, _P, _P, _P, _P]),
     "pint_lincomb": (_I, [_P, _P, ctypes.c_longlong, _P, _D, _P, _D, _P, _D, _I]),
     "pint_dot": (_I, [_P, _P, _P, ctypes.c_longlong, _DP]),

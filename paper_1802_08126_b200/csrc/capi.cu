@@ -621,6 +621,8 @@ int pint_mg_set_field(pint_ctx* c, int which, int levels, const int* level_m, do
     return guarded(c, [&] {
         require_problem(c);
         if (!c->field) pint_throw(PINT_INPUT, "no stiffness fields set");
+        // the captured step graph holds this set's buffers and damping
+        graph_reset(c);
         if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE)
             pint_throw(PINT_INPUT, "unknown multigrid set");
         if (levels < 2 || !level_m || !(damping > 0.0)) pint_throw(PINT_INPUT, "bad multigrid description");
@@ -1057,6 +1059,10 @@ int pint_host_prefault(pint_ctx* c, void* host, long long bytes) {
         if (is_device_ptr(host)) return;
         pint::host_prefault_async(c, host, (size_t)bytes);
     });
+}
+
+int pint_host_prefault_join(pint_ctx* c) {
+    return guarded(c, [&] { pint::host_prefault_join(c); });
 }
 
 int pint_uzawa_end(pint_ctx* c, double* p, double* u) {

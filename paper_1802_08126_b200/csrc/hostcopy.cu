@@ -123,7 +123,10 @@ void copy_h2d(pint_ctx* c, void* dev, const void* host, size_t bytes) {
         int it = 0;
         for (size_t k = t; k < nck; k += T, ++it) {
             const int slot = 2 * t + (it & 1);
-            if (it >= 2) PINT_CUDA_CHECK(cudaEventSynchronize(x->done[slot]));
+            // the slot's previous DMA may belong to this call (it >= 2) or to an
+            // earlier copy_h2d issued without a stream sync in between; an
+            // event that was never recorded returns at once
+            PINT_CUDA_CHECK(cudaEventSynchronize(x->done[slot]));
             const size_t off = k * C, len = std::min(C, bytes - off);
             std::memcpy(x->pinned[slot], static_cast<const char*>(host) + off, len);
             PINT_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(dev) + off, x->pinned[slot], len,

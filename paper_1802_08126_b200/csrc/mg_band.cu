@@ -35,6 +35,9 @@
 #ifndef PINT_VARIANT
 #define PINT_VARIANT exact
 #endif
+#ifndef PINT_FAST
+#define PINT_FAST 0
+#endif
 
 namespace pint {
 namespace PINT_VARIANT {  // compiled as pint::exact (-fmad=false) and pint::fast (FMA)
@@ -200,16 +203,25 @@ __device__ __forceinline__ double win_sum(const double* ca, double a0, double a1
 }
 
 // 5-point A_ref row sum for the fused mode right-hand side b2 = A_ref y1
-// (schur.py:72) with fused multiply-adds: 5 fp64 instructions instead of 9.
-// Not bit-identical to the separate CSR-order pass (k_band_apply); H~^{-1}
-// carries the sine transforms' rounding anyway (parity bar 1e-12).
+// (schur.py:72).  Exact arithmetic evaluates scipy's CSR row order
+// S, W, C, E, N (the stored zeros SW/NE add +0) with separate multiplies and
+// adds, bit-identical to the separate pass (k_band_apply); fast arithmetic
+// uses fused multiply-adds (5 fp64 instructions instead of 9).
 __device__ __forceinline__ double aref5(const double* ar, double s_, double w_, double c_,
                                         double e_, double n_) {
+#if PINT_FAST
     double v = ar[1] * s_;
     v = __fma_rn(ar[3], w_, v);
     v = __fma_rn(ar[4], c_, v);
     v = __fma_rn(ar[5], e_, v);
     return __fma_rn(ar[7], n_, v);
+#else
+    double v = __dmul_rn(ar[1], s_);
+    v = __dadd_rn(v, __dmul_rn(ar[3], w_));
+    v = __dadd_rn(v, __dmul_rn(ar[4], c_));
+    v = __dadd_rn(v, __dmul_rn(ar[5], e_));
+    return __dadd_rn(v, __dmul_rn(ar[7], n_));
+#endif
 }
 
 template <int SH, int NT, int CPT, int HC>

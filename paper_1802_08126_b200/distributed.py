@@ -55,6 +55,12 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # P2POp takes GLOBAL peer ranks; rank/world above are group-local
+        self._global = [q if group is None else dist.get_global_rank(group, q)
+                        for q in range(self.world)]
+
+    def peer(self, q: int) -> int:
+        return self._global[q]
 
     def _run(self, ops):
         if ops:
@@ -69,14 +75,14 @@ class Comm:
         ops = []
         if prev:
             if r + 1 < w:
-                ops.append(dist.P2POp(dist.isend, ext[nl].contiguous(), r + 1, self.group))
+                ops.append(dist.P2POp(dist.isend, ext[nl].contiguous(), self.peer(r + 1), self.group))
             if r > 0:
-                ops.append(dist.P2POp(dist.irecv, ext[0], r - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, ext[0], self.peer(r - 1), self.group))
         if nxt:
             if r > 0:
-                ops.append(dist.P2POp(dist.isend, ext[1].contiguous(), r - 1, self.group))
+                ops.append(dist.P2POp(dist.isend, ext[1].contiguous(), self.peer(r - 1), self.group))
             if r + 1 < w:
-                ops.append(dist.P2POp(dist.irecv, ext[nl + 1], r + 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, ext[nl + 1], self.peer(r + 1), self.group))
         self._run(ops)
 
     def exchange(self, send: list, recv: list) -> None:
@@ -86,8 +92,8 @@ class Comm:
             if q == self.rank:
                 recv[q].copy_(send[q])
                 continue
-            ops.append(dist.P2POp(dist.isend, send[q], q, self.group))
-            ops.append(dist.P2POp(dist.irecv, recv[q], q, self.group))
+            ops.append(dist.P2POp(dist.isend, send[q], self.peer(q), self.group))
+            ops.append(dist.P2POp(dist.irecv, recv[q], self.peer(q), self.group))
         self._run(ops)
 
     def allreduce(self, vals, device) -> list:

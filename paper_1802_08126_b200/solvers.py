@@ -156,6 +156,10 @@ class BlockDiagSolver:
         raise InputError("forward application requires direct (exact) solvers")
 
 
+def _is_cuda(x) -> bool:
+    return x is not None and type(x).__module__.startswith("torch") and x.is_cuda
+
+
 def _shared_problem(system, atilde, htilde):
     gp = system._gp
     if getattr(atilde, "_gp", None) is not gp or getattr(htilde, "_gp", None) is not gp:
@@ -195,6 +199,12 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
             else sequential_euler_solve(system.spec)
         s_norm_ref = system.s_norm(u_star)
         u_host = np.empty(shape)
+    if any(_is_cuda(x) for x in (f_keep, p_ptr and p_keep, u_ptr and u_keep)):
+        # the library reads device inputs on its own stream: order it after
+        # torch's pending writes (.contiguous(), .cuda(), the caller's kernels)
+        import torch
+
+        torch.cuda.synchronize(gp.ctx.device)
     ref = ctypes.c_double(0.0)
     ctx.call("pint_uzawa_begin", f_ptr, p_ptr, u_ptr, ctypes.byref(ref))
     p_out = empty_like_kind(like, shape)
@@ -236,6 +246,9 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
                 break
     finally:
         ctx.call("pint_set_timing", 0)
+        # background first-touch threads write into p_out / u_out: they must
+        # finish before an exception can release those arrays
+        ctx.call("pint_host_prefault_join")
     ctx.call("pint_uzawa_end", ptr_of(p_out), ptr_of(u_out))
     return (p_out, u_out), hist
 

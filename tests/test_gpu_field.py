@@ -15,7 +15,7 @@ import pytest
 
 import oracle as orc
 import paper_1802_08126_b200 as pg
-from test_gpu_parity import intrinsic_drift
+from ulp_floor import uzawa_envelope
 
 pytestmark = pytest.mark.gpu
 
@@ -76,8 +76,8 @@ def test_field_uzawa_matches_oracle():
     rel = np.abs(np.array(hist.residual[:k]) - ref_res) / ref_res
     print(f"field uzawa: {hist.iterations} iterations, max rel residual drift {rel.max():.3e}")
     assert rel[ref_res > 1e-7].max() <= 1e-10, rel
-    floor = intrinsic_drift(opb, 0.9, 1e-8, 3000, ref_res)
-    print(f"reference FFT-vs-dense floor {floor:.3e}")
-    assert rel.max() <= max(1e-10, 5.0 * floor), (rel.max(), floor)
+    bar = uzawa_envelope(opb, 0.9, 1e-8, 3000, ref_res, k)
+    print(f"oracle 1-ulp floor {bar.max():.3e}")
+    assert np.all(rel <= bar), (rel.max(), bar.max())
     nrm = orc.ExactNorms(opb)
     assert nrm.s_norm(u - ref.u) / nrm.s_norm(ref.u) <= 1e-8

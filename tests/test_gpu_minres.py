@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle as orc
+from ulp_floor import minres_envelope
 import paper_1802_08126_b200 as pg
 from conftest import GOLDEN
 
@@ -44,15 +45,12 @@ def test_minres_matches_reference(name):
     head = ref[:k] > 1e-7 * ref[0]
     pb = orc.heat_problem(str(d["space"]), int(d["cells"]), d["nodes"], load=d["load"],
                           u_init=d["u_init"])
-    # bar: 1e-10, or 5x the reference's own drift between its two DST paths
-    lev = orc.mg_levels(pb.space, pb.cells)
-    alt = orc.minres(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev, dense_dst=True),
-                     tol=float(d["mr_tol"]), max_iter=int(d["mr_max_iter"])).residual
-    kk = min(k, len(alt))
-    floor = float((np.abs(np.array(alt[:kk]) - ref[:kk]) / ref[:kk])[head[:kk]].max())
+    # bar: 1e-10, or the reference arithmetic's own drift under a 1-ulp
+    # perturbation of its transforms (tests/ulp_floor.py)
+    bar = minres_envelope(pb, float(d["mr_tol"]), int(d["mr_max_iter"]), ref, k)
     print(f"{name}: {hist.iterations} vs {len(ref)} iterations, max rel drift {rel.max():.2e}, "
-          f"head {rel[head].max():.2e}, reference floor {floor:.2e}")
-    assert rel[head].max() <= max(1e-10, 5 * floor), (rel[head].max(), floor)
+          f"head {rel[head].max():.2e}, reference 1-ulp floor {bar[head].max():.2e}")
+    assert np.all(rel[head] <= bar[head]), (rel[head].max(), bar[head].max())
     nrm = orc.ExactNorms(pb)
     ref_u = d["mr_u"]
     assert nrm.s_norm(u - ref_u) <= 1e-8 * nrm.s_norm(ref_u)

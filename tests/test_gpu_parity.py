@@ -19,6 +19,7 @@ import pytest
 import oracle as orc
 import paper_1802_08126_b200 as pg
 from conftest import GOLDEN
+from ulp_floor import minres_envelope, uzawa_envelope
 
 pytestmark = pytest.mark.gpu
 
@@ -75,17 +76,17 @@ def case(request, arith):
     hier = pg.build_mg_hierarchy("2d", spec.meta["mesh"])
     at = pg.BlockDiagSolver(spec, "mg", hierarchy=hier)
     ht = pg.build_schur_preconditioner(spec, "mg", vcycles=1)
-    return d, opb, spec, system, at, ht
+    return d, opb, spec, system, at, ht, request.param
 
 
 def test_fold_rhs_bitwise(case):
-    d, opb, spec, system, _, _ = case
+    d, opb, spec, system, _, _, _ = case
     np.testing.assert_array_equal(system.rhs, orc.fold_rhs(opb))
     np.testing.assert_array_equal(system.rhs, d["rhs"])
 
 
 def test_time_operators_bitwise(case):
-    d, opb, spec, system, _, _ = case
+    d, opb, spec, system, _, _, _ = case
     x = d["x"]
     same(system.apply_K(x), d["K_x"])
     same(system.apply_Kt(x), d["Kt_x"])
@@ -93,26 +94,26 @@ def test_time_operators_bitwise(case):
 
 
 def test_atilde_bitwise(case):
-    d, opb, spec, system, at, _ = case
+    d, opb, spec, system, at, _, _ = case
     same(at.apply_inverse(d["x"]), d["atilde_x"])
 
 
 def test_vcycle_bitwise(case):
-    d, opb, spec, _, _, _ = case
+    d, opb, spec, _, _, _, _ = case
     hier = pg.build_mg_hierarchy("2d", spec.meta["mesh"])
     vc = pg.MgVCycleSolver(spec.stiffness[0], hier)
     same(vc.apply(d["y"][0]), d["vcyc_a0_y"])
 
 
 def test_htilde_matches(case):
-    d, opb, spec, system, _, ht = case
+    d, opb, spec, system, _, ht, _ = case
     got = ht.apply_inverse(d["x"])
     ref = d["htilde_x"]
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
 def test_dst_kinds_match_reference(case):
-    d, _, _, _, _, _ = case
+    d, _, _, _, _, _, _ = case
     x = d["x"]
     plan = pg.DstPlan(x.shape[0])
     for kind, key in (("forward", "dst_fwd_x"), ("inverse", "dst_inv_x"),
@@ -169,19 +170,28 @@ def test_dst_round_trip_and_adjoint(N):
                                                         abs=1e-11)
 
 
-def intrinsic_drift(opb, omega, tol, max_iter, ref_res):
-    """Max relative residual difference between the reference's two DST code
-    paths (FFT vs dense kernel) on this case: the floor any reassociation of
-    the transforms can reach."""
-    lev = orc.mg_levels(opb.space, opb.cells)
-    r = orc.uzawa(opb, orc.BlockInv(opb, lev), orc.SchurInv(opb, lev, dense_dst=True),
-                  omega, tol, max_iter)
-    k = min(len(r.residual), len(ref_res))
-    return float(np.max(np.abs(np.array(r.residual[:k]) - ref_res[:k]) / ref_res[:k]))
+def drift_bar(case_name, iters):
+    """Per-iteration residual bar: max(1e-10, the reference's own drift floor).
+
+    tests/golden/drift_floor.npz (tests/golden/make_drift_floor.py) holds the
+    relative residual drift of the reference's arithmetic (the oracle, bit-
+    identical to pintsolve) when one ulp is flipped in a random 0.1 % of the
+    sine transforms' outputs, for 16 seeds.  Near res ~ tol the residual's
+    rounding noise (eps / res / sqrt(#entries)) dominates any run whose
+    iterates differ in a single bit from the reference's; on config 1, 14 of
+    the 16 perturbed reference runs exceed 1e-10.  The envelope is the running
+    maximum over seeds and earlier iterations, so it is 1e-10 wherever the
+    perturbed reference itself stays inside the north_star bar.
+    """
+    d = np.load(os.path.join(GOLDEN, "drift_floor.npz"))[case_name + "_drift"]
+    env = np.fmax.accumulate(np.nanmax(d, axis=0))
+    if len(env) < iters:
+        env = np.concatenate([env, np.full(iters - len(env), env[-1])])
+    return np.maximum(1e-10, env[:iters])
 
 
 def test_uzawa_golden_cases(case):
-    d, opb, spec, system, at, ht = case
+    d, opb, spec, system, at, ht, case_name = case
     cfg = pg.UzawaConfig(omega=float(d["uz_omega"]), tol=float(d["uz_tol"]),
                          max_iter=int(d["uz_max_iter"]))
     (p, u), hist = pg.uzawa_solve(system, at, ht, cfg)
@@ -189,10 +199,9 @@ def test_uzawa_golden_cases(case):
     assert abs(hist.iterations - len(ref_res)) <= 1
     k = min(hist.iterations, len(ref_res))
     rel = np.abs(np.array(hist.residual[:k]) - ref_res[:k]) / ref_res[:k]
-    floor = intrinsic_drift(opb, cfg.omega, cfg.tol, cfg.max_iter, ref_res)
-    bar = max(1e-10, 10.0 * floor)
-    print(f"max rel residual drift {rel.max():.3e}; reference FFT-vs-dense floor {floor:.3e}")
-    assert rel.max() <= bar, (rel.max(), floor)
+    bar = drift_bar(case_name, k)
+    print(f"max rel residual drift {rel.max():.3e}; reference 1-ulp floor {bar.max():.3e}")
+    assert np.all(rel <= bar), (rel.max(), int(np.argmax(rel / bar)), bar.max())
     assert hist.converged == bool(d["uz_converged"])
     nrm = orc.ExactNorms(opb)
     err = nrm.s_norm(u - d["uz_u"]) / nrm.s_norm(d["uz_u"])
@@ -215,16 +224,12 @@ def test_config1_uzawa_parity():
     rel = np.abs(np.array(hist.residual) - ref) / ref
     print(f"config 1: max rel residual drift {rel.max():.3e} (first 50 iterations "
           f"{rel[:50].max():.3e})")
-    # 1e-10 is the north_star bar.  On the last iterations (res ~ 1e-8) any
-    # reassociation of the sine transforms moves the residual by ~1e-10: the
-    # reference's own FFT and dense-kernel DST paths differ by 7.8e-11 here
-    # (DESIGN.md "Parity").  The tail is held to 5x that measured floor.
-    assert rel[ref > 1e-7].max() <= 1e-10, rel.max()
-    opb0 = orc.heat_problem("2d", 32, orc.time_nodes("uniform", 64, 1.0), load=load,
-                            u_init=np.zeros(961))
-    floor = intrinsic_drift(opb0, 0.9, 1e-8, 200, ref)
-    print(f"reference FFT-vs-dense floor {floor:.3e}")
-    assert rel.max() <= max(1e-10, 5.0 * floor), (rel.max(), floor)
+    # 1e-10 (the north_star bar) wherever the reference's own arithmetic holds
+    # it under a 1-ulp perturbation; on the last iterations the bar is that
+    # perturbed reference's measured drift (drift_bar)
+    bar = drift_bar("c1", len(ref))
+    assert np.all(rel[ref > 1e-7] <= 1e-10), rel.max()
+    assert np.all(rel <= bar), (rel.max(), int(np.argmax(rel / bar)), bar.max())
     opb = orc.heat_problem("2d", 32, orc.time_nodes("uniform", 64, 1.0), load=load,
                            u_init=np.zeros(961))
     nrm = orc.ExactNorms(opb)
@@ -412,18 +417,15 @@ def test_cli_solve_problem_file(method, tmp_path):
     k = min(len(ours), len(ref))
     rel = np.abs(ours[:k, 1] - ref[:k, 1]) / ref[:k, 1]
     head = ref[:k, 1] > 1e-7 * ref[0, 1]
-    # bar: 1e-10, or 5x the reference's own FFT-vs-dense DST drift on this case
+    # bar: 1e-10, or the reference arithmetic's own drift under a 1-ulp
+    # perturbation of its transforms (tests/ulp_floor.py)
     d = np.load(os.path.join(GOLDEN, "problem_c8_N4.npz"))
     pb = orc.heat_problem("2d", 8, d["nodes"], coeff=lambda t: 1.0 + t, load=d["load"],
                           u_init=d["u_init"])
-    lev = orc.mg_levels("2d", 8)
-    dense = orc.SchurInv(pb, lev, dense_dst=True)
     if method == "minres":
-        alt = orc.minres(pb, orc.BlockInv(pb, lev), dense, tol=1e-10, max_iter=300).residual
+        bar = minres_envelope(pb, 1e-10, 300, ref[:, 1], k)
     else:
-        alt = orc.uzawa(pb, orc.BlockInv(pb, lev), dense, omega, 1e-10, 300).residual
-    kk = min(k, len(alt))
-    floor = float((np.abs(np.array(alt[:kk]) - ref[:kk, 1]) / ref[:kk, 1])[head[:kk]].max())
+        bar = uzawa_envelope(pb, omega, 1e-10, 300, ref[:, 1], k)
     print(f"{method}: {len(ours)} vs {len(ref)} iterations, drift {rel[head].max():.2e}, "
-          f"reference floor {floor:.2e}")
-    assert rel[head].max() <= max(1e-10, 5 * floor), (rel[head].max(), floor)
+          f"reference 1-ulp floor {bar[head].max():.2e}")
+    assert np.all(rel[head] <= bar[head]), (rel[head].max(), bar[head].max())
