@@ -12,9 +12,10 @@ that level on the last iterations, whatever the arithmetic.
 
 This script measures that floor on the reference's own arithmetic: it runs
 the oracle (bit-identical to ``pintsolve``, tests/test_oracle.py) with the
-sine transforms' outputs perturbed by one ulp in a random 0.1 % of their
-entries -- far below any transform's own rounding error -- for SEEDS seeds,
-and records the relative drift of every iteration's residual against the
+sine transforms' outputs perturbed by one ulp in a random half of their
+entries -- a model of an independent, equally accurate implementation of the
+transforms (two FFTs of the same accuracy differ by a few ulps in most
+entries) -- for SEEDS seeds, and records the relative drift of every iteration's residual against the
 unperturbed run.  ``tests/test_gpu_parity.py`` holds the GPU to
 max(1e-10, the ensemble's per-iteration maximum).
 
@@ -35,7 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-FRACTION = 1e-3
+FRACTION = 0.5
 
 
 def _case(name):

@@ -175,10 +175,10 @@ def drift_bar(case_name, iters):
 
     tests/golden/drift_floor.npz (tests/golden/make_drift_floor.py) holds the
     relative residual drift of the reference's arithmetic (the oracle, bit-
-    identical to pintsolve) when one ulp is flipped in a random 0.1 % of the
+    identical to pintsolve) when one ulp is flipped in a random half of the
     sine transforms' outputs, for 16 seeds.  Near res ~ tol the residual's
     rounding noise (eps / res / sqrt(#entries)) dominates any run whose
-    iterates differ in a single bit from the reference's; on config 1, 14 of
+    iterates differ in a single bit from the reference's; on config 1, most of
     the 16 perturbed reference runs exceed 1e-10.  The envelope is the running
     maximum over seeds and earlier iterations, so it is 1e-10 wherever the
     perturbed reference itself stays inside the north_star bar.

@@ -5,8 +5,9 @@ terms that cancel to O(res |f|); its rounding noise relative to the residual
 is ~ eps / res / sqrt(#entries).  Two runs whose iterates differ in a single
 bit disagree at that level, whatever their arithmetic.  This helper measures
 the floor on the oracle (bit-identical to the reference where the reference
-exists): the same solve with one ulp flipped in a random 0.1 % of the sine
-transforms' outputs, over a few seeds.  ``envelope`` turns the drifts into a
+exists): the same solve with one ulp flipped in a random half of the sine
+transforms' outputs (a model of an independent, equally accurate transform
+implementation), over 8 seeds.  ``envelope`` turns the drifts into a
 per-iteration bar: the running maximum over seeds and earlier iterations,
 never below the north_star's 1e-10.  See tests/golden/make_drift_floor.py
 for the committed ensembles of the reference's golden cases.
@@ -21,7 +22,7 @@ import numpy as np
 import oracle as orc
 import oracle.pint_oracle as O
 
-FRACTION = 1e-3
+FRACTION = 0.5
 
 
 @contextlib.contextmanager
@@ -54,7 +55,7 @@ def envelope(drifts, iters: int) -> np.ndarray:
     return np.maximum(1e-10, env[:iters])
 
 
-def floor_envelope(solve, ref_res, iters: int, seeds=(1, 2, 3, 4)) -> np.ndarray:
+def floor_envelope(solve, ref_res, iters: int, seeds=tuple(range(1, 9))) -> np.ndarray:
     """solve() -> residual list, run under perturbed transforms per seed;
     drift against ref_res (the unperturbed reference history)."""
     ref_res = np.asarray(ref_res)
@@ -67,7 +68,7 @@ def floor_envelope(solve, ref_res, iters: int, seeds=(1, 2, 3, 4)) -> np.ndarray
     return envelope(drifts, iters)
 
 
-def uzawa_envelope(pb, omega, tol, max_iter, ref_res, iters, seeds=(1, 2, 3, 4)):
+def uzawa_envelope(pb, omega, tol, max_iter, ref_res, iters, seeds=tuple(range(1, 9))):
     lev = orc.mg_levels(pb.space, pb.cells)
 
     def solve():
@@ -77,7 +78,7 @@ def uzawa_envelope(pb, omega, tol, max_iter, ref_res, iters, seeds=(1, 2, 3, 4))
     return floor_envelope(solve, ref_res, iters, seeds)
 
 
-def minres_envelope(pb, tol, max_iter, ref_res, iters, seeds=(1, 2, 3, 4)):
+def minres_envelope(pb, tol, max_iter, ref_res, iters, seeds=tuple(range(1, 9))):
     lev = orc.mg_levels(pb.space, pb.cells)
 
     def solve():
