@@ -46,6 +46,7 @@ extern "C" {
 /* which batched multigrid set a call refers to */
 #define PINT_MG_ATILDE 0   /* per-step blocks of A~ (solvers.py:127-155) */
 #define PINT_MG_HTILDE 1   /* per-mode blocks H_k of H~ (schur.py:30-52) */
+#define PINT_MG_EULER 2    /* per-step M + tau_n A_n of the sequential oracle (solvers.py:166-170) */
 
 typedef struct pint_ctx pint_ctx;
 
@@ -261,6 +262,35 @@ int pint_uzawa_run(pint_ctx* ctx, double omega, int iters, double* res_num, doub
 
 /* Number of kernel launches issued by this context so far (bench evidence). */
 long long pint_launch_count(const pint_ctx* ctx);
+
+
+/* ---------------------------------------------------------------------------
+ * Diagnostic mode on the device: the reference's exact-solve oracles.
+ * Every SPD spatial solve is multigrid-preconditioned CG to relative residual
+ * <= tol (1e-14 typical; it stops earlier only at the rounding floor),
+ * batched over planes.  Not available for per-point stiffness fields.
+ *
+ * pint_sequential_euler: forward implicit-Euler sweep
+ *   (M + tau_n A_n) u_n = M u_{n-1} + tau_n load_n        (solvers.py:158-174)
+ *   needs the PINT_MG_EULER set (tables of M + tau_n A_n, sid per step);
+ *   *iters = most CG iterations of any step, *worst_rel = largest final
+ *   relative residual.
+ * pint_s_norm: |a - b|_S (b may be NULL), the discrete parabolic norm
+ *   s(v,v) = sum tau_n (M dv_n/tau_n).A_n^{-1}(M dv_n/tau_n) + sum v.A_bd v
+ *            + v_N.M v_N + sum dv.M dv                   (operators.py:141-183)
+ *   needs the A~ set (its level-0 operators are the A_n).
+ * pint_uzawa_s_error: |u_j - u_star|_S of the context's Uzawa iterate
+ *   (uzawa_solve's diagnostic branch, solvers.py:236-244).
+ * pint_abd_inverse: out = A_bd^{-1} in, A_bd = diag(tau_n A_n)  (operators.py:113-122)
+ * ------------------------------------------------------------------------- */
+int pint_sequential_euler(pint_ctx* ctx, const double* load, const double* u_init,
+                          double* u_out, double tol, int max_iter, int* iters,
+                          double* worst_rel);
+int pint_s_norm(pint_ctx* ctx, const double* a, const double* b, double tol, int max_iter,
+                double* out);
+int pint_uzawa_s_error(pint_ctx* ctx, const double* u_star, double tol, int max_iter,
+                       double* out);
+int pint_abd_inverse(pint_ctx* ctx, const double* in, double* out, double tol, int max_iter);
 
 #ifdef __cplusplus
 }

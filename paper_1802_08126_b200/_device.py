@@ -14,11 +14,11 @@ import math
 
 import numpy as np
 
-from ._native import MG_ATILDE, MG_HTILDE, Context
+from ._native import MG_ATILDE, MG_EULER, MG_HTILDE, Context
 from .errors import InputError
 from .linalg import grid_fields, grid_stencil, grid_stencil3
 from .problems import WeightedStiffness
-from .spatial import DEFAULT_DAMPING, MgHierarchy, galerkin_tables
+from .spatial import DEFAULT_DAMPING, MgHierarchy, build_mg_hierarchy, galerkin_tables
 
 
 def _grid_side(spec):
@@ -155,6 +155,22 @@ class HostProblem:
         return galerkin_tables(st, hierarchy, damping), np.arange(self.N, dtype=np.int32)
 
 
+    def euler_tables(self, hierarchy: MgHierarchy, damping: float):
+        """Operators M + tau_n A_n of the sequential implicit-Euler oracle
+        (solvers.py:166-170), one set per distinct (A_n, tau_n); coefficient
+        fl(1.0 m) + fl(tau_n a) as add_matrices(1.0, M, tau, A_n) forms it."""
+        index: dict = {}
+        sets = []
+        sid = np.empty(self.N, dtype=np.int32)
+        for k, (a, tau) in enumerate(zip(self.spec.stiffness, self.steps)):
+            key = (id(a), float(tau))
+            if key not in index:
+                index[key] = len(sets)
+                sets.append(1.0 * self.mass_st + float(tau) * self._stencil(a, self.m))
+            sid[k] = index[key]
+        return galerkin_tables(np.stack(sets), hierarchy, damping), sid
+
+
 class GpuProblem(HostProblem):
     """Device copy of one ProblemSpec: stencils, steps, scales, MG sets."""
 
@@ -212,6 +228,23 @@ class GpuProblem(HostProblem):
             tab, sid = self.htilde_tables(hierarchy, damping, mu)
             self._upload_set(MG_HTILDE, hierarchy, tab, sid)
         self.htilde_ready = True
+
+    def ensure_exact(self):
+        """Multigrid sets the device-side exact solves precondition with: the
+        A~ set (operators A_n; configured with the default hierarchy unless a
+        BlockDiagSolver already did) and the EULER set (M + tau_n A_n)."""
+        if self.field is not None:
+            raise InputError("exact solves are not built for per-point stiffness fields")
+        if getattr(self, "exact_ready", False):
+            return
+        space = "2d" if self.dims == 2 else "3d"
+        hier = build_mg_hierarchy(space, self.m + 1)
+        damping = self.default_damping()
+        if not self.atilde_ready:
+            self.set_atilde(hier, damping)
+        tab, sid = self.euler_tables(hier, damping)
+        self._upload_set(MG_EULER, hier, tab, sid)
+        self.exact_ready = True
 
     def _set_field(self, which, hierarchy, damping, mu):
         if hierarchy.cells[0] - 1 != self.m or hierarchy.space != "2d":

@@ -43,7 +43,7 @@ def set_arithmetic(mode: str) -> str:
 
 def get_arithmetic() -> str:
     return _ARITH
-MG_ATILDE, MG_HTILDE = 0, 1
+MG_ATILDE, MG_HTILDE, MG_EULER = 0, 1, 2
 
 _P = ctypes.c_void_p
 _D = ctypes.c_double
@@ -99,6 +99,10 @@ _SIGNATURES = {
     "pint_field_assemble": (_I, [_P, _I, _I, _P]),
     "pint_field_aref": (_I, [_P, _I, _P]),
     "pint_mg_set_field": (_I, [_P, _I, _I, _P, _D, _P]),
+    "pint_sequential_euler": (_I, [_P, _P, _P, _P, _D, _I, _IP, _DP]),
+    "pint_s_norm": (_I, [_P, _P, _P, _D, _I, _DP]),
+    "pint_uzawa_s_error": (_I, [_P, _P, _D, _I, _DP]),
+    "pint_abd_inverse": (_I, [_P, _P, _P, _D, _I]),
 }
 
 _lib = None

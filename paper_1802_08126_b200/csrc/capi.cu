@@ -227,6 +227,7 @@ void free_problem(pint_ctx* c) {
     }
     free_field(c);
     free_slabs(c);
+    pint::exact_free(c);
     pint::dst_plan_free(c->dst);
     c->problem_ready = false;
     c->uz_ready = false;
@@ -511,7 +512,7 @@ int pint_mg_set(pint_ctx* c, int which, int levels, const int* level_m, int n_se
     return guarded(c, [&] {
         require_problem(c);
         graph_reset(c);
-        if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE)
+        if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE && which != PINT_MG_EULER)
             pint_throw(PINT_INPUT, "unknown multigrid set");
         if (levels < 2 || !level_m || !tables || !sid || n_sets < 1)
             pint_throw(PINT_INPUT, "bad multigrid description");
@@ -1123,6 +1124,89 @@ int pint_uzawa(pint_ctx* c, const double* f, double* p, double* u, double omega,
     }
     if (st != PINT_OK) return st;
     return pint_uzawa_end(c, p, u);
+}
+
+// ---------------------------------------------------------------------------
+// diagnostic mode: exact solves on the device (exact_solve.cu)
+// ---------------------------------------------------------------------------
+static void require_exact_capable(pint_ctx* c) {
+    require_problem(c);
+    if (c->field) pint_throw(PINT_INPUT, "exact solves are not built for per-point stiffness fields");
+}
+
+int pint_sequential_euler(pint_ctx* c, const double* load, const double* u_init, double* u_out,
+                          double tol, int max_iter, int* iters, double* worst_rel) {
+    return guarded(c, [&] {
+        require_exact_capable(c);
+        if (!load || !u_init || !u_out) pint_throw(PINT_INPUT, "null argument");
+        ensure_stage(c);
+        const double* dl = stage_in(c, load, c->d_stage_in, slab(c));
+        const double* du0 = u_init;
+        if (!is_device_ptr(u_init)) {
+            if (!c->d_vec) c->d_vec = dalloc<double>(c->n);
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_vec, u_init, c->n * sizeof(double),
+                                            cudaMemcpyHostToDevice, c->stream));
+            du0 = c->d_vec;
+        }
+        OutBuf o = stage_out(c, u_out, c->d_stage_out);
+        double rel = 0.0;
+        const int it = pint::sequential_euler(c, dl, du0, o.dev, tol, max_iter, &rel);
+        finish_out(c, o, slab(c));
+        if (iters) *iters = it;
+        if (worst_rel) *worst_rel = rel;
+    });
+}
+
+// |a - b|_S (b may be NULL): S-norm of operators.py:182-183
+int pint_s_norm(pint_ctx* c, const double* a, const double* b, double tol, int max_iter,
+                double* out) {
+    return guarded(c, [&] {
+        require_exact_capable(c);
+        if (!set_ready(c, PINT_MG_ATILDE)) pint_throw(PINT_INPUT, "A~ multigrid set not configured");
+        if (!a || !out) pint_throw(PINT_INPUT, "null argument");
+        ensure_stage(c);
+        const size_t S = slab(c);
+        const double* da = stage_in(c, a, c->d_stage_in, S);
+        const double* v = da;
+        if (b) {
+            const double* db = stage_in(c, b, c->d_stage_out, S);
+            pint::launch_lincomb(c, c->d_stage_out, da, -1.0, db, 0.0, nullptr, 1.0, false,
+                                 (long long)S);
+            v = c->d_stage_out;
+        }
+        const double q = pint::s_norm_sq(c, v, tol, max_iter, nullptr);
+        *out = std::sqrt(q > 0.0 ? q : 0.0);
+    });
+}
+
+// |u_j - u_star|_S of the Uzawa iterate held by the context (diagnostic mode
+// of uzawa_solve, solvers.py:236-244); u_star device or host
+int pint_uzawa_s_error(pint_ctx* c, const double* u_star, double tol, int max_iter, double* out) {
+    return guarded(c, [&] {
+        if (!c->uz_ready) pint_throw(PINT_INPUT, "pint_uzawa_begin not called");
+        require_exact_capable(c);
+        ensure_stage(c);
+        const size_t S = slab(c);
+        const double* ds = stage_in(c, u_star, c->d_stage_in, S);
+        pint::launch_lincomb(c, c->d_stage_out, c->d_u, -1.0, ds, 0.0, nullptr, 1.0, false,
+                             (long long)S);
+        const double q = pint::s_norm_sq(c, c->d_stage_out, tol, max_iter, nullptr);
+        *out = std::sqrt(q > 0.0 ? q : 0.0);
+    });
+}
+
+// exact A_bd^{-1} (operators.py:113-122)
+int pint_abd_inverse(pint_ctx* c, const double* in, double* out, double tol, int max_iter) {
+    return guarded(c, [&] {
+        require_exact_capable(c);
+        if (!set_ready(c, PINT_MG_ATILDE)) pint_throw(PINT_INPUT, "A~ multigrid set not configured");
+        ensure_stage(c);
+        const double* d = stage_in(c, in, c->d_stage_in, slab(c));
+        OutBuf o = stage_out(c, out, c->d_stage_out);
+        if (o.dev == d) pint_throw(PINT_INPUT, "in-place operator application is not supported");
+        pint::abd_inverse(c, d, o.dev, tol, max_iter);
+        finish_out(c, o, slab(c));
+    });
 }
 
 }  // extern "C"

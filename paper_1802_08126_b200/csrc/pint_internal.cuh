@@ -22,6 +22,7 @@
 
 #define PINT_S2 9   // 2D stencil size
 #define PINT_TW 10  // table row: 9 coefficients + dinv
+#define PINT_EX_BUFS 11  // work buffers of the diagnostic exact solves (exact_solve.cu)
 
 struct PintFail {
     int code;
@@ -131,7 +132,7 @@ struct pint_ctx {
     double* d_aref = nullptr;    // [9]
     bool problem_ready = false;
 
-    MgSet mg[2];
+    MgSet mg[3];  // PINT_MG_ATILDE, PINT_MG_HTILDE, PINT_MG_EULER
     // field mode (pint_field_set / pint_field_assemble): per-point stiffness
     bool field = false;
     double* d_fa = nullptr;      // [N][3][n] compact fine A_n (centre, east, north)
@@ -184,6 +185,10 @@ struct pint_ctx {
     std::vector<cudaEvent_t> prof_pool;
     std::vector<ProfRec> prof_open;
     KStat kstat[K_COUNT];
+
+    // diagnostic exact solves (exact_solve.cu)
+    double* ex_buf[PINT_EX_BUFS] = {};
+    size_t ex_cap[PINT_EX_BUFS] = {};
 };
 
 // RAII event pair around one launch when ctx->profile is on
@@ -280,6 +285,17 @@ void host_prefault_async(pint_ctx* c, void* p, size_t bytes);
 void host_prefault_join(pint_ctx* c);
 void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const double* in,
              double* out, const double* base, double alpha);
+
+// diagnostic-mode exact solves (exact_solve.cu): multigrid-preconditioned CG
+void st_apply(pint_ctx* c, const double* tab, int stride, const int* sid, const double* scale,
+              long long planes, const double* x, const double* base, double* y);
+int spd_solve(pint_ctx* c, int which, long long planes, const double* rhs, double* x,
+              double tol, int max_iter, double* rel_out);
+int sequential_euler(pint_ctx* c, const double* load, const double* u0, double* out,
+                     double tol, int max_iter, double* worst_rel);
+double s_norm_sq(pint_ctx* c, const double* v, double tol, int max_iter, int* iters);
+int abd_inverse(pint_ctx* c, const double* rhs, double* out, double tol, int max_iter);
+void exact_free(pint_ctx* c);
 
 // reductions (stencil_ops.cu)
 void reduce_partials(pint_ctx* c, int nparts, int slot);

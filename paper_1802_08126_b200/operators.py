@@ -4,18 +4,27 @@
 ``apply_K``, ``apply_Kt``, ``apply_Abd``, ``apply_B``, ``apply_Bt``,
 ``apply_saddle``) with the arithmetic done by the sm_100a kernels of
 csrc/stencil_ops.cu: block vectors of shape (N, dim), numpy (host) or CUDA
-float64 torch tensors (device), results of the same kind.  Diagnostic-mode
-operators (exact per-step inverses, S-norm, P, S; operators.py:51-214) are
-the reference's host-side SuperLU computations (diagnostics.py); they serve
-error measurement, never the iteration.
+float64 torch tensors (device), results of the same kind.
+
+Diagnostic mode (operators.py:51-214: exact A_bd^{-1}, P, S and the discrete
+parabolic S-norm) runs on the device too (csrc/exact_solve.cu): the exact
+per-step solves the reference does with SuperLU are multigrid-preconditioned
+CG solves to the rounding floor (relative residual <= EXACT_TOL), batched
+over all steps.  They measure errors; the Uzawa iteration never uses them.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 import numpy as np
 
 from ._device import gpu_problem
 from ._native import _is_tensor, as_buffer, empty_like_kind, ptr_of
+
+# exact solves of diagnostic mode: relative residual target and CG iteration cap
+EXACT_TOL = 1e-14
+EXACT_MAX_ITER = 200
 from .errors import DiagnosticModeRequiredError
 
 
@@ -50,46 +59,68 @@ class TimeGlobalSystem:
         return self._exact is not None
 
     def build_exact_solvers(self) -> None:
-        """Exact per-step factorisations on the host (operators.py:51-61)."""
-        if self._exact is None:
-            from .diagnostics import ExactNorms
-
-            self._exact = ExactNorms(self.spec)
+        """Enable diagnostic mode (operators.py:51-61): configures the
+        multigrid sets that precondition the device's exact solves."""
+        self._gp.ensure_exact()
+        self._exact = True
 
     def _need_exact(self):
         if self._exact is None:
             raise DiagnosticModeRequiredError(
                 "exact per-step factorizations not built; pass diagnostic=True")
-        return self._exact
 
     # --- diagnostic-mode operators and norms (operators.py:113-183) --------
     def apply_Abd_inv(self, b):
-        return self._need_exact().apply_Abd_inv(_host(b))
+        """diag(tau_n A_n)^{-1} b (operators.py:113-122)."""
+        self._need_exact()
+        shape = (self.spec.N, self.spec.dim)
+        ptr, keep = as_buffer(b, shape)
+        out = empty_like_kind(keep, shape)
+        self._gp.ctx.call("pint_abd_inverse", ptr, ptr_of(out), EXACT_TOL, EXACT_MAX_ITER)
+        return out
 
     def apply_P(self, u):
-        """Optimal-test-function map (operators.py:124-126)."""
-        return self.apply_Abd_inv(self.apply_K(_host(u))) + _host(u)
+        """Optimal test functions A_bd^{-1} K u + u (operators.py:124-126)."""
+        return self.apply_Abd_inv(self.apply_K(u)) + u
 
     def apply_Pt(self, u):
-        return self.apply_Kt(self.apply_Abd_inv(_host(u))) + _host(u)
+        return self.apply_Kt(self.apply_Abd_inv(u)) + u
 
     def apply_S(self, u):
-        """Schur complement operator (operators.py:131-139)."""
-        u = _host(u)
+        """Schur complement K^T A_bd^{-1} K u + K u + K^T u + A_bd u (operators.py:131-139)."""
         ku = self.apply_K(u)
         return self.apply_Kt(self.apply_Abd_inv(ku)) + ku + self.apply_Kt(u) + self.apply_Abd(u)
 
-    def a_norm(self, u) -> float:
-        return self._need_exact().a_norm(_host(u))
+    def s_norm_diff(self, a, b=None) -> float:
+        """|a - b|_S on the device (b = None: |a|_S)."""
+        self._need_exact()
+        shape = (self.spec.N, self.spec.dim)
+        pa, ka = as_buffer(a, shape)
+        pb, kb = as_buffer(b, shape) if b is not None else (None, None)
+        if _is_tensor(ka) or _is_tensor(kb):
+            import torch
 
-    def jump_form(self, u, v) -> float:
-        return self._need_exact().jump_form(_host(u), _host(v))
-
-    def s_bilinear(self, u, v) -> float:
-        return self._need_exact().s_bilinear(_host(u), _host(v))
+            torch.cuda.synchronize(self._gp.ctx.device)
+        out = ctypes.c_double()
+        self._gp.ctx.call("pint_s_norm", pa, pb, EXACT_TOL, EXACT_MAX_ITER, ctypes.byref(out))
+        return float(out.value)
 
     def s_norm(self, u) -> float:
-        return self._need_exact().s_norm(_host(u))
+        """Discrete parabolic norm (operators.py:182-183)."""
+        return self.s_norm_diff(u)
+
+    def s_bilinear(self, u, v) -> float:
+        """s(u, v) by polarisation of the device S-norm (operators.py:174-178)."""
+        return 0.25 * (self.s_norm_diff(u, -v) ** 2 - self.s_norm_diff(u, v) ** 2)
+
+    def jump_form(self, u, v) -> float:
+        """sum_n (u_n - u_{n-1}) . M (v_n - v_{n-1}) + u_N . M v_N, u_0 = v_0 = 0
+        (operators.py:146-153), host sparse products."""
+        u, v = _host(u), _host(v)
+        m = self.spec.mass
+        jumps_u = np.vstack([u[:1], u[1:] - u[:-1]])
+        jumps_v = np.vstack([v[:1], v[1:] - v[:-1]])
+        return float(np.einsum("ij,ij->", jumps_u, m.dot(jumps_v.T).T) + u[-1] @ m.dot(v[-1]))
 
     def _apply(self, name: str, u):
         shape = (self.spec.N, self.spec.dim)

@@ -15,10 +15,12 @@ The iteration itself is one call per iteration into libpint
 only the two partial sums come back.  ``fft_seconds`` / ``spatial_seconds``
 are cumulative device time of the DST and multigrid phases (CUDA events).
 Diagnostic mode (exact S-norm error per iteration, stopping='s_norm_error',
-solvers.py:201-244) keeps the iteration on the device and measures the error
-on the host against the sequential implicit-Euler solution with the
-reference's SuperLU factorisations (diagnostics.py): u is copied back once
-per iteration, as the reference's bench.run_table2 needs it.
+solvers.py:201-244) stays on the device end to end: the sequential
+implicit-Euler solution and every S-norm come from the device's exact solves
+(csrc/exact_solve.cu, ``sequential_euler_solve`` below), and the error of
+the iterate held in HBM is measured in place (pint_uzawa_s_error).
+The reference's rate theory (solvers.py:77-124) is analysis tooling, out of
+scope for the GPU path.
 """
 
 from __future__ import annotations
@@ -32,6 +34,7 @@ import numpy as np
 from ._device import gpu_problem
 from ._native import as_buffer, empty_like_kind, ptr_of
 from .errors import InputError
+from .operators import EXACT_MAX_ITER, EXACT_TOL
 from .spatial import MgHierarchy, _check_mg_options
 
 
@@ -90,42 +93,6 @@ class ConvergenceHistory:
         return "\n".join(out) + "\n"
 
 
-@dataclass(frozen=True)
-class RateReport:
-    """Contraction quantities of the damped two-stage iteration (solvers.py:77-88)."""
-
-    rho_a: float
-    omega: float
-    lam_min: float
-    lam_max: float
-    sigma_minus: float
-    sigma_plus: float
-    rho_u: float
-    damping_ok: bool
-
-
-def safe_damping(alpha: float, margin: float = 0.9) -> float:
-    """omega with omega * 3 alpha < 2 (solvers.py:91-100)."""
-    if alpha < 1.0:
-        raise InputError("quasi-uniformity constant is at least one")
-    return margin * 2.0 / (3.0 * alpha)
-
-
-def compute_rate_report(rho_a: float, omega: float, lam_min: float, lam_max: float) -> RateReport:
-    """Proven contraction rates (solvers.py:103-124)."""
-    if not 0.0 <= rho_a < 1.0:
-        raise InputError("preconditioner quality must lie in [0, 1)")
-    if omega <= 0.0 or lam_min <= 0.0 or lam_max <= 0.0:
-        raise InputError("damping and eigenvalue bounds must be positive")
-    tm = (1.0 - rho_a) * (1.0 - omega * lam_min)
-    sm = 0.5 * (tm + np.sqrt(4.0 * rho_a + tm ** 2))
-    tp = (1.0 + rho_a) * (1.0 + omega * lam_max) - 2.0
-    spl = 0.5 * (tp + np.sqrt(4.0 * rho_a + tp ** 2))
-    ok = omega * lam_max < 2.0 * (1.0 - rho_a) / (1.0 + rho_a)
-    return RateReport(rho_a, omega, lam_min, lam_max, float(sm), float(spl),
-                      float(max(sm, spl)), bool(ok))
-
-
 class BlockDiagSolver:
     """A~^{-1}: one V-cycle per step on A_n, divided by tau_n (solvers.py:127-155),
     all steps in one batched launch per level."""
@@ -154,6 +121,33 @@ class BlockDiagSolver:
 
     def forward(self, x):
         raise InputError("forward application requires direct (exact) solvers")
+
+
+def _sequential_euler_device(gp):
+    """u_n = (M + tau_n A_n)^{-1} (M u_{n-1} + tau_n load_n) on the device as a
+    CUDA tensor (the oracle of solvers.py:158-174, exact_solve.cu)."""
+    import torch
+
+    gp.ensure_exact()
+    spec = gp.spec
+    dev = torch.device("cuda", gp.ctx.device)
+    load = torch.from_numpy(np.ascontiguousarray(spec.load, dtype=np.float64)).to(dev)
+    u0 = torch.from_numpy(np.ascontiguousarray(spec.u_init, dtype=np.float64)).to(dev)
+    out = torch.empty((spec.N, spec.dim), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    it = ctypes.c_int()
+    rel = ctypes.c_double()
+    gp.ctx.call("pint_sequential_euler", load.data_ptr(), u0.data_ptr(), out.data_ptr(),
+                EXACT_TOL, EXACT_MAX_ITER, ctypes.byref(it), ctypes.byref(rel))
+    return out
+
+
+def sequential_euler_solve(spec, device=None) -> np.ndarray:
+    """Forward implicit-Euler sweep with exact per-step solves (the oracle of
+    solvers.py:158-174), on the GPU: one multigrid-preconditioned CG solve of
+    (M + tau_n A_n) u_n = M u_{n-1} + tau_n load_n per step, to the rounding
+    floor.  Returns a numpy array (N, dim)."""
+    return _sequential_euler_device(gpu_problem(spec, device)).cpu().numpy()
 
 
 def _is_cuda(x) -> bool:
@@ -188,17 +182,18 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
         p_ptr = u_ptr = None
         like = f_keep
     hist = ConvergenceHistory()
-    # diagnostic mode (solvers.py:201-210): exact solution and its S-norm on
-    # the host (diagnostics.py); the iterate u comes back once per iteration
+    # diagnostic mode (solvers.py:201-210): the exact solution and its S-norm
+    # on the device; the error of the device-resident iterate is measured in
+    # place each iteration
     u_star = s_norm_ref = None
     if diagnostics:
-        from .diagnostics import sequential_euler_solve
-
         system.build_exact_solvers()
-        u_star = np.asarray(u_oracle, dtype=np.float64) if u_oracle is not None \
-            else sequential_euler_solve(system.spec)
+        if u_oracle is not None:
+            u_star = u_oracle
+        else:
+            u_star = _sequential_euler_device(gp)
         s_norm_ref = system.s_norm(u_star)
-        u_host = np.empty(shape)
+        us_ptr, us_keep = as_buffer(u_star, shape)
     if any(_is_cuda(x) for x in (f_keep, p_ptr and p_keep, u_ptr and u_keep)):
         # the library reads device inputs on its own stream: order it after
         # torch's pending writes (.contiguous(), .cuda(), the caller's kernels)
@@ -231,8 +226,10 @@ def uzawa_solve(system, atilde, htilde, cfg: UzawaConfig, initial=None, u_oracle
             ctx.call("pint_phase_ms", ms.ctypes.data)
             s_err = None
             if diagnostics:
-                ctx.call("pint_uzawa_end", None, u_host.ctypes.data)  # copy u, keep iterating
-                s_err = system.s_norm(u_host - u_star) / s_norm_ref
+                err = ctypes.c_double()
+                ctx.call("pint_uzawa_s_error", us_ptr, EXACT_TOL, EXACT_MAX_ITER,
+                         ctypes.byref(err))
+                s_err = err.value / s_norm_ref
             hist.append(res, s_err, None, time.perf_counter() - t0, ms[0] / 1e3, ms[1] / 1e3)
             if res > 1e6 * first:
                 from .errors import SolverDivergenceError

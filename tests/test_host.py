@@ -153,7 +153,6 @@ def test_config_and_history_types():
     h = pg.ConvergenceHistory()
     h.append(0.5, None, None, 1.0, 0.1, 0.2)
     assert h.to_csv().splitlines()[1] == "1,0.5,,,1,0.10000000000000001,0.20000000000000001"
-    assert pg.safe_damping(1.0) == pytest.approx(0.6)
 
 
 def test_library_exports_every_header_symbol():
