@@ -79,10 +79,37 @@ def operator_case(spec, seed, uzawa_tol, max_iter=300, omega=0.9):
     return out
 
 
+def write_c2_summary(run_dir):
+    """c2_summary.npz from a full config-2 reference run (run_ref_c2.py):
+    17-digit residual history, reference S-norms, seeded samples of the final
+    p, u and of the sequential-Euler solution, and per-plane 2-norms."""
+    h = json.load(open(os.path.join(run_dir, "c2_hist.json")))
+    u = np.load(os.path.join(run_dir, "c2_u.npy"))
+    p = np.load(os.path.join(run_dir, "c2_p.npy"))
+    useq = np.load(os.path.join(run_dir, "c2_useq.npy"))
+    idx = np.sort(np.random.default_rng(123).choice(u.size, 4096, replace=False))
+    np.savez_compressed(os.path.join(HERE, "c2_summary.npz"),
+                        residual=np.array(h["residual"]), converged=np.array(h["converged"]),
+                        sample_idx=idx, u_sample=u.ravel()[idx], p_sample=p.ravel()[idx],
+                        useq_sample=useq.ravel()[idx],
+                        u_plane_norms=np.linalg.norm(u, axis=1),
+                        p_plane_norms=np.linalg.norm(p, axis=1),
+                        useq_plane_norms=np.linalg.norm(useq, axis=1),
+                        s_norm_seq=np.array(h["s_norm_seq"]), s_norm_u=np.array(h["s_norm_u"]),
+                        s_norm_err=np.array(h["s_norm_err"]),
+                        solve_s=np.array(h["solve_s"]), setup_s=np.array(h["setup_s"]),
+                        wall=np.array(h["wall"]), fft=np.array(h["fft"]),
+                        spatial=np.array(h["spatial"]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", default=None, help="directory with the c2 reference run")
+    ap.add_argument("--only-c2", action="store_true", help="write c2_summary.npz only")
     args = ap.parse_args()
+    if args.only_c2:
+        write_c2_summary(args.c2)
+        return
 
     # A: 2D, perturbed grid, c(t) coefficient, random data (test-suite style)
     grid = ps.build_time_grid("perturbed", 16, 1.3, perturbation=0.3, seed=3)
@@ -125,17 +152,7 @@ def main():
                         s_norm_seq=np.array(system.s_norm(u_star)))
 
     if args.c2:
-        h = json.load(open(os.path.join(args.c2, "c2_hist.json")))
-        u = np.load(os.path.join(args.c2, "c2_u.npy"))
-        p = np.load(os.path.join(args.c2, "c2_p.npy"))
-        idx = np.random.default_rng(123).choice(u.size, 4096, replace=False)
-        np.savez_compressed(os.path.join(HERE, "c2_summary.npz"),
-                            residual=np.array(h["residual"]), converged=np.array(h["converged"]),
-                            u_sample_idx=idx, u_sample=u.ravel()[idx], p_sample=p.ravel()[idx],
-                            u_norm=np.array(np.linalg.norm(u)), p_norm=np.array(np.linalg.norm(p)),
-                            u_plane_norms=np.linalg.norm(u, axis=1),
-                            solve_s=np.array(h["solve_s"]), setup_s=np.array(h["setup_s"]),
-                            wall=np.array(h["wall"]))
+        write_c2_summary(args.c2)
     print("golden fixtures written to", HERE)
 
 
