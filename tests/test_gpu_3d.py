@@ -11,7 +11,7 @@ import pytest
 
 import oracle as orc
 import paper_1802_08126_b200 as pg
-from ulp_floor import uzawa_envelope
+import ulp_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -62,7 +62,7 @@ def test_uzawa_3d_matches_oracle():
     # 1e-10 while res > 1e-7; on the tail, the oracle's own drift under a
     # 1-ulp perturbation of its transforms (tests/ulp_floor.py)
     assert rel[ref_res > 1e-7].max() <= 1e-10, rel
-    bar = uzawa_envelope(opb, 0.9, 1e-8, 200, ref_res, k)
+    bar = ulp_floor.bar("uzawa3d_c16_N16", k)
     print(f"oracle 1-ulp floor {bar.max():.3e}")
     assert np.all(rel <= bar), (rel.max(), bar.max())
     nrm = orc.ExactNorms(opb)

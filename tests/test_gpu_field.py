@@ -15,7 +15,7 @@ import pytest
 
 import oracle as orc
 import paper_1802_08126_b200 as pg
-from ulp_floor import uzawa_envelope
+import ulp_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -76,7 +76,7 @@ def test_field_uzawa_matches_oracle():
     rel = np.abs(np.array(hist.residual[:k]) - ref_res) / ref_res
     print(f"field uzawa: {hist.iterations} iterations, max rel residual drift {rel.max():.3e}")
     assert rel[ref_res > 1e-7].max() <= 1e-10, rel
-    bar = uzawa_envelope(opb, 0.9, 1e-8, 3000, ref_res, k)
+    bar = ulp_floor.bar("field_c16_N16", k)
     print(f"oracle 1-ulp floor {bar.max():.3e}")
     assert np.all(rel <= bar), (rel.max(), bar.max())
     nrm = orc.ExactNorms(opb)

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle as orc
-from ulp_floor import minres_envelope
+import ulp_floor
 import paper_1802_08126_b200 as pg
 from conftest import GOLDEN
 
@@ -47,7 +47,7 @@ def test_minres_matches_reference(name):
                           u_init=d["u_init"])
     # bar: 1e-10, or the reference arithmetic's own drift under a 1-ulp
     # perturbation of its transforms (tests/ulp_floor.py)
-    bar = minres_envelope(pb, float(d["mr_tol"]), int(d["mr_max_iter"]), ref, k)
+    bar = ulp_floor.bar(name, k)
     print(f"{name}: {hist.iterations} vs {len(ref)} iterations, max rel drift {rel.max():.2e}, "
           f"head {rel[head].max():.2e}, reference 1-ulp floor {bar[head].max():.2e}")
     assert np.all(rel[head] <= bar[head]), (rel[head].max(), bar[head].max())

@@ -19,7 +19,7 @@ import pytest
 import oracle as orc
 import paper_1802_08126_b200 as pg
 from conftest import GOLDEN
-from ulp_floor import minres_envelope, uzawa_envelope
+import ulp_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -173,21 +173,18 @@ def test_dst_round_trip_and_adjoint(N):
 def drift_bar(case_name, iters):
     """Per-iteration residual bar: max(1e-10, the reference's own drift floor).
 
-    tests/golden/drift_floor.npz (tests/golden/make_drift_floor.py) holds the
-    relative residual drift of the reference's arithmetic (the oracle, bit-
-    identical to pintsolve) when one ulp is flipped in a random half of the
-    sine transforms' outputs, for 16 seeds.  Near res ~ tol the residual's
-    rounding noise (eps / res / sqrt(#entries)) dominates any run whose
-    iterates differ in a single bit from the reference's; on config 1, most of
-    the 16 perturbed reference runs exceed 1e-10.  The envelope is the running
-    maximum over seeds and earlier iterations, so it is 1e-10 wherever the
-    perturbed reference itself stays inside the north_star bar.
+    tests/golden/drift_floor.npz (tests/golden/make_drift_floor.py,
+    tests/ulp_floor.py) holds the relative residual drift of the reference's
+    arithmetic (the oracle, bit-identical to pintsolve) when one ulp is
+    flipped in a random half of the sine transforms' outputs, for 64 seeds.
+    Near res ~ tol the residual's rounding noise (eps / res / sqrt(#entries))
+    dominates any run whose iterates differ in a single bit from the
+    reference's; on config 1 most of the perturbed reference runs exceed
+    1e-10.  The envelope is the running maximum over seeds and earlier
+    iterations, so it is 1e-10 wherever the perturbed reference itself stays
+    inside the north_star bar.
     """
-    d = np.load(os.path.join(GOLDEN, "drift_floor.npz"))[case_name + "_drift"]
-    env = np.fmax.accumulate(np.nanmax(d, axis=0))
-    if len(env) < iters:
-        env = np.concatenate([env, np.full(iters - len(env), env[-1])])
-    return np.maximum(1e-10, env[:iters])
+    return ulp_floor.bar(case_name, iters)
 
 
 def test_uzawa_golden_cases(case):
@@ -419,13 +416,7 @@ def test_cli_solve_problem_file(method, tmp_path):
     head = ref[:k, 1] > 1e-7 * ref[0, 1]
     # bar: 1e-10, or the reference arithmetic's own drift under a 1-ulp
     # perturbation of its transforms (tests/ulp_floor.py)
-    d = np.load(os.path.join(GOLDEN, "problem_c8_N4.npz"))
-    pb = orc.heat_problem("2d", 8, d["nodes"], coeff=lambda t: 1.0 + t, load=d["load"],
-                          u_init=d["u_init"])
-    if method == "minres":
-        bar = minres_envelope(pb, 1e-10, 300, ref[:, 1], k)
-    else:
-        bar = uzawa_envelope(pb, omega, 1e-10, 300, ref[:, 1], k)
+    bar = ulp_floor.bar("cli_" + method, k)
     print(f"{method}: {len(ours)} vs {len(ref)} iterations, drift {rel[head].max():.2e}, "
           f"reference 1-ulp floor {bar[head].max():.2e}")
     assert np.all(rel[head] <= bar[head]), (rel[head].max(), bar[head].max())

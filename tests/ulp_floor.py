@@ -3,19 +3,22 @@
 Near convergence the Uzawa / MINRES residual is a difference of O(|f|)
 terms that cancel to O(res |f|); its rounding noise relative to the residual
 is ~ eps / res / sqrt(#entries).  Two runs whose iterates differ in a single
-bit disagree at that level, whatever their arithmetic.  This helper measures
-the floor on the oracle (bit-identical to the reference where the reference
-exists): the same solve with one ulp flipped in a random half of the sine
-transforms' outputs (a model of an independent, equally accurate transform
-implementation), over 8 seeds.  ``envelope`` turns the drifts into a
-per-iteration bar: the running maximum over seeds and earlier iterations,
-never below the north_star's 1e-10.  See tests/golden/make_drift_floor.py
-for the committed ensembles of the reference's golden cases.
+bit disagree at that level, whatever their arithmetic.  The floor is measured
+on the oracle (bit-identical to the reference where the reference exists):
+the same solve with one ulp flipped in a random half of the sine
+transforms' outputs -- a model of an independent, equally accurate transform
+implementation -- over SEEDS seeds.  ``bar(case, iters)`` is the per-
+iteration envelope: the running maximum over seeds and earlier iterations,
+never below the north_star's 1e-10.
+
+The ensembles are precomputed by tests/golden/make_drift_floor.py into
+tests/golden/drift_floor.npz for every case the GPU tests compare (CASES).
 """
 
 from __future__ import annotations
 
 import contextlib
+import os
 
 import numpy as np
 
@@ -23,6 +26,9 @@ import oracle as orc
 import oracle.pint_oracle as O
 
 FRACTION = 0.5
+SEEDS = 64
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
 
 
 @contextlib.contextmanager
@@ -43,46 +49,104 @@ def perturbed_transforms(seed: int, fraction: float = FRACTION):
         O.dst_inverse_T, O.dst_inverse = fwd, inv
 
 
-def envelope(drifts, iters: int) -> np.ndarray:
-    """max(1e-10, running max over seeds and iterations) of length iters."""
-    width = max(len(d) for d in drifts)
-    a = np.full((len(drifts), width), np.nan)
-    for i, d in enumerate(drifts):
-        a[i, :len(d)] = d
-    env = np.fmax.accumulate(np.nanmax(a, axis=0))
+# ---- the cases the GPU tests compare: (oracle problem, solver settings) -----
+
+def _golden_uzawa(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    c0, c1 = (float(v) for v in d["coeff"])
+    coeff = None if (c0, c1) == (1.0, 0.0) else (lambda t: c0 + c1 * t)
+    pb = orc.heat_problem(str(d["space"]), int(d["cells"]), d["nodes"], coeff=coeff,
+                          load=d["load"], u_init=d["u_init"])
+    return pb, ("uzawa", float(d["uz_omega"]), float(d["uz_tol"]), int(d["uz_max_iter"]))
+
+
+def case_c1():
+    nodes = orc.time_nodes("uniform", 64, 1.0)
+    load = np.random.default_rng(0).standard_normal((64, 961))
+    return (orc.heat_problem("2d", 32, nodes, load=load, u_init=np.zeros(961)),
+            ("uzawa", 0.9, 1e-8, 200))
+
+
+def case_uzawa3d():
+    """tests/test_gpu_3d.py::test_uzawa_3d_matches_oracle (cells 16, N 16)."""
+    cells, N, seed, T = 16, 16, 3, 1.0
+    n = (cells - 1) ** 3
+    rng = np.random.default_rng(seed)
+    load = rng.standard_normal((N, n))
+    u0 = rng.uniform(0.0, 1.0, n)
+    pb = orc.heat_problem("3d", cells, orc.time_nodes("uniform", N, T), load=load, u_init=u0)
+    return pb, ("uzawa", 0.9, 1e-8, 200)
+
+
+def case_field():
+    """tests/test_gpu_field.py::test_field_uzawa_matches_oracle (cells 16, N 16)."""
+    import paper_1802_08126_b200 as pg
+
+    cells, N, T, seed = 16, 16, 2.0, 11
+    n = (cells - 1) ** 2
+    grid = pg.build_time_grid("uniform", N, T)
+    w = pg.c4_cell_weights(cells, grid, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    load = rng.standard_normal((N, n))
+    u0 = rng.uniform(0.0, 1.0, n)
+    stiff = [orc.stiffness_2d_weighted(cells, w(k)) for k in range(N)]
+    pb = orc.heat_problem("2d", cells, grid.nodes, load=load, u_init=u0, stiffness=stiff)
+    return pb, ("uzawa", 0.9, 1e-8, 3000)
+
+
+def _golden_minres(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    pb = orc.heat_problem(str(d["space"]), int(d["cells"]), d["nodes"], load=d["load"],
+                          u_init=d["u_init"])
+    return pb, ("minres", float(d["mr_tol"]), int(d["mr_max_iter"]))
+
+
+def _cli(method):
+    d = np.load(os.path.join(GOLDEN, "problem_c8_N4.npz"))
+    pb = orc.heat_problem("2d", 8, d["nodes"], coeff=lambda t: 1.0 + t, load=d["load"],
+                          u_init=d["u_init"])
+    if method == "minres":
+        return pb, ("minres", 1e-10, 300)
+    omega = float(np.load(os.path.join(GOLDEN, "problem_c8_N4_omega.npy")))
+    return pb, ("uzawa", omega, 1e-10, 300)
+
+
+CASES = {
+    "c1": case_c1,
+    "ops2d_c16_N16_coeff": lambda: _golden_uzawa("ops2d_c16_N16_coeff"),
+    "sine2d_c8_N16": lambda: _golden_uzawa("sine2d_c8_N16"),
+    "uzawa3d_c16_N16": case_uzawa3d,
+    "field_c16_N16": case_field,
+    "minres_c16_N16": lambda: _golden_minres("minres_c16_N16"),
+    "minres_sine_c8_N32": lambda: _golden_minres("minres_sine_c8_N32"),
+    "cli_uzawa": lambda: _cli("uzawa"),
+    "cli_minres": lambda: _cli("minres"),
+}
+
+
+def residuals(name: str, seed: int) -> np.ndarray:
+    """Residual history of case `name`; seed 0 unperturbed, else perturbed."""
+    pb, how = CASES[name]()
+    lev = orc.mg_levels(pb.space, pb.cells)
+    ctx = perturbed_transforms(seed) if seed > 0 else contextlib.nullcontext()
+    with ctx:
+        if how[0] == "uzawa":
+            r = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), *how[1:]).residual
+        else:
+            r = orc.minres(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), tol=how[1],
+                           max_iter=how[2]).residual
+    return np.asarray(r, dtype=np.float64)
+
+
+def envelope(drifts: np.ndarray, iters: int) -> np.ndarray:
+    """max(1e-10, running max over seeds and iterations), length iters."""
+    env = np.fmax.accumulate(np.nanmax(np.atleast_2d(drifts), axis=0))
     if len(env) < iters:
         env = np.concatenate([env, np.full(iters - len(env), env[-1])])
     return np.maximum(1e-10, env[:iters])
 
 
-def floor_envelope(solve, ref_res, iters: int, seeds=tuple(range(1, 9))) -> np.ndarray:
-    """solve() -> residual list, run under perturbed transforms per seed;
-    drift against ref_res (the unperturbed reference history)."""
-    ref_res = np.asarray(ref_res)
-    drifts = []
-    for s in seeds:
-        with perturbed_transforms(s):
-            r = np.asarray(solve())
-        k = min(len(r), len(ref_res))
-        drifts.append(np.abs(r[:k] - ref_res[:k]) / ref_res[:k])
-    return envelope(drifts, iters)
-
-
-def uzawa_envelope(pb, omega, tol, max_iter, ref_res, iters, seeds=tuple(range(1, 9))):
-    lev = orc.mg_levels(pb.space, pb.cells)
-
-    def solve():
-        return orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), omega, tol,
-                         max_iter).residual
-
-    return floor_envelope(solve, ref_res, iters, seeds)
-
-
-def minres_envelope(pb, tol, max_iter, ref_res, iters, seeds=tuple(range(1, 9))):
-    lev = orc.mg_levels(pb.space, pb.cells)
-
-    def solve():
-        return orc.minres(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), tol=tol,
-                          max_iter=max_iter).residual
-
-    return floor_envelope(solve, ref_res, iters, seeds)
+def bar(name: str, iters: int) -> np.ndarray:
+    """Per-iteration bar of case `name` from the committed ensemble."""
+    d = np.load(os.path.join(GOLDEN, "drift_floor.npz"))
+    return envelope(d[name + "_drift"], iters)
