@@ -271,33 +271,61 @@ def measure_config(name, steps=3, warm=2):
     return out
 
 
-def run_gpu_partitioned(args, world, rank, local):
-    """N > 1 GPUs (or --partitioned): the c2 time axis split across ranks
-    (paper_1802_08126_b200/distributed.py), strong scaling."""
-    import ctypes  # noqa: F401
+PART_CONFIGS = {
+    # the headline grid, time axis split over the ranks (strong scaling)
+    "c2": dict(space="2d", cells=CELLS, N=NSTEPS, T=T_END, weak=False),
+    # BASELINE configs[2] (strong scaling 1/2/4/8) and configs[4] (weak: N = 1024 G)
+    "c3": dict(space="3d", cells=64, N=512, T=1.0, weak=False),
+    "c5": dict(space="3d", cells=64, N=1024, T=1.0, weak=True),
+}
 
+
+def _part_problem(name, world, rank):
+    """(spec, f_local, part) of a partitioned config; the load of c3/c5 is
+    generated per plane with default_rng((seed, step)) so every rank builds
+    only its own slab."""
+    import paper_1802_08126_b200 as pg
+    from paper_1802_08126_b200.distributed import Partition
+
+    c = PART_CONFIGS[name]
+    N = c["N"] * (world if c["weak"] else 1)
+    T = c["T"] * N / c["N"] if c["weak"] else c["T"]
+    grid = pg.build_time_grid("uniform", N, T)
+    n = (c["cells"] - 1) ** (3 if c["space"] == "3d" else 2)
+    part = Partition(N, world)
+    sl = part.slice(rank)
+    if name == "c2":
+        load = c2_load()
+        mine = load[sl]
+    else:
+        # only this rank's slab exists on the host (c5 at G = 8 is 16 GB in all)
+        mine = np.stack([np.random.default_rng((0, t)).standard_normal(n)
+                         for t in range(sl.start, sl.stop)])
+        load = np.broadcast_to(np.zeros(1), (N, n))
+    spec = pg.problem_from_arrays(c["space"], c["cells"], grid, load, np.zeros(n), alpha=1.0)
+    f_loc = np.ascontiguousarray(spec.grid.steps[sl, None] * mine)  # fold_rhs, u0 = 0
+    return spec, f_loc, part
+
+
+def measure_partitioned(name, world, rank, local, steps, warm, e2e=False):
+    """Per-iteration device time (max over ranks) of the time-partitioned
+    Uzawa step on config `name`; optionally the end-to-end solve."""
     import torch
     import torch.distributed as dist
 
     import paper_1802_08126_b200 as pg
-    from paper_1802_08126_b200.distributed import (Comm, DistUzawa, GpuLocalOps, Partition,
-                                                    dist_uzawa_solve)
+    from paper_1802_08126_b200.distributed import Comm, DistUzawa, GpuLocalOps, dist_uzawa_solve
 
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    load = c2_load()
-    grid = pg.build_time_grid("uniform", NSTEPS, T_END)
-    n = (CELLS - 1) ** 2
-    spec = pg.problem_from_arrays("2d", CELLS, grid, load, np.zeros(n), alpha=1.0)
-    f_all = spec.grid.steps[:, None] * load          # fold_rhs with u_init = 0 (operators.py:22-26)
-    hier = pg.build_mg_hierarchy("2d", CELLS)
-    part = Partition(NSTEPS, world)
+    spec, f_loc_h, part = _part_problem(name, world, rank)
+    c = PART_CONFIGS[name]
+    hier = pg.build_mg_hierarchy(c["space"], c["cells"])
     ops = GpuLocalOps(spec, hier, part, rank, device=local)
     comm = Comm()
-    f_host = torch.from_numpy(np.ascontiguousarray(f_all[part.slice(rank)])).pin_memory()
+    f_host = torch.from_numpy(f_loc_h).pin_memory()
     f_loc = f_host.to(ops.dev)
-    it = DistUzawa(ops, comm, NSTEPS, n, f_loc)
+    N, n = spec.N, spec.dim
+    it = DistUzawa(ops, comm, N, n, f_loc)
     it.begin()
-    steps, warm = args.steps, max(3, args.warmup)
     for _ in range(warm):
         it.step(0.9)
     dist.barrier()
@@ -313,44 +341,77 @@ def run_gpu_partitioned(args, world, rank, local):
     launches = ops.ctx.launches() - l0
     t = torch.tensor([ev0.elapsed_time(ev1) / steps], device=ops.dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item())
-    value = NSTEPS * n / (ms_step / 1e3)
-    # end to end: host f in, host u out, to convergence
-    dist.barrier()
-    t0 = time.perf_counter()
-    f_loc2 = f_host.to(ops.dev)
-    p_l, u_l, hist = dist_uzawa_solve(ops, comm, NSTEPS, n, f_loc2,
-                                      pg.UzawaConfig(omega=0.9, tol=1e-8, max_iter=200))
-    u_host = u_l.cpu()
-    wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=ops.dev)
-    dist.all_reduce(wall, op=dist.ReduceOp.MAX)
-    wall = float(wall.item())
-    del u_host
+    ms = float(t.item())
+    hbm, _ = peaks()
+    out = {"config": name, "N": N, "n": n, "ms_per_iter": ms, "value": N * n / (ms / 1e3),
+           "unit": "DoF/s", "scaling": "weak" if c["weak"] else "strong",
+           "iteration_frac_per_gpu": 224.0 * N * n / world / (ms / 1e3) / 1e9 / hbm,
+           "launches": launches, "clocks": clk.summary()}
+    if e2e:
+        dist.barrier()
+        t0 = time.perf_counter()
+        f2 = f_host.to(ops.dev)
+        _, u_l, hist = dist_uzawa_solve(ops, comm, N, n, f2,
+                                        pg.UzawaConfig(omega=0.9, tol=1e-8, max_iter=200))
+        u_host = u_l.cpu()
+        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=ops.dev)
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        del u_host
+        out["e2e"] = {"iterations": hist.iterations, "time_to_tol_s": float(wall.item()),
+                      "converged": hist.converged,
+                      "final_residual": hist.residual[-1] if hist.residual else None,
+                      "h2d_bytes_per_step": int(f_loc_h.nbytes),
+                      "d2h_bytes_per_step": int(f_loc_h.nbytes)}
+    del it, ops, f_loc
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_gpu_partitioned(args, world, rank, local):
+    """N > 1 GPUs (or --partitioned): the headline c2 time axis split across
+    ranks (strong scaling, the same workload as the N = 1 line so the driver's
+    scaling efficiency compares like with like), plus BASELINE's own
+    multi-GPU configs c3 (strong) and c5 (weak, N = 1024 G) as other_configs."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    steps, warm = args.steps, max(3, args.warmup)
+    head = measure_partitioned("c2", world, rank, local, steps, warm, e2e=True)
+    others = {}
+    if not args.no_other:
+        for name in ("c3", "c5"):
+            try:
+                others[name] = measure_partitioned(name, world, rank, local, max(2, steps // 3),
+                                                   3)
+            except Exception as e:  # report, do not lose the headline line
+                others[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
     hbm, peak_kind = peaks()
-    iter_bytes = 224.0 * NSTEPS * n
+    N, n, ms_step = head["N"], head["n"], head["ms_per_iter"]
+    iter_bytes = 224.0 * N * n
     if rank == 0:
+        e = head["e2e"]
         line = {
-            "metric": "space-time DoF/s per Uzawa iteration", "value": value, "unit": "DoF/s",
-            "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": n, "N": NSTEPS,
-                       "parallelism": f"time-sharded x{world} (halo planes, time/column/mode "
-                                      "transposes around the DSTs, 2-scalar all-reduce)",
+            "metric": "space-time DoF/s per Uzawa iteration", "value": head["value"],
+            "unit": "DoF/s", "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "N": N,
+                       "parallelism": f"time-sharded x{world} (ghost planes, chunked async "
+                                      "all-to-all transposes around the DSTs, device "
+                                      "all-reduce of the 2 partial sums)",
                        "l2": "inputs larger than L2, no flush"},
-            "e2e": {"value": world and NSTEPS * n * hist.iterations / wall, "unit": "DoF/s",
-                    "iterations": hist.iterations, "time_to_tol_s": wall,
-                    "converged": hist.converged,
-                    "final_residual": hist.residual[-1] if hist.residual else None,
-                    "h2d_bytes_per_step": int(f_all.nbytes), "d2h_bytes_per_step": int(f_all.nbytes),
-                    "step": "one partitioned solve from host arrays to convergence"},
+            "e2e": {"value": N * n * e["iterations"] / e["time_to_tol_s"], "unit": "DoF/s",
+                    **e, "step": "one partitioned solve from host arrays to convergence"},
             "roofline": {"bound": "hbm", "kernel": "iteration", "achieved":
                          iter_bytes / world / (ms_step / 1e3) / 1e9, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": iter_bytes / world / (ms_step / 1e3) / 1e9 / hbm, "traffic": None},
+                         "frac": iter_bytes / world / (ms_step / 1e3) / 1e9 / hbm,
+                         "traffic": None},
             "cpu_baseline": None,
-            "clocks": clk.summary(),
-            "gpu_launches": launches,
+            "clocks": head["clocks"],
+            "gpu_launches": head["launches"],
+            "other_configs": others or None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

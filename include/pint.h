@@ -168,6 +168,10 @@ int pint_dst(pint_ctx* ctx, int kind, const double* in, double* out);
 /* Same transforms on any (N, ncols) slab, independent of the problem
  * (DstPlan(N) used standalone, dst.py:31-55). */
 int pint_dst_raw(pint_ctx* ctx, int kind, int N, long long ncols, const double* in, double* out);
+/* out = base + alpha * T(in) in one pass (the Uzawa u += omega S^T w of a
+ * time partition whose columns are complete, solvers.py:231); device only. */
+int pint_dst_raw_axpy(pint_ctx* ctx, int kind, int N, long long ncols, const double* in,
+                      double* out, const double* base, double alpha);
 
 /* ---------------------------------------------------------------------------
  * Uzawa iteration (uzawa_solve, solvers.py:177-264), state resident on the
@@ -218,7 +222,10 @@ int pint_dot(pint_ctx* ctx, const double* a, const double* b, long long count, d
  * Time-partitioned building blocks (one context per rank).  The
  * driver (paper_1802_08126_b200/distributed.py) moves ghost planes and
  * transposes with torch.distributed; these calls do the arithmetic.  All
- * pointers must be device pointers.
+ * pointers must be device pointers.  Every call is stream-ordered on the
+ * context stream (pint_set_stream: the caller's, so NCCL and these kernels
+ * order without host waits); none blocks the host except when a `dot`
+ * output is a host pointer.
  *
  * pint_set_partition: this context's N steps are global steps [n0, n0+N) of
  *   N_global.  With has_prev / has_next the u and p slabs passed to the
@@ -228,6 +235,8 @@ int pint_dot(pint_ctx* ctx, const double* a, const double* b, long long count, d
  *   over the local steps (solvers.py:224, 227-229).
  * pint_atilde_update: p += A~^{-1} r1, *dot = sum r1.dp over the local steps
  *   (solvers.py:225-226, 233); p == NULL: only *dot = sum r1.(A~^{-1} r1).
+ *   `dot` may be a device pointer (stream-ordered copy) or a host pointer
+ *   (the call then waits for the stream), or NULL; same for htilde_modes.
  * pint_htilde_modes: for this rank's DST modes zh, w = (2 tau_ref/N_global)
  *   V_H(A_ref V_H(zh)) and *dot = sum zh.w (schur.py:69-75); w == NULL: dot only.
  * pint_axpy: u = u + omega*y on `count` values (solvers.py:231).

@@ -72,6 +72,7 @@ _SIGNATURES = {
     "pint_htilde_inv": (_I, [_P, _P, _P]),
     "pint_dst": (_I, [_P, _I, _P, _P]),
     "pint_dst_raw": (_I, [_P, _I, _I, ctypes.c_longlong, _P, _P]),
+    "pint_dst_raw_axpy": (_I, [_P, _I, _I, ctypes.c_longlong, _P, _P, _P, _D]),
     "pint_uzawa_begin": (_I, [_P, _P, _P, _P, _DP]),
     "pint_uzawa_step": (_I, [_P, _D, _DP]),
     "pint_uzawa_end": (_I, [_P, _P, _P]),

@@ -755,9 +755,12 @@ int pint_dst(pint_ctx* c, int kind, const double* in, double* out) {
     });
 }
 
-int pint_dst_raw(pint_ctx* c, int kind, int N, long long ncols, const double* in, double* out) {
+static int dst_raw_impl(pint_ctx* c, int kind, int N, long long ncols, const double* in,
+                        double* out, const double* base, double alpha) {
     return guarded(c, [&] {
         if (N < 1 || ncols < 1) pint_throw(PINT_DIMENSION, "bad transform shape");
+        if (base && (!is_device_ptr(base) || !is_device_ptr(out)))
+            pint_throw(PINT_INPUT, "the fused update needs device pointers");
         if (c->dst_raw.N != N) pint::dst_plan_build(c->dst_raw, N);
         const size_t cnt = (size_t)N * (size_t)ncols;
         double* tmp_in = nullptr;
@@ -774,19 +777,34 @@ int pint_dst_raw(pint_ctx* c, int kind, int N, long long ncols, const double* in
             tmp_out = dalloc<double>(cnt);
             o = tmp_out;
         }
-        pint::dst_run(c, c->dst_raw, kind, ncols, d, o, nullptr, 1.0);
+        pint::dst_run(c, c->dst_raw, kind, ncols, d, o, base, alpha);
         if (tmp_out)
             PINT_CUDA_CHECK(cudaMemcpyAsync(out, tmp_out, cnt * sizeof(double),
                                             cudaMemcpyDeviceToHost, c->stream));
-        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        dfree(tmp_in);
-        dfree(tmp_out);
+        // device in / out: stream-ordered, no host wait
+        if (tmp_in || tmp_out) {
+            PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+            dfree(tmp_in);
+            dfree(tmp_out);
+        }
     });
+}
+
+int pint_dst_raw(pint_ctx* c, int kind, int N, long long ncols, const double* in, double* out) {
+    return dst_raw_impl(c, kind, N, ncols, in, out, nullptr, 1.0);
+}
+
+// out = base + alpha * T(in) on an (N, ncols) column slab (base may alias out)
+int pint_dst_raw_axpy(pint_ctx* c, int kind, int N, long long ncols, const double* in,
+                      double* out, const double* base, double alpha) {
+    return dst_raw_impl(c, kind, N, ncols, in, out, base, alpha);
 }
 
 // ---------------------------------------------------------------------------
 // time-partitioned building blocks (driven by paper_1802_08126_b200/distributed.py)
 // ---------------------------------------------------------------------------
+static void drain_if_profiling(pint_ctx* c);
+
 static void require_device(const void* p, const char* what) {
     if (p == nullptr || !is_device_ptr(p))
         pint_throw(PINT_INPUT, std::string(what) + " must be a device pointer");
@@ -814,8 +832,7 @@ int pint_residual_r1(pint_ctx* c, const double* u, const double* p, const double
         require_device(f, "f");
         require_device(r1, "r1");
         pint::launch_timeop(c, pint::OP_R1, u, p, f, r1);
-        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        pint_prof_drain(c);
+        drain_if_profiling(c);
     });
 }
 
@@ -827,17 +844,32 @@ int pint_residual_z(pint_ctx* c, const double* u, const double* p, const double*
         require_device(f, "f");
         require_device(z, "z");
         pint::launch_timeop(c, pint::OP_Z, u, p, f, z);
-        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        pint_prof_drain(c);
+        drain_if_profiling(c);
     });
 }
 
-static double read_acc(pint_ctx* c, int slot) {
+// stream-ordered: without profiling nothing here waits for the device
+static void drain_if_profiling(pint_ctx* c) {
+    if (!c->profile) return;
+    PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    pint_prof_drain(c);
+}
+
+// deliver d_acc[slot]: to a device pointer as a stream-ordered copy (no host
+// wait: the caller all-reduces it on the same stream), to a host pointer
+// after a stream sync, nowhere for NULL
+static void deliver_acc(pint_ctx* c, int slot, double* dst) {
+    drain_if_profiling(c);
+    if (!dst) return;
+    if (is_device_ptr(dst)) {
+        PINT_CUDA_CHECK(cudaMemcpyAsync(dst, c->d_acc + slot, sizeof(double),
+                                        cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
     PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_acc, c->d_acc + slot, sizeof(double),
                                     cudaMemcpyDeviceToHost, c->stream));
     PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-    pint_prof_drain(c);
-    return c->h_acc[0];
+    *dst = c->h_acc[0];
 }
 
 int pint_atilde_update(pint_ctx* c, const double* r1, double* p, double* dot) {
@@ -848,8 +880,7 @@ int pint_atilde_update(pint_ctx* c, const double* r1, double* p, double* dot) {
         if (p) require_device(p, "p");
         pint::vcycle(c, PINT_MG_ATILDE, c->N, r1, p, p ? EPI_UZAWA_P : EPI_DOT_TAU, 1.0, p,
                      nullptr, 0);
-        const double v = read_acc(c, 0);
-        if (dot) *dot = v;
+        deliver_acc(c, 0, dot);
     });
 }
 
@@ -871,8 +902,7 @@ int pint_htilde_modes(pint_ctx* c, const double* zh, double* w, double* dot) {
             pint::vcycle(c, PINT_MG_HTILDE, c->N, c->d_z, w, w ? EPI_SCALE_DOT : EPI_SCALE_DOTONLY,
                          s, nullptr, zh, 1);
         }
-        const double v = read_acc(c, 1);
-        if (dot) *dot = v;
+        deliver_acc(c, 1, dot);
     });
 }
 
@@ -881,7 +911,6 @@ int pint_axpy(pint_ctx* c, double* u, const double* y, double omega, long long c
         require_device(u, "u");
         require_device(y, "y");
         pint::launch_axpy(c, u, y, omega, count);
-        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
 

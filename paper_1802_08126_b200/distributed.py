@@ -1,24 +1,37 @@
-"""Time-partitioned Uzawa iteration over several ranks.
+"""Time-partitioned Uzawa iteration over several GPUs.
 
-The time axis is split into contiguous blocks of steps, one per rank.  The
-arithmetic stays in the rank-local building blocks (``GpuLocalOps`` calls the
-C ABI of libpint; the CPU tests plug in numpy ops); this module moves data:
+One process per GPU (torchrun); the time axis is split into contiguous blocks
+of steps, one per rank, as the north_star prescribes.  The arithmetic stays in
+the rank-local building blocks (``GpuLocalOps``: the partition-aware C ABI of
+libpint; the CPU tests plug in numpy ops); this module moves data:
 
 * ghost planes: u's boundary planes to both neighbours, p's first plane to the
   left neighbour (K u, K^T u, K^T p couple adjacent steps, operators.py:78-90);
-* H~^{-1} (schur.py:62-76) needs the whole time column: the z slab is
-  transposed time-sharded -> column-sharded, sine-transformed along the full
-  time axis, transposed to mode-sharded planes for the per-mode V-cycles, and
-  back the same way; the transposes are grouped point-to-point exchanges
-  (NCCL groups them into one all-to-all; gloo has no all-to-all);
-* the two residual partial sums are one all-reduce per iteration.
+* H~^{-1} (schur.py:62-76) needs whole time columns: z is transposed
+  time-sharded -> column-sharded, sine-transformed along the full time axis,
+  and transposed back mode-sharded for the per-mode V-cycles; w goes the same
+  way back and lands as the u update.  The transposes are split into column
+  chunks and pipelined: with NCCL every chunk is an asynchronous
+  all_to_all_single on NCCL's stream, so chunk j+1 moves over NVLink while the
+  transform of chunk j runs (gloo, used by the CPU tests, exchanges
+  point-to-point and synchronously);
+* the two residual partial sums stay on the device and are one all-reduce per
+  iteration; the host reads the residual once per iteration (the reference's
+  stopping and divergence rules, solvers.py:234-263).
 
-The residual, stopping rule and divergence guard are the reference's
-(solvers.py:212-263), evaluated identically on every rank.
+Every libpint call is stream-ordered on torch's current stream
+(pint_set_stream), so the kernels, the NCCL exchanges and the packing copies
+are ordered without host synchronisation.  With one rank there is nothing to
+transpose and the u update is fused into the final transform
+(pint_dst_raw_axpy).
 """
 
 from __future__ import annotations
 
+import argparse
+import ctypes
+import os
+import sys
 import time
 from dataclasses import dataclass
 
@@ -49,7 +62,8 @@ class Partition:
 
 
 class Comm:
-    """The few collectives the time-partitioned iteration needs."""
+    """The collectives the time-partitioned iteration needs, on a process
+    group (default: the world)."""
 
     def __init__(self, group=None):
         self.group = group
@@ -58,6 +72,7 @@ class Comm:
         # P2POp takes GLOBAL peer ranks; rank/world above are group-local
         self._global = [q if group is None else dist.get_global_rank(group, q)
                         for q in range(self.world)]
+        self.nccl = dist.get_backend(group) == "nccl"
 
     def peer(self, q: int) -> int:
         return self._global[q]
@@ -75,12 +90,12 @@ class Comm:
         ops = []
         if prev:
             if r + 1 < w:
-                ops.append(dist.P2POp(dist.isend, ext[nl].contiguous(), self.peer(r + 1), self.group))
+                ops.append(dist.P2POp(dist.isend, ext[nl], self.peer(r + 1), self.group))
             if r > 0:
                 ops.append(dist.P2POp(dist.irecv, ext[0], self.peer(r - 1), self.group))
         if nxt:
             if r > 0:
-                ops.append(dist.P2POp(dist.isend, ext[1].contiguous(), self.peer(r - 1), self.group))
+                ops.append(dist.P2POp(dist.isend, ext[1], self.peer(r - 1), self.group))
             if r + 1 < w:
                 ops.append(dist.P2POp(dist.irecv, ext[nl + 1], self.peer(r + 1), self.group))
         self._run(ops)
@@ -96,70 +111,123 @@ class Comm:
             ops.append(dist.P2POp(dist.irecv, recv[q], self.peer(q), self.group))
         self._run(ops)
 
-    def allreduce(self, vals, device) -> list:
-        t = torch.tensor(list(vals), dtype=torch.float64, device=device)
+    def all_to_all(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits):
+        """Asynchronous all-to-all of contiguous split blocks (NCCL); returns
+        the work handle, whose wait() orders the current stream after it."""
+        return dist.all_to_all_single(out, inp, list(out_splits), list(in_splits),
+                                      group=self.group, async_op=True)
+
+    def allreduce_(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, group=self.group)
-        return [float(x) for x in t.cpu()]
 
 
 class Transposer:
-    """Layout changes between time-sharded [N_r][n], column-sharded [N][n_c]
-    and mode-sharded [N_r][n] slabs (modes split like steps)."""
+    """Row-sharded [N_r][n] (steps or modes; modes split like steps) <->
+    column-sharded [N][n_c] around a transform of whole time columns,
+    pipelined over column chunks."""
 
-    def __init__(self, comm: Comm, N: int, n: int, device):
+    def __init__(self, comm, N: int, n: int, chunks: int = 4):
         self.comm = comm
-        self.tp = Partition(N, comm.world)
-        self.cp = Partition(n, comm.world)
-        self.N, self.n, self.device = N, n, device
-        r = comm.rank
-        self.nl = self.tp.count(r)
-        self.nc = self.cp.count(r)
-
-    def rows_to_cols(self, x: torch.Tensor) -> torch.Tensor:
-        """[N_r][n] sharded by rows (steps or modes) -> [N][n_c] sharded by columns."""
-        c, w, r = self.comm, self.comm.world, self.comm.rank
-        send = [x[:, self.cp.slice(q)].contiguous() for q in range(w)]
-        out = torch.empty((self.N, self.nc), dtype=x.dtype, device=x.device)
-        recv = [out[self.tp.slice(q)] for q in range(w)]  # contiguous row blocks
-        c.exchange(send, recv)
-        del r
-        return out
-
-    def cols_to_rows(self, y: torch.Tensor) -> torch.Tensor:
-        """[N][n_c] sharded by columns -> [N_r][n] sharded by rows."""
-        c, w = self.comm, self.comm.world
-        send = [y[self.tp.slice(q)].contiguous() for q in range(w)]
-        recv = [torch.empty((self.nl, self.cp.count(q)), dtype=y.dtype, device=y.device)
-                for q in range(w)]
-        c.exchange(send, recv)
-        out = torch.empty((self.nl, self.n), dtype=y.dtype, device=y.device)
+        w = comm.world
+        self.tp = Partition(N, w)
+        self.cp = Partition(n, w)
+        self.N, self.n = N, n
+        self.nl = self.tp.count(comm.rank)
+        # chunk j of rank q's columns: cols[q][j] (a slice of the global columns)
+        self.chunks = max(1, chunks)
+        self.cols = []
         for q in range(w):
-            out[:, self.cp.slice(q)] = recv[q]
-        return out
+            s = self.cp.slice(q)
+            sub = Partition(s.stop - s.start, self.chunks)
+            self.cols.append([slice(s.start + sub.start(j), s.start + sub.start(j) + sub.count(j))
+                              for j in range(self.chunks)])
+
+    def _width(self, q: int, j: int) -> int:
+        s = self.cols[q][j]
+        return s.stop - s.start
+
+    def apply(self, x: torch.Tensor, transform, out: torch.Tensor, omega=None) -> None:
+        """out[:, :] (row-sharded) = rows of transform(column-sharded x);
+        with omega: out += omega * (...) (the fused u update).
+        transform(cols_in [N][w], cols_out [N][w]) acts along dim 0."""
+        comm, w, me = self.comm, self.comm.world, self.comm.rank
+        nl, N = self.nl, self.N
+        rows = [self.tp.count(q) for q in range(w)]
+        if getattr(comm, "nccl", False):
+            # pack every chunk for every destination (contiguous blocks), then
+            # stream the chunks: a2a in (async) -> transform -> a2a out (async)
+            packs, handles, recvs = [], [], []
+            for j in range(self.chunks):
+                blocks = [x[:, self.cols[q][j]] for q in range(w)]
+                packs.append(torch.cat([b.reshape(-1) for b in blocks]))
+            for j in range(self.chunks):
+                wj = self._width(me, j)
+                recv = torch.empty((N, wj), dtype=x.dtype, device=x.device)
+                handles.append(comm.all_to_all(
+                    recv.view(-1), packs[j], [r * wj for r in rows],
+                    [nl * self._width(q, j) for q in range(w)]))
+                recvs.append(recv)
+            backs, outs = [], []
+            for j in range(self.chunks):
+                handles[j].wait()
+                res = torch.empty_like(recvs[j])
+                transform(recvs[j], res)
+                back = torch.empty(sum(nl * self._width(q, j) for q in range(w)),
+                                   dtype=x.dtype, device=x.device)
+                backs.append((back, comm.all_to_all(
+                    back, res.view(-1), [nl * self._width(q, j) for q in range(w)],
+                    [r * self._width(me, j) for r in rows])))
+            for j in range(self.chunks):
+                back, h = backs[j]
+                h.wait()
+                off = 0
+                for q in range(w):
+                    wq = self._width(q, j)
+                    blk = back[off:off + nl * wq].view(nl, wq)
+                    off += nl * wq
+                    if omega is None:
+                        out[:, self.cols[q][j]] = blk
+                    else:
+                        out[:, self.cols[q][j]].add_(blk, alpha=omega)
+            return
+        # synchronous point-to-point path (gloo / loopback): whole columns
+        mine = self.cp.slice(me)
+        send = [x[:, self.cp.slice(q)].contiguous() for q in range(w)]
+        cols_in = torch.empty((N, mine.stop - mine.start), dtype=x.dtype, device=x.device)
+        comm.exchange(send, [cols_in[self.tp.slice(q)] for q in range(w)])
+        cols_out = torch.empty_like(cols_in)
+        transform(cols_in, cols_out)
+        send = [cols_out[self.tp.slice(q)].contiguous() for q in range(w)]
+        recv = [torch.empty((nl, self.cp.count(q)), dtype=x.dtype, device=x.device)
+                for q in range(w)]
+        comm.exchange(send, recv)
+        for q in range(w):
+            if omega is None:
+                out[:, self.cp.slice(q)] = recv[q]
+            else:
+                out[:, self.cp.slice(q)].add_(recv[q], alpha=omega)
 
 
 class LocalOps:
     """Rank-local arithmetic of one Uzawa iteration (interface).
 
     Slabs are torch tensors; ``u_ext``/``p_ext`` carry one ghost plane before
-    and after the local steps."""
+    and after the local steps.  Partial sums are written into 1-element
+    tensors on the slab's device (``dot``), never returned to the host."""
 
-    def r1(self, u_ext, p_ext, f):  # -> r1 [N_r][n]
+    def r1(self, u_ext, p_ext, f, out):  # out = r1 [N_r][n]
         raise NotImplementedError
 
-    def z(self, u_ext, p_ext, f):  # -> z [N_r][n]
+    def z(self, u_ext, p_ext, f, out):  # out = z [N_r][n]
         raise NotImplementedError
 
-    def atilde_update(self, r1, p_ext):  # p_local += A~^-1 r1 ; -> sum r1.dp  (p_ext None: dot only)
+    def atilde_update(self, r1, p_ext, dot):  # p_local += A~^-1 r1; dot = sum r1.dp (p_ext None: dot only)
         raise NotImplementedError
 
-    def dst_cols(self, kind, x):  # kind 1: S x ; kind 0: S^T x  along dim 0 of [N][n_c]
+    def dst_cols(self, kind, x, out, base=None, alpha=1.0):  # out = [base + alpha*] T x along dim 0
         raise NotImplementedError
 
-    def htilde_modes(self, zh, want_w=True):  # -> (w or None, sum zh.w)
-        raise NotImplementedError
-
-    def axpy(self, u_local, y, omega):  # u_local += omega * y
+    def htilde_modes(self, zh, w, dot):  # w = modes of H~^-1 (None: dot only); dot = sum zh.w
         raise NotImplementedError
 
 
@@ -170,52 +238,79 @@ class DistUzawa:
     ``step()`` is one iteration (solvers.py:224-233) and returns the residual
     numerator sqrt(max(sum r1.dp + sum z.y, 0)), identical on every rank."""
 
-    def __init__(self, ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.Tensor,
-                 initial=None):
+    def __init__(self, ops: LocalOps, comm, N: int, n: int, f_local: torch.Tensor,
+                 initial=None, chunks: int = 4):
         self.ops, self.comm = ops, comm
         self.dev = f_local.device
-        self.tr = tr = Transposer(comm, N, n, self.dev)
+        self.tr = tr = Transposer(comm, N, n, chunks)
         nl = self.nl = tr.nl
         if f_local.shape != (nl, n):
             raise InputError(f"local rhs has shape {tuple(f_local.shape)}, expected {(nl, n)}")
+        self.N, self.n = N, n
         self.f = f_local
-        self.u_ext = torch.zeros((nl + 2, n), dtype=torch.float64, device=self.dev)
-        self.p_ext = torch.zeros((nl + 2, n), dtype=torch.float64, device=self.dev)
+        kw = dict(dtype=torch.float64, device=self.dev)
+        self.u_ext = torch.zeros((nl + 2, n), **kw)
+        self.p_ext = torch.zeros((nl + 2, n), **kw)
         if initial is not None:
             self.p_ext[1:nl + 1].copy_(initial[0])
             self.u_ext[1:nl + 1].copy_(initial[1])
         self.u, self.p = self.u_ext[1:nl + 1], self.p_ext[1:nl + 1]
+        self.r1 = torch.empty((nl, n), **kw)
+        self.z = torch.empty((nl, n), **kw)
+        self.zh = torch.empty((nl, n), **kw)
+        self.w = torch.empty((nl, n), **kw)
+        self.dots = torch.zeros(2, **kw)
+        self.single = comm.world == 1
+
+    def _transform(self, kind):
+        ops = self.ops
+
+        def run(x, out):
+            ops.dst_cols(kind, x, out)
+
+        return run
+
+    def _modes(self, x, out):
+        """out = S x (mode-sharded rows) for the time-sharded slab x."""
+        if self.single:
+            self.ops.dst_cols(1, x, out)
+        else:
+            self.tr.apply(x, self._transform(1), out)
 
     def begin(self) -> float:
-        ops, tr = self.ops, self.tr
-        a = ops.atilde_update(self.f, None)
-        fh = tr.cols_to_rows(ops.dst_cols(1, tr.rows_to_cols(self.f)))
-        h = ops.htilde_modes(fh, want_w=False)[1]
-        tot = self.comm.allreduce([a, h], self.dev)
-        return float(np.sqrt(max(tot[0] + tot[1], 0.0)))
+        self.ops.atilde_update(self.f, None, self.dots[0:1])
+        self._modes(self.f, self.zh)
+        self.ops.htilde_modes(self.zh, None, self.dots[1:2])
+        self.comm.allreduce_(self.dots)
+        a, h = (float(v) for v in self.dots.cpu())
+        return float(np.sqrt(max(a + h, 0.0)))
 
     def step(self, omega: float) -> float:
-        ops, tr, comm, nl = self.ops, self.tr, self.comm, self.nl
+        ops, comm, nl = self.ops, self.comm, self.nl
         comm.halo(self.u_ext, nl, prev=True, nxt=True)
-        r1 = ops.r1(self.u_ext, self.p_ext, self.f)
-        d1 = ops.atilde_update(r1, self.p_ext)
+        ops.r1(self.u_ext, self.p_ext, self.f, self.r1)
+        ops.atilde_update(self.r1, self.p_ext, self.dots[0:1])
         comm.halo(self.p_ext, nl, prev=False, nxt=True)
-        z = ops.z(self.u_ext, self.p_ext, self.f)
-        zh = tr.cols_to_rows(ops.dst_cols(1, tr.rows_to_cols(z)))  # mode-sharded S z
-        w, d2 = ops.htilde_modes(zh, want_w=True)
-        y = tr.cols_to_rows(ops.dst_cols(0, tr.rows_to_cols(w)))  # time-sharded S^T w
-        ops.axpy(self.u, y, omega)
-        s = comm.allreduce([d1, d2], self.dev)
-        return float(np.sqrt(max(s[0] + s[1], 0.0)))
+        ops.z(self.u_ext, self.p_ext, self.f, self.z)
+        self._modes(self.z, self.zh)
+        ops.htilde_modes(self.zh, self.w, self.dots[1:2])
+        # u += omega S^T w   (y = H~^{-1} z never materialised time-sharded)
+        if self.single:
+            ops.dst_cols(0, self.w, self.u, base=self.u, alpha=omega)
+        else:
+            self.tr.apply(self.w, self._transform(0), self.u, omega=omega)
+        comm.allreduce_(self.dots)
+        s = self.dots.cpu()  # the one host read per iteration (stopping rule)
+        return float(np.sqrt(max(float(s[0]) + float(s[1]), 0.0)))
 
 
-def dist_uzawa_solve(ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.Tensor,
-                     cfg: UzawaConfig, initial=None):
+def dist_uzawa_solve(ops: LocalOps, comm, N: int, n: int, f_local: torch.Tensor,
+                     cfg: UzawaConfig, initial=None, chunks: int = 4):
     """uzawa_solve (solvers.py:177-264) on a time-partitioned problem.
     Returns (p_local, u_local, ConvergenceHistory) on every rank."""
     if cfg.diagnostics or cfg.stopping == "s_norm_error":
         raise InputError("diagnostic stopping is not available on the partitioned path")
-    it = DistUzawa(ops, comm, N, n, f_local, initial)
+    it = DistUzawa(ops, comm, N, n, f_local, initial, chunks)
     ref = it.begin()
     hist = ConvergenceHistory()
     if ref == 0.0:
@@ -237,7 +332,9 @@ def dist_uzawa_solve(ops: LocalOps, comm: Comm, N: int, n: int, f_local: torch.T
 
 
 class GpuLocalOps(LocalOps):
-    """libpint building blocks for this rank's steps / modes (CUDA tensors)."""
+    """libpint building blocks for this rank's steps / modes (CUDA tensors);
+    2D and 3D problems with stencil operators (the A(x,t) field mode is not
+    partitioned)."""
 
     def __init__(self, spec, hierarchy, part: Partition, rank: int, device=None,
                  damping: float | None = None):
@@ -246,6 +343,8 @@ class GpuLocalOps(LocalOps):
         from .schur import frequency_weights
 
         hp = HostProblem(spec)
+        if hp.field is not None:
+            raise InputError("per-point stiffness fields are not time-partitioned")
         if damping is None:
             damping = hp.default_damping()
         sl = part.slice(rank)
@@ -282,46 +381,88 @@ class GpuLocalOps(LocalOps):
         ctx.call("pint_mg_set", MG_HTILDE, len(lm), lm.ctypes.data, self.nl,
                  tab_h.ctypes.data, sid_h.ctypes.data)
 
-    @staticmethod
-    def _ptr(t):
-        return t.data_ptr()
-
-    def r1(self, u_ext, p_ext, f):
-        out = torch.empty_like(f)
+    def r1(self, u_ext, p_ext, f, out):
         self.ctx.call("pint_residual_r1", u_ext[1].data_ptr(), p_ext[1].data_ptr(),
                       f.data_ptr(), out.data_ptr())
-        return out
 
-    def z(self, u_ext, p_ext, f):
-        out = torch.empty_like(f)
+    def z(self, u_ext, p_ext, f, out):
         self.ctx.call("pint_residual_z", u_ext[1].data_ptr(), p_ext[1].data_ptr(),
                       f.data_ptr(), out.data_ptr())
-        return out
 
-    def atilde_update(self, r1, p_ext):
-        import ctypes
-
-        d = ctypes.c_double()
+    def atilde_update(self, r1, p_ext, dot):
         self.ctx.call("pint_atilde_update", r1.data_ptr(),
-                      None if p_ext is None else p_ext[1].data_ptr(), ctypes.byref(d))
-        return d.value
+                      None if p_ext is None else p_ext[1].data_ptr(),
+                      ctypes.cast(dot.data_ptr(), ctypes.POINTER(ctypes.c_double)))
 
-    def dst_cols(self, kind, x):
+    def dst_cols(self, kind, x, out, base=None, alpha=1.0):
         x = x.contiguous()
-        out = torch.empty_like(x)
-        self.ctx.call("pint_dst_raw", int(kind), int(x.shape[0]), int(x.shape[1]),
-                      x.data_ptr(), out.data_ptr())
-        return out
+        if base is None:
+            self.ctx.call("pint_dst_raw", int(kind), int(x.shape[0]), int(x.shape[1]),
+                          x.data_ptr(), out.data_ptr())
+        else:
+            self.ctx.call("pint_dst_raw_axpy", int(kind), int(x.shape[0]), int(x.shape[1]),
+                          x.data_ptr(), out.data_ptr(), base.data_ptr(), float(alpha))
 
-    def htilde_modes(self, zh, want_w=True):
-        import ctypes
-
-        d = ctypes.c_double()
-        w = torch.empty_like(zh) if want_w else None
+    def htilde_modes(self, zh, w, dot):
         self.ctx.call("pint_htilde_modes", zh.data_ptr(), None if w is None else w.data_ptr(),
-                      ctypes.byref(d))
-        return w, d.value
+                      ctypes.cast(dot.data_ptr(), ctypes.POINTER(ctypes.c_double)))
 
-    def axpy(self, u_local, y, omega):
-        self.ctx.call("pint_axpy", u_local.data_ptr(), y.contiguous().data_ptr(), float(omega),
-                      int(u_local.numel()))
+
+# ----------------------------------------------------------------------------
+# torchrun worker: python -m torch.distributed.run --nproc-per-node G
+#     -m paper_1802_08126_b200.distributed --space 3d --h 64 --N 512 ...
+# prints "scaling,<s/iter>,<total s>,<fft share>,<spatial share>" on rank 0
+# (cli.py scaling; the shares are not split per phase on this path: 0)
+# ----------------------------------------------------------------------------
+
+def _worker_main(argv=None) -> int:
+    from . import build_mg_hierarchy, build_time_grid, make_heat_problem
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--space", default="2d")
+    ap.add_argument("--h", type=int, default=32)
+    ap.add_argument("--N", type=int, default=256)
+    ap.add_argument("--T", type=float, default=1.0)
+    ap.add_argument("--omega", type=float, default=0.9)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--repeats", type=int, default=5)
+    ap.add_argument("--chunks", type=int, default=4)
+    args = ap.parse_args(argv)
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        comm = Comm()
+        spec = make_heat_problem(args.space, args.h, build_time_grid("uniform", args.N, args.T),
+                                 data="sine")
+        part = Partition(args.N, comm.world)
+        ops = GpuLocalOps(spec, build_mg_hierarchy(args.space, args.h), part, comm.rank,
+                          device=local)
+        f_all = spec.grid.steps[:, None] * spec.load
+        f_all[0] += spec.mass.dot(spec.u_init)      # fold_rhs (operators.py:22-26)
+        f = torch.from_numpy(np.ascontiguousarray(f_all[part.slice(comm.rank)])).to(ops.dev)
+        times = []
+        for _ in range(args.repeats + 1):
+            it = DistUzawa(ops, comm, args.N, spec.dim, f, chunks=args.chunks)
+            it.begin()
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.iters):
+                it.step(args.omega)
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=ops.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times.append(float(t.item()))
+        total = float(np.median(times[1:]))
+        if comm.rank == 0:
+            print(f"scaling,{total / args.iters!r},{total!r},0.0,0.0", flush=True)
+    finally:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(_worker_main())

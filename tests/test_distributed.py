@@ -28,15 +28,15 @@ def _free_port():
     return p
 
 
-def _problem(cells=8, N=12, T=0.5, seed=4):
+def _problem(cells=8, N=12, T=0.5, seed=4, space="2d"):
     import oracle as orc
 
-    n = (cells - 1) ** 2
+    n = (cells - 1) ** (2 if space == "2d" else 3)
     rng = np.random.default_rng(seed)
     load = rng.standard_normal((N, n))
     u0 = rng.standard_normal(n)
     nodes = orc.time_nodes("perturbed", N, T, 0.2, seed)
-    pb = orc.heat_problem("2d", cells, nodes, coeff=lambda t: 1.0 + t, load=load, u_init=u0)
+    pb = orc.heat_problem(space, cells, nodes, coeff=lambda t: 1.0 + t, load=load, u_init=u0)
     return pb
 
 
@@ -54,7 +54,7 @@ class OracleLocalOps:
         self.N = pb.N
         self.prev = self.n0 > 0
         self.next = self.n0 + self.nl < self.N
-        lev = orc.mg_levels("2d", pb.cells)
+        lev = orc.mg_levels(pb.space, pb.cells)
         self.scales = orc.stiffness_scales(pb)
         self.steps = pb.steps
         self.A0 = pb.stiffness[0]
@@ -73,7 +73,7 @@ class OracleLocalOps:
         # scales_n * (A_0 x_n), operators.py:92-99 (proportional case)
         return self.scales[idx][:, None] * self.A0.dot(x.T).T
 
-    def r1(self, u_ext, p_ext, f):
+    def r1(self, u_ext, p_ext, f, out):
         u = u_ext.numpy()
         mu = self._M(u)  # planes -1 .. nl
         loc = mu[1:self.nl + 1]
@@ -84,9 +84,9 @@ class OracleLocalOps:
             ku[1:] = loc[1:] - loc[:-1]
         idx = np.arange(self.n0, self.n0 + self.nl)
         ap = self._A(p_ext.numpy()[1:self.nl + 1], idx)
-        return torch.from_numpy((ku - ap) - f.numpy())
+        out.copy_(torch.from_numpy((ku - ap) - f.numpy()))
 
-    def z(self, u_ext, p_ext, f):
+    def z(self, u_ext, p_ext, f, out):
         u, p = u_ext.numpy(), p_ext.numpy()
         mu, mp = self._M(u), self._M(p)
         nl = self.nl
@@ -105,34 +105,36 @@ class OracleLocalOps:
             ktp[:-1] = loc_p[:-1] - loc_p[1:]
         idx = np.arange(self.n0, self.n0 + nl)
         au = self._A(u[1:nl + 1], idx)
-        return torch.from_numpy((f.numpy() - ktp) - ((ku + ktu) + au))
+        out.copy_(torch.from_numpy((f.numpy() - ktp) - ((ku + ktu) + au)))
 
-    def atilde_update(self, r1, p_ext):
+    def atilde_update(self, r1, p_ext, dot):
         r = r1.numpy()
         dp = np.stack([v.apply(r[k]) / self.steps[self.n0 + k] for k, v in enumerate(self.vA)])
         if p_ext is not None:
             p = p_ext.numpy()
             p[1:self.nl + 1] = p[1:self.nl + 1] + dp
-        return float(np.sum(r * dp))
+        dot.fill_(float(np.sum(r * dp)))
 
-    def dst_cols(self, kind, x):
+    def dst_cols(self, kind, x, out, base=None, alpha=1.0):
         fn = self.orc.dst_inverse_T if kind == 1 else self.orc.dst_inverse
-        return torch.from_numpy(np.ascontiguousarray(fn(x.numpy())))
+        y = fn(x.numpy())
+        if base is not None:
+            y = base.numpy() + alpha * y
+        out.copy_(torch.from_numpy(np.ascontiguousarray(y)))
 
-    def htilde_modes(self, zh, want_w=True):
+    def htilde_modes(self, zh, w, dot):
         z = zh.numpy()
-        w = np.empty_like(z)
+        wv = np.empty_like(z)
         for k, v in enumerate(self.vH):
             y = v.apply(z[k])
             y = self.aref.dot(y)
-            w[k] = self.scale_h * v.apply(y)
-        return (torch.from_numpy(w) if want_w else None), float(np.sum(z * w))
+            wv[k] = self.scale_h * v.apply(y)
+        if w is not None:
+            w.copy_(torch.from_numpy(wv))
+        dot.fill_(float(np.sum(z * wv)))
 
-    def axpy(self, u_local, y, omega):
-        u_local.copy_(u_local + omega * y)
 
-
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, space="2d"):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -142,27 +144,33 @@ def _worker(rank, world, port, out_dir):
         from paper_1802_08126_b200.distributed import Comm, Partition, dist_uzawa_solve
         from paper_1802_08126_b200.solvers import UzawaConfig
 
-        pb = _problem()
+        pb = _problem(**_SHAPES[space])
         part = Partition(pb.N, world)
         ops = OracleLocalOps(pb, part, rank)
         f = torch.from_numpy(np.ascontiguousarray(orc.fold_rhs(pb)[part.slice(rank)]))
         p, u, hist = dist_uzawa_solve(ops, Comm(), pb.N, pb.dim, f,
-                                      UzawaConfig(omega=0.9, tol=1e-10, max_iter=300))
+                                      UzawaConfig(omega=_OMEGA[space], tol=1e-10, max_iter=300))
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), p=p.numpy(), u=u.numpy(),
                  res=np.array(hist.residual), conv=hist.converged)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_time_partitioned_uzawa_matches_single_process(world, tmp_path):
+_SHAPES = {"2d": dict(cells=8, N=12, T=0.5, seed=4, space="2d"),
+           "3d": dict(cells=8, N=10, T=0.5, seed=5, space="3d")}
+# the 3D case's perturbed grid and c(t) make omega = 0.9 diverge (alpha > 1.15)
+_OMEGA = {"2d": 0.9, "3d": 0.5}
+
+
+@pytest.mark.parametrize("world,space", [(2, "2d"), (3, "2d"), (2, "3d"), (3, "3d")])
+def test_time_partitioned_uzawa_matches_single_process(world, space, tmp_path):
     import oracle as orc
     from paper_1802_08126_b200.distributed import Partition
 
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    pb = _problem()
-    lev = orc.mg_levels("2d", pb.cells)
-    ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), 0.9, 1e-10, 300)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), space), nprocs=world, join=True)
+    pb = _problem(**_SHAPES[space])
+    lev = orc.mg_levels(space, pb.cells)
+    ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), _OMEGA[space], 1e-10, 300)
     part = Partition(pb.N, world)
     outs = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
     for o in outs:  # every rank holds the same history
@@ -213,12 +221,14 @@ class LoopbackComm:
             ext[nl + 1].copy_(self.sh["box"][r + 1][0])
         self._sync()
 
-    def allreduce(self, vals, device):
-        self.sh["box"][self.rank] = list(vals)
+    def allreduce_(self, t):
+        self.sh["box"][self.rank] = t.clone()
         self._sync()
-        out = [sum(self.sh["box"][q][i] for q in range(self.world)) for i in range(len(vals))]
+        tot = self.sh["box"][0].clone()
+        for q in range(1, self.world):
+            tot += self.sh["box"][q]
         self._sync()
-        return out
+        t.copy_(tot)
 
 
 @pytest.mark.gpu
