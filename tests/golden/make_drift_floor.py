@@ -20,7 +20,9 @@ iteration's residual against the unperturbed run.  The GPU tests hold the
 device to max(1e-10, the ensemble's running maximum) per iteration.
 
 Fixture: tests/golden/drift_floor.npz, one array per case:
-    <case>_drift  [seeds, iterations]  relative residual drift per seed
+    <case>_drift      [seeds, iterations]  relative residual drift per seed, transforms perturbed
+    <case>_drift_all  the same with every block operator perturbed (--mode all): the bar of
+                      the FMA-contracted "fast" band kernels
 """
 
 from __future__ import annotations
@@ -40,8 +42,8 @@ sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 def _run(args):
     import ulp_floor
 
-    name, seed = args
-    return name, seed, ulp_floor.residuals(name, seed)
+    name, seed, mode = args
+    return name, seed, ulp_floor.residuals(name, seed, mode)
 
 
 def main():
@@ -50,10 +52,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seeds", type=int, default=ulp_floor.SEEDS)
     ap.add_argument("--jobs", type=int, default=6)
-    ap.add_argument("--cases", default=",".join(ulp_floor.CASES))
+    ap.add_argument("--cases", default=None)
+    ap.add_argument("--mode", default="dst", choices=["dst", "all"],
+                    help="dst: perturb the sine transforms (-> <case>_drift); all: perturb "
+                         "every block operator (-> <case>_drift_all, the fast-arithmetic bar)")
     args = ap.parse_args()
-    cases = [c for c in args.cases.split(",") if c]
-    work = [(c, s) for c in cases for s in range(args.seeds + 1)]
+    default = ulp_floor.FAST_CASES if args.mode == "all" else ulp_floor.CASES
+    cases = [c for c in (args.cases.split(",") if args.cases else default) if c]
+    suffix = "_drift_all" if args.mode == "all" else "_drift"
+    work = [(c, s, args.mode) for c in cases for s in range(args.seeds + 1)]
     with ProcessPoolExecutor(args.jobs) as ex:
         runs = list(ex.map(_run, work, chunksize=4))
     path = os.path.join(HERE, "drift_floor.npz")
@@ -68,8 +75,8 @@ def main():
             d = np.full(len(base), np.nan)
             d[:k] = np.abs(r[:k] - base[:k]) / base[:k]
             rows.append(d)
-        out[c + "_drift"] = np.array(rows)
-        m = np.nanmax(out[c + "_drift"], axis=1)
+        out[c + suffix] = np.array(rows)
+        m = np.nanmax(out[c + suffix], axis=1)
         print(f"{c}: {len(base)} iterations; per-seed max drift median {np.median(m):.1e}, "
               f"max {m.max():.1e}; seeds over 1e-10: {int(np.sum(m > 1e-10))}/{len(m)}")
     out["fraction"] = np.array(ulp_floor.FRACTION)

@@ -67,3 +67,24 @@ def test_uzawa_3d_matches_oracle():
     assert np.all(rel <= bar), (rel.max(), bar.max())
     nrm = orc.ExactNorms(opb)
     assert nrm.s_norm(u - ref.u) / nrm.s_norm(ref.u) <= 1e-8
+
+
+def test_c3_full_mesh_short_history():
+    """BASELINE config 3's full spatial mesh (cells = 64, 63^3 = 250,047 nodes
+    per step, the 6-level hierarchy of the benchmarked run) with N = 8 steps:
+    6 Uzawa iterations against the oracle, u0 ~ U[0,1] as in c3."""
+    cells, N = 64, 8
+    rng, opb, spec = _case(cells, N, 0, T=N / 512.0)
+    lev = orc.mg_levels("3d", cells)
+    ref = orc.uzawa(opb, orc.BlockInv(opb, lev), orc.SchurInv(opb, lev), 0.9, 1e-300, 6)
+    system = pg.TimeGlobalSystem(spec)
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy("3d", cells))
+    ht = pg.build_schur_preconditioner(spec, "mg")
+    x = rng.standard_normal((N, spec.dim))
+    np.testing.assert_array_equal(at.apply_inverse(x), orc.BlockInv(opb, lev).apply(x))
+    (p, u), hist = pg.uzawa_solve(system, at, ht, pg.UzawaConfig(tol=1e-300, max_iter=6))
+    rel = np.abs(np.array(hist.residual) - ref.residual) / np.array(ref.residual)
+    print(f"c3 mesh, N=8: max rel residual drift over 6 iterations {rel.max():.3e}")
+    assert rel.max() <= 1e-12, rel
+    assert np.max(np.abs(u - ref.u)) <= 1e-12 * np.max(np.abs(ref.u))
+    assert np.max(np.abs(p - ref.p)) <= 1e-12 * np.max(np.abs(ref.p))

@@ -47,7 +47,7 @@ def test_minres_matches_reference(name):
                           u_init=d["u_init"])
     # bar: 1e-10, or the reference arithmetic's own drift under a 1-ulp
     # perturbation of its transforms (tests/ulp_floor.py)
-    bar = ulp_floor.bar(name, k)
+    bar = ulp_floor.bar(name, k, pg.get_arithmetic())
     print(f"{name}: {hist.iterations} vs {len(ref)} iterations, max rel drift {rel.max():.2e}, "
           f"head {rel[head].max():.2e}, reference 1-ulp floor {bar[head].max():.2e}")
     assert np.all(rel[head] <= bar[head]), (rel[head].max(), bar[head].max())

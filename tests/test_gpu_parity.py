@@ -182,9 +182,12 @@ def drift_bar(case_name, iters):
     reference's; on config 1 most of the perturbed reference runs exceed
     1e-10.  The envelope is the running maximum over seeds and earlier
     iterations, so it is 1e-10 wherever the perturbed reference itself stays
-    inside the north_star bar.
+    inside the north_star bar.  In fast arithmetic (FMA-contracted band
+    kernels: every operator within a few ulps of the reference's, not only the
+    transforms) the ensemble perturbs every block operator the same way
+    (<case>_drift_all).
     """
-    return ulp_floor.bar(case_name, iters)
+    return ulp_floor.bar(case_name, iters, pg.get_arithmetic())
 
 
 def test_uzawa_golden_cases(case):
@@ -416,7 +419,7 @@ def test_cli_solve_problem_file(method, tmp_path):
     head = ref[:k, 1] > 1e-7 * ref[0, 1]
     # bar: 1e-10, or the reference arithmetic's own drift under a 1-ulp
     # perturbation of its transforms (tests/ulp_floor.py)
-    bar = ulp_floor.bar("cli_" + method, k)
+    bar = ulp_floor.bar("cli_" + method, k, pg.get_arithmetic())
     print(f"{method}: {len(ours)} vs {len(ref)} iterations, drift {rel[head].max():.2e}, "
           f"reference 1-ulp floor {bar[head].max():.2e}")
     assert np.all(rel[head] <= bar[head]), (rel[head].max(), bar[head].max())

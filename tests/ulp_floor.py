@@ -49,6 +49,43 @@ def perturbed_transforms(seed: int, fraction: float = FRACTION):
         O.dst_inverse_T, O.dst_inverse = fwd, inv
 
 
+@contextlib.contextmanager
+def perturbed_operators(seed: int, fraction: float = FRACTION):
+    """Every block operator of the iteration (the sine transforms, K, K^T,
+    A and each V-cycle) is evaluated on an input with one ulp flipped in a
+    random half of the entries (backward error) and returns its result
+    perturbed the same way (forward error): a model of an independent,
+    equally backward-stable implementation of ALL operators -- what the
+    FMA-contracted ("fast") band kernels are against the reference's CSR
+    products (a contracted row sum differs by ~1 ulp of its largest term,
+    i.e. by the effect of ~1 ulp on its inputs, not 1 ulp of the result)."""
+    names = ("dst_inverse_T", "dst_inverse", "op_K", "op_Kt", "op_Abd")
+    saved = {k: getattr(O, k) for k in names}
+    vc = O.VCycle.apply
+    rng = np.random.default_rng(seed)
+
+    def pert(x):
+        hit = rng.random(x.shape) < fraction
+        toward = np.where(rng.random(x.shape) < 0.5, np.inf, -np.inf)
+        return np.where(hit, np.nextafter(x, toward), x)
+
+    def pert_in(a):
+        return pert(a) if isinstance(a, np.ndarray) and a.ndim == 2 else a
+
+    def wrap(fn):
+        return lambda *a, **k: pert(fn(*[pert_in(v) for v in a], **k))
+
+    for k in names:
+        setattr(O, k, wrap(saved[k]))
+    O.VCycle.apply = lambda self, b: pert(vc(self, pert_in(b)))
+    try:
+        yield
+    finally:
+        for k in names:
+            setattr(O, k, saved[k])
+        O.VCycle.apply = vc
+
+
 # ---- the cases the GPU tests compare: (oracle problem, solver settings) -----
 
 def _golden_uzawa(name):
@@ -124,11 +161,21 @@ CASES = {
 }
 
 
-def residuals(name: str, seed: int) -> np.ndarray:
-    """Residual history of case `name`; seed 0 unperturbed, else perturbed."""
+# cases that run on the 2D band / stencil kernels, which exist in "fast" (FMA-
+# contracted) arithmetic: their fast-arithmetic bar is the all-operator ensemble
+FAST_CASES = ("c1", "ops2d_c16_N16_coeff", "sine2d_c8_N16", "minres_c16_N16",
+              "minres_sine_c8_N32", "cli_uzawa", "cli_minres")
+
+
+def residuals(name: str, seed: int, mode: str = "dst") -> np.ndarray:
+    """Residual history of case `name`; seed 0 unperturbed, else perturbed
+    (mode "dst": the transforms only; "all": every block operator)."""
     pb, how = CASES[name]()
     lev = orc.mg_levels(pb.space, pb.cells)
-    ctx = perturbed_transforms(seed) if seed > 0 else contextlib.nullcontext()
+    if seed == 0:
+        ctx = contextlib.nullcontext()
+    else:
+        ctx = perturbed_operators(seed) if mode == "all" else perturbed_transforms(seed)
     with ctx:
         if how[0] == "uzawa":
             r = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), *how[1:]).residual
@@ -146,7 +193,11 @@ def envelope(drifts: np.ndarray, iters: int) -> np.ndarray:
     return np.maximum(1e-10, env[:iters])
 
 
-def bar(name: str, iters: int) -> np.ndarray:
-    """Per-iteration bar of case `name` from the committed ensemble."""
+def bar(name: str, iters: int, arith: str = "exact") -> np.ndarray:
+    """Per-iteration bar of case `name` from the committed ensemble: the
+    transform-only ensemble for exact arithmetic (every other operator is
+    bit-identical to the reference there), the all-operator ensemble for
+    fast arithmetic."""
     d = np.load(os.path.join(GOLDEN, "drift_floor.npz"))
-    return envelope(d[name + "_drift"], iters)
+    key = name + ("_drift_all" if arith == "fast" else "_drift")
+    return envelope(d[key], iters)
