@@ -858,455 +858,8 @@ __global__ void __launch_bounds__(ZX * ZY)
     }
 }
 
-// ---------------------------------------------------------------------------
-// Fused 3D V-cycle band kernels.
-//
-// A unit is (plane of the batch, band of rows, chunk of z).  Every z-slice
-// of a band of full-width rows is one contiguous range of the slab, so it
-// moves with one 1D TMA bulk copy (cp.async.bulk, band.cuh) into a ring of
-// shared-memory stages completed on mbarriers; thread 0 keeps three stages
-// in flight ahead of the compute.  Out-of-domain rows / planes are never
-// copied: reads are predicated to exact zeros, which is what the
-// thread-per-point kernels load there.
-//
-// kb3_pre : x0 = d b, r = b - S x0, b_c = P^T r      (spatial.py:153,156-157)
-//           one pass over b instead of residual + restriction (3.1 -> 1.1
-//           slab passes); r lives one fine z-slice at a time in shared memory
-//           and every coarse point accumulates its 27 terms in ascending fine
-//           index as the march crosses fine planes 2Z, 2Z+1, 2Z+2.
-// kb3_post: x = d b + P e, out = epi(x + d (b - S x))  (spatial.py:157-160)
-//           one pass over b (+ the epilogue operand) instead of prolongation +
-//           smoothing (5.1-6.1 -> 2.1-3.1 passes); x is formed for the band
-//           plus one halo row on each side, three z-slices deep, in shared
-//           memory.
-// Arithmetic and summation order are those of kz_residual / kz_restrict /
-// kz_prolong / kz_smooth (bit-identical results, tests/test_gpu_3d.py).
-// ---------------------------------------------------------------------------
-constexpr int B3T = 256;
-constexpr int B3_RING = 4;
-
-struct Band3 {
-    int m, mc;
-    const double* tab;   // this level's table rows [n_sets][28]
-    const double* tabc;  // next level's (DIRECT: the coarsest 1x1 operator)
-    const int* sid;
-    const double* b;     // rhs of this level
-    const double* ec;    // post: coarse correction (DIRECT: coarsest rhs)
-    double* out;         // pre: coarse rhs b_c; post: x / epilogue output
-    int rows, zc;        // unit: fine rows (post) or coarse rows (pre); z chunk
-    int nrb, nzb;        // bands / z chunks per plane
-    int words;           // shared words per b stage
-    int cwords;          // post: shared words per coarse stage
-    int qwords;          // post: shared words per epilogue-operand stage
-    int xwords;          // post: shared words per x slice
-    // post epilogue
-    int epi;
-    double scale;
-    const double* steps;
-    const double* rsteps;
-    const double* pin;
-    const double* aux;
-    double* part;
-};
-
-// element offset of the first wanted element of rows [r0, r1) of plane z of
-// slab plane base `pb` inside a stage filled by load_rows
-__device__ __forceinline__ int band_off(long long pb, int m, int z, int r0) {
-    return (int)((pb + ((long long)z * m + r0) * m) & 1LL);
-}
-
-// Every thread owns up to PPT fixed points of the band (their in-stage
-// offsets and boundary flags are computed once); per z-slice only the three
-// stage bases change, so the inner loops are loads at constant offsets.
-template <uint32_t PAT, int PPT>
-__global__ void __launch_bounds__(B3T) kb3_pre(Band3 P) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t full[B3_RING];
-    __shared__ double cs[28];
-    const int m = P.m, mc = P.mc, tid = threadIdx.x;
-    const int pl = blockIdx.y;
-    const int yb = blockIdx.x % P.nrb, zb = blockIdx.x / P.nrb;
-    const int Y0 = yb * P.rows, YN = min(P.rows, mc - Y0);
-    const int Z0 = zb * P.zc, ZN = min(P.zc, mc - Z0);
-    const long long n = (long long)m * m * m, pb = pl * n;
-    // fine rows of r: 2Y0 .. 2Y0+2YN; of b: one more on each side (clipped)
-    const int row0 = max(0, 2 * Y0 - 1), row1 = min(m, 2 * Y0 + 2 * YN + 2);
-    const int RR = 2 * YN + 1;
-    double* rs = sm + B3_RING * P.words;  // RR x m
-    if (tid < 27) cs[tid] = pat_has(PAT, tid) ? __ldg(P.tab + (size_t)__ldg(P.sid + pl) * 28 + tid) : 0.0;
-    if (tid == 27) cs[27] = __ldg(P.tab + (size_t)__ldg(P.sid + pl) * 28 + 27);
-    const int f0 = 2 * Z0, f1 = 2 * Z0 + 2 * ZN;  // fine planes of r
-    const int zlo = f0 - 1;                        // first staged plane
-    if (tid == 0) {
-        for (int s = 0; s < B3_RING; ++s) mbar_init(&full[s], 1);
-        fence_barrier_init();
-    }
-    // this thread's r points: stage offset (without the 0/1 alignment shift),
-    // rs offset, flags: 1 valid, 2 x-1 in, 4 x+1 in, 8 y-1 in, 16 y+1 in
-    int po[PPT], ro[PPT];
-    uint32_t pf[PPT];
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-        const int p = tid + i * B3T;
-        const int ry = p / m, x = p - (p / m) * m;
-        const int y = 2 * Y0 + ry;
-        po[i] = (y - row0) * m + x;
-        ro[i] = ry * m + x;
-        pf[i] = (p < RR * m ? 1u : 0u) | (x > 0 ? 2u : 0u) | (x + 1 < m ? 4u : 0u) |
-                (y > 0 ? 8u : 0u) | (y + 1 < m ? 16u : 0u);
-    }
-    // restriction: coarse points q = tid + i B3T of the YN x mc band
-    constexpr int RPT = PPT;
-    int qo[RPT];
-    long long qg[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-        const int q = tid + i * B3T;
-        const int cy = q / mc, cx = q - (q / mc) * mc;
-        qo[i] = q < YN * mc ? (2 * cy) * m + 2 * cx : -1;
-        qg[i] = ((long long)Y0 + cy) * mc + cx;
-    }
-    __syncthreads();
-    auto issue = [&](int z) {  // thread 0: stage plane z
-        const int s = (z - zlo) % B3_RING;
-        if (z >= 0 && z < m && z <= f1 + 1) {
-            const Span sp = span_of(pb + ((long long)z * m + row0) * m, pb + ((long long)z * m + row1) * m);
-            mbar_expect_tx(&full[s], sp.bytes);
-            bulk_g2s(sm + (size_t)s * P.words, P.b + sp.g0, sp.bytes, &full[s]);
-        } else {
-            mbar_expect_tx(&full[s], 0);
-        }
-    };
-    if (tid == 0)
-        for (int z = zlo; z < zlo + B3_RING; ++z) issue(z);
-    const double d = cs[27];
-    double racc[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) racc[i] = 0.0;
-    const double w3[3] = {0.5, 1.0, 0.5};
-    const long long ncp = (long long)mc * mc * mc;
-    for (int f = f0; f <= f1; ++f) {
-        const double* base[3];
-        bool zin[3];
-#pragma unroll
-        for (int dz = 0; dz < 3; ++dz) {
-            const int z = f + dz - 1;
-            const int k = z - zlo;
-            mbar_wait(&full[k % B3_RING], (uint32_t)((k / B3_RING) & 1));
-            zin[dz] = z >= 0 && z < m;
-            base[dz] = sm + (size_t)(k % B3_RING) * P.words + (zin[dz] ? band_off(pb, m, z, row0) : 0);
-        }
-#pragma unroll
-        for (int i = 0; i < PPT; ++i) {
-            if (!(pf[i] & 1u)) continue;
-            double sum = 0.0;
-            bool first = true;
-#pragma unroll
-            for (int k = 0; k < 27; ++k) {
-                if (!pat_has(PAT, k)) continue;
-                const int dz = k / 9, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-                const bool in = zin[dz] && (dx < 0 ? (pf[i] & 2u) : dx > 0 ? (pf[i] & 4u) : true) &&
-                                (dy < 0 ? (pf[i] & 8u) : dy > 0 ? (pf[i] & 16u) : true);
-                double val = 0.0;
-                if (in) val = d * base[dz][po[i] + dy * m + dx];
-                const double t = cs[k] * val;
-                sum = first ? t : sum + t;
-                first = false;
-            }
-            rs[ro[i]] = base[1][po[i]] - sum;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            fence_proxy_async();
-            issue(f + 3);  // into the stage of f-1, read by everyone above
-        }
-        // plane f is fine index 2Z + a of coarse Z: a = 0 (start), 1, 2 (finish)
-        const int j = f - f0;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            if (qo[i] < 0) continue;
-            const double* r0p = rs + qo[i];
-            auto terms = [&](int a, double acc, bool fresh) {
-#pragma unroll
-                for (int t9 = 0; t9 < 9; ++t9) {
-                    const double v = r0p[(t9 / 3) * m + t9 % 3];
-                    const double t = ((w3[a] * w3[t9 / 3]) * w3[t9 % 3]) * v;
-                    acc = (fresh && t9 == 0) ? t : acc + t;
-                }
-                return acc;
-            };
-            if (j & 1) {
-                racc[i] = terms(1, racc[i], false);
-            } else {
-                if (j >= 2) {
-                    const double v = terms(2, racc[i], false);
-                    const int Z = Z0 + j / 2 - 1;
-                    P.out[pl * ncp + (long long)Z * mc * mc + qg[i]] = v;
-                }
-                if (j / 2 < ZN) racc[i] = terms(0, 0.0, true);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-template <uint32_t PAT, int PPT>
-__global__ void __launch_bounds__(B3T) kb3_post(Band3 P) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t full[B3_RING];
-    __shared__ double cs[28];
-    __shared__ double red[B3T / 32];
-    const int m = P.m, mc = P.mc, tid = threadIdx.x;
-    const int pl = blockIdx.y;
-    const int yb = blockIdx.x % P.nrb, zb = blockIdx.x / P.nrb;
-    const int Y0 = yb * P.rows, YN = min(P.rows, m - Y0);
-    const int Z0 = zb * P.zc, ZN = min(P.zc, m - Z0);
-    const long long n = (long long)m * m * m, nc = (long long)mc * mc * mc;
-    const long long pb = pl * n, pbc = pl * nc;
-    const int set = __ldg(P.sid + pl);
-    const bool direct = P.tabc != nullptr;
-    if (tid < 27) cs[tid] = pat_has(PAT, tid) ? __ldg(P.tab + (size_t)set * 28 + tid) : 0.0;
-    if (tid == 27) cs[27] = __ldg(P.tab + (size_t)set * 28 + 27);
-    const double ac = direct ? __ldg(P.tabc + (size_t)set * 28 + 13) : 1.0;
-    // rows of x (and b): Y0-1 .. Y0+YN (clipped); coarse rows covering them
-    const int xr0 = max(0, Y0 - 1), xr1 = min(m, Y0 + YN + 1);
-    const int XR = xr1 - xr0;
-    const int cr0 = max(0, (xr0 - 1) >> 1), cr1 = min(mc, (xr1 >> 1) + 1);
-    const bool has_q = P.epi == EPI_UZAWA_P || P.epi == EPI_SCALE_DOT || P.epi == EPI_SCALE_DOTONLY;
-    const double* qsrc = P.epi == EPI_UZAWA_P ? P.pin : P.aux;
-    // shared layout: B3_RING stages of {b rows, q rows}, 3 coarse stages, 3 x slices
-    const int sw = P.words + P.qwords;
-    double* cst = sm + (size_t)B3_RING * sw;
-    double* xs = cst + 3 * P.cwords;
-    const int glo = Z0 - 1;  // first staged fine plane
-    if (tid == 0) {
-        for (int s = 0; s < B3_RING; ++s) mbar_init(&full[s], 1);
-        fence_barrier_init();
-    }
-    // x points of this thread: x-slice / b-stage offset, coarse (y, x) offsets
-    // and weights of the prolongation, flags 1 valid, 2 second y term, 4 second x term,
-    // 8 first y term present
-    int xo[PPT], cyo0[PPT], cyo1[PPT], cxo0[PPT], cxo1[PPT];
-    double wyx[PPT];
-    uint32_t xf[PPT];
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-        const int p = tid + i * B3T;
-        const int ry = p / m, x = p - (p / m) * m;
-        const int y = xr0 + ry;
-        xo[i] = ry * m + x;
-        int jy0, jy1, jx0, jx1;
-        double wy, wx;
-        bool hy0, hy1, hx0, hx1;
-        if (y & 1) { jy0 = jy1 = (y - 1) >> 1; wy = 1.0; hy0 = true; hy1 = false; }
-        else { jy0 = (y >> 1) - 1; jy1 = y >> 1; wy = 0.5; hy0 = jy0 >= 0; hy1 = jy1 < mc; }
-        if (x & 1) { jx0 = jx1 = (x - 1) >> 1; wx = 1.0; hx0 = true; hx1 = false; }
-        else { jx0 = (x >> 1) - 1; jx1 = x >> 1; wx = 0.5; hx0 = jx0 >= 0; hx1 = jx1 < mc; }
-        // a missing first term is shifted into the first slot (ascending order kept)
-        if (!hy0) { jy0 = jy1; hy0 = hy1; hy1 = false; }
-        if (!hx0) { jx0 = jx1; hx0 = hx1; hx1 = false; }
-        cyo0[i] = (jy0 - cr0) * mc;
-        cyo1[i] = (jy1 - cr0) * mc;
-        cxo0[i] = jx0;
-        cxo1[i] = jx1;
-        wyx[i] = wy;  // (wz * wy) * wx is formed per plane in this order
-        xf[i] = (p < XR * m ? 1u : 0u) | (hy1 ? 2u : 0u) | (hx1 ? 4u : 0u) | (hy0 ? 8u : 0u) |
-                (hx0 ? 32u : 0u) | ((x & 1) ? 0u : 64u);
-    }
-    // output points: x-slice offset of (y, x), q offset, flags 1 valid, 2 x-1, 4 x+1, 8 y-1, 16 y+1
-    int oo[PPT], oq[PPT];
-    long long og[PPT];
-    uint32_t of[PPT];
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-        const int p = tid + i * B3T;
-        const int ry = p / m, x = p - (p / m) * m;
-        const int y = Y0 + ry;
-        oo[i] = (y - xr0) * m + x;
-        oq[i] = ry * m + x;
-        og[i] = (long long)y * m + x;
-        of[i] = (p < YN * m ? 1u : 0u) | (x > 0 ? 2u : 0u) | (x + 1 < m ? 4u : 0u) |
-                (y > 0 ? 8u : 0u) | (y + 1 < m ? 16u : 0u);
-    }
-    __syncthreads();
-    // stage g: b rows xr0..xr1 of plane g, q rows Y0..Y0+YN of plane g, and the
-    // coarse plane first needed by x(g) (k = g/2 for even g; the one below
-    // the first plane at the first stage); all on full[(g - glo) % RING]
-    auto issue = [&](int g) {
-        const int s = (g - glo) % B3_RING;
-        uint32_t tx = 0;
-        const bool gin = g >= 0 && g < m && g <= Z0 + ZN;
-        Span sb{}, sq{}, sc0{}, sc1{};
-        int k0 = -1, k1 = -1;
-        if (gin) {
-            sb = span_of(pb + ((long long)g * m + xr0) * m, pb + ((long long)g * m + xr1) * m);
-            tx += sb.bytes;
-            if (has_q && g >= Z0 && g < Z0 + ZN) {
-                sq = span_of(pb + ((long long)g * m + Y0) * m, pb + ((long long)g * m + Y0 + YN) * m);
-                tx += sq.bytes;
-            }
-            if ((g & 1) == 0 && (g >> 1) < mc) k0 = g >> 1;
-            if (g == glo && ((g + 1) & 1) == 0 && ((g + 1) >> 1) - 1 >= 0) k1 = ((g + 1) >> 1) - 1;
-            if (g == glo && (g & 1) == 0 && (g >> 1) - 1 >= 0) k1 = (g >> 1) - 1;
-            if (k0 >= 0) {
-                sc0 = span_of(pbc + ((long long)k0 * mc + cr0) * mc, pbc + ((long long)k0 * mc + cr1) * mc);
-                tx += sc0.bytes;
-            }
-            if (k1 >= 0) {
-                sc1 = span_of(pbc + ((long long)k1 * mc + cr0) * mc, pbc + ((long long)k1 * mc + cr1) * mc);
-                tx += sc1.bytes;
-            }
-        }
-        mbar_expect_tx(&full[s], tx);
-        if (!gin) return;
-        bulk_g2s(sm + (size_t)s * sw, P.b + sb.g0, sb.bytes, &full[s]);
-        if (sq.bytes) bulk_g2s(sm + (size_t)s * sw + P.words, qsrc + sq.g0, sq.bytes, &full[s]);
-        if (k0 >= 0) bulk_g2s(cst + (size_t)(k0 % 3) * P.cwords, P.ec + sc0.g0, sc0.bytes, &full[s]);
-        if (k1 >= 0) bulk_g2s(cst + (size_t)(k1 % 3) * P.cwords, P.ec + sc1.g0, sc1.bytes, &full[s]);
-    };
-    auto wait_stage = [&](int g) {
-        const int k = g - glo;
-        mbar_wait(&full[k % B3_RING], (uint32_t)((k / B3_RING) & 1));
-    };
-    auto bstage = [&](int g) { return sm + (size_t)((g - glo) % B3_RING) * sw; };
-    auto cplane = [&](int k) {
-        return cst + (size_t)(k % 3) * P.cwords + (int)((pbc + ((long long)k * mc + cr0) * mc) & 1LL);
-    };
-    if (tid == 0)
-        for (int g = glo; g < glo + B3_RING; ++g) issue(g);
-    const double d = cs[27];
-    // x(g) = d b + P e on rows xr0..xr1 of plane g into x slice g % 3
-    auto form_x = [&](int g) {
-        if (g < 0 || g >= m) return;
-        double* xsl = xs + (size_t)(g % 3) * P.xwords;
-        const double* bs = bstage(g) + band_off(pb, m, g, xr0);
-        // z terms: odd g -> coarse (g-1)/2 weight 1; even -> g/2-1, g/2 weight 1/2
-        int kz0, kz1;
-        double wz;
-        bool hz0, hz1;
-        if (g & 1) { kz0 = kz1 = (g - 1) >> 1; wz = 1.0; hz0 = true; hz1 = false; }
-        else { kz0 = (g >> 1) - 1; kz1 = g >> 1; wz = 0.5; hz0 = kz0 >= 0; hz1 = kz1 < mc; }
-        if (!hz0) { kz0 = kz1; hz0 = hz1; hz1 = false; }
-        const double* c0 = hz0 ? cplane(kz0) : cst;
-        const double* c1 = hz1 ? cplane(kz1) : cst;
-#pragma unroll
-        for (int i = 0; i < PPT; ++i) {
-            if (!(xf[i] & 1u)) continue;
-            const double wzy = wz * wyx[i];
-            const double wxv = (xf[i] & 64u) ? 0.5 : 1.0;
-            const double w = wzy * wxv;
-            const bool y2 = xf[i] & 2u, x2 = xf[i] & 4u;
-            double pe = 0.0;
-            bool first = true;
-#pragma unroll
-            for (int a = 0; a < 2; ++a) {
-                if (a == 1 && !hz1) break;
-                if (a == 0 && !hz0) continue;
-                const double* cp = a ? c1 : c0;
-#pragma unroll
-                for (int bb = 0; bb < 2; ++bb) {
-                    if (bb == 1 && !y2) break;
-                    if (bb == 0 && !(xf[i] & 8u)) continue;
-                    const double* crow = cp + (bb ? cyo1[i] : cyo0[i]);
-#pragma unroll
-                    for (int cc = 0; cc < 2; ++cc) {
-                        if (cc == 1 && !x2) break;
-                        if (cc == 0 && !(xf[i] & 32u)) continue;
-                        double e = crow[cc ? cxo1[i] : cxo0[i]];
-                        if (direct) e = e / ac;
-                        const double t = w * e;
-                        pe = first ? t : pe + t;
-                        first = false;
-                    }
-                }
-            }
-            xsl[xo[i]] = d * bs[xo[i]] + pe;
-        }
-    };
-    wait_stage(glo);
-    wait_stage(glo + 1);
-    form_x(glo);
-    form_x(glo + 1);
-    double acc = 0.0;
-    const double rtau = __ldg(P.rsteps + pl), tau = __ldg(P.steps + pl);
-    auto divtau = [&](double v) { return rtau > 0.0 ? v * rtau : div_rn(v, tau); };
-    for (int z = Z0; z < Z0 + ZN; ++z) {
-        wait_stage(z + 1);
-        form_x(z + 1);
-        __syncthreads();
-        // out(z) from x slices z-1, z, z+1
-        const double* xsl[3];
-        bool zin[3];
-#pragma unroll
-        for (int dz = 0; dz < 3; ++dz) {
-            const int g = z + dz - 1;
-            zin[dz] = g >= 0 && g < m;
-            xsl[dz] = xs + (size_t)(zin[dz] ? g % 3 : 0) * P.xwords;
-        }
-        const double* bs = bstage(z) + band_off(pb, m, z, xr0);
-        const double* qs = bstage(z) + P.words + (has_q ? band_off(pb, m, z, Y0) : 0);
-        const long long zoff = pb + (long long)z * m * m;
-#pragma unroll
-        for (int i = 0; i < PPT; ++i) {
-            if (!(of[i] & 1u)) continue;
-            double sum = 0.0;
-            bool first = true;
-#pragma unroll
-            for (int k = 0; k < 27; ++k) {
-                if (!pat_has(PAT, k)) continue;
-                const int dz = k / 9, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-                const bool in = zin[dz] && (dx < 0 ? (of[i] & 2u) : dx > 0 ? (of[i] & 4u) : true) &&
-                                (dy < 0 ? (of[i] & 8u) : dy > 0 ? (of[i] & 16u) : true);
-                double val = 0.0;
-                if (in) val = xsl[dz][oo[i] + dy * m + dx];
-                const double t = cs[k] * val;
-                sum = first ? t : sum + t;
-                first = false;
-            }
-            const double xv = xsl[1][oo[i]];
-            const double bv = bs[oo[i]];
-            const double xn = xv + d * (bv - sum);
-            const long long gi = zoff + og[i];
-            const double qv = has_q ? qs[oq[i]] : 0.0;
-            switch (P.epi) {
-                case EPI_PLAIN: P.out[gi] = xn; break;
-                case EPI_DIV_TAU: P.out[gi] = divtau(xn); break;
-                case EPI_UZAWA_P: {
-                    const double dp = divtau(xn);
-                    P.out[gi] = qv + dp;
-                    acc = acc + bv * dp;
-                    break;
-                }
-                case EPI_DOT_TAU: acc = acc + bv * divtau(xn); break;
-                case EPI_SCALE: P.out[gi] = P.scale * xn; break;
-                case EPI_SCALE_DOT: {
-                    const double w = P.scale * xn;
-                    P.out[gi] = w;
-                    acc = acc + qv * w;
-                    break;
-                }
-                case EPI_SCALE_DOTONLY: acc = acc + qv * (P.scale * xn); break;
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
-            fence_proxy_async();
-            issue(z + 3);  // into the stage of z-1 (its b / q rows are consumed)
-        }
-    }
-    if (P.part) {
-        double v = acc;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((tid & 31) == 0) red[tid >> 5] = v;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < B3T / 32; ++w) t += red[w];
-            P.part[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
-        }
-    }
-}
+constexpr size_t smem_cap3 = 220 * 1024;
+#include "mg3_band_kernels.inc"
 
 // run f(std::integral_constant<uint32_t, PAT>) for the smallest compiled pattern covering mask
 template <typename F>
@@ -1420,50 +973,72 @@ void launch_fold3(pint_ctx* c, const double* load, const double* u0, double* f) 
     PINT_CUDA_CHECK(cudaGetLastError());
 }
 
-// fused band V-cycle (kb3_pre / kb3_post): 2 launches per level
+// fused band V-cycle (kc3_pre / kc3_post): 2 launches per level
+static int band3_lp(int m) {  // log2(m + 1) for the level sizes the band kernels are built for
+    for (int lp = 2; lp <= 6; ++lp)
+        if (m == (1 << lp) - 1) return lp;
+    return 0;
+}
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && *e ? atoi(e) : dflt;
+}
+
+template <auto Kern>
+static void launch_c3(dim3 g, size_t smem, cudaStream_t st, const Band3& P) {
+    static bool attr = false;  // one per kernel (Kern is a template value)
+    if (!attr) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem_cap3));
+        attr = true;
+    }
+    Kern<<<g, C3T, smem, st>>>(P);
+}
+
+// levels below 63^3 run the 27-point code whatever their pattern (zeros in the table)
+template <bool PRE>
+static void dispatch_c3(uint32_t shape, int lp, int units_z, int count, bool has_q,
+                        cudaStream_t st, const Band3& P, dim3* grid_out) {
+    auto go = [&](auto PT, auto LPV) {
+        constexpr uint32_t PAT = decltype(PT)::value;
+        constexpr int LP = decltype(LPV)::value;
+        using G = C3Geom<LP>;
+        const dim3 g((unsigned)((PRE ? G::NRB_PRE : G::NRB) * units_z), (unsigned)count);
+        if (grid_out) *grid_out = g;
+        if constexpr (PRE)
+            launch_c3<kc3_pre<PAT, LP>>(g, G::smem_pre(), st, P);
+        else
+            launch_c3<kc3_post<PAT, LP>>(g, G::smem_post(has_q), st, P);
+    };
+    using F27 = std::integral_constant<uint32_t, PAT_F27>;
+    switch (lp) {
+        case 6: zdispatch(shape, [&](auto PT) { go(PT, std::integral_constant<int, 6>{}); }); break;
+        case 5: go(F27{}, std::integral_constant<int, 5>{}); break;
+        case 4: go(F27{}, std::integral_constant<int, 4>{}); break;
+        case 3: go(F27{}, std::integral_constant<int, 3>{}); break;
+        case 2: go(F27{}, std::integral_constant<int, 2>{}); break;
+        default: pint_throw(PINT_INPUT, "3D band kernels: unsupported level size");
+    }
+}
+
 static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, double* out, int epi,
                          double scale, const double* pin, const double* aux, int acc_slot) {
     const int L = s.levels;
     auto tab = [&](int l) { return s.tab + (size_t)l * s.n_sets * 28; };
-    constexpr int PRE_ROWS = 4, PRE_ZC = 8, POST_ROWS = 8, POST_ZC = 16;
+    static const int zc_post = env_int("PINT_3D_POST_ZC", 0), zc_pre = env_int("PINT_3D_PRE_ZC", 0);
     const double* bl = b;
     for (int l = 0; l + 1 < L; ++l) {
+        const int m = s.m[l], mc = s.m[l + 1];
         Band3 P{};
-        P.m = s.m[l];
-        P.mc = s.m[l + 1];
         P.tab = tab(l);
         P.sid = s.sid;
         P.b = bl;
         P.out = c->lev_b[l + 1];
-        P.rows = PRE_ROWS;
-        P.zc = PRE_ZC;
-        P.nrb = (P.mc + PRE_ROWS - 1) / PRE_ROWS;
-        P.nzb = (P.mc + PRE_ZC - 1) / PRE_ZC;
-        P.words = band_words(std::min(P.m, 2 * PRE_ROWS + 3), P.m);
-        const size_t smem = sizeof(double) * ((size_t)B3_RING * P.words +
-                                              (size_t)(2 * PRE_ROWS + 1) * P.m + P.m + 2);
-        if (PRE_ROWS * P.mc > 8 * B3T) pint_throw(PINT_INPUT, "3D grid too large for the band kernels");
-        const dim3 g((unsigned)(P.nrb * P.nzb), (unsigned)count);
+        P.zc = zc_pre > 0 ? std::min(zc_pre, mc) : mc;
         ProfScope prof(c, l == 0 ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
-                       8.0 * count * ((double)P.m * P.m * P.m + (double)P.mc * P.mc * P.mc));
-        const bool small = (2 * PRE_ROWS + 1) * P.m <= 4 * B3T;
-        zdispatch(s.shape3[l], [&](auto PT) {
-            constexpr uint32_t PAT = decltype(PT)::value;
-            auto launch = [&](auto kern) {
-                static bool attr = false;
-                if (!attr) {
-                    PINT_CUDA_CHECK(cudaFuncSetAttribute(kern,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         200 * 1024));
-                    attr = true;
-                }
-                kern<<<g, B3T, smem, c->stream>>>(P);
-            };
-            if (small)
-                launch(kb3_pre<PAT, 4>);
-            else
-                launch(kb3_pre<PAT, 8>);
-        });
+                       8.0 * count * ((double)m * m * m + (double)mc * mc * mc));
+        dispatch_c3<true>(s.shape3[l], band3_lp(m), (mc + P.zc - 1) / P.zc, count, false,
+                          c->stream, P, nullptr);
         PINT_LAUNCHED(c);
         PINT_CUDA_CHECK(cudaGetLastError());
         bl = c->lev_b[l + 1];
@@ -1471,9 +1046,8 @@ static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, doub
     for (int l = L - 2; l >= 0; --l) {
         const bool top = l == 0;
         const bool direct = l + 1 == L - 1;
+        const int m = s.m[l], mc = s.m[l + 1];
         Band3 P{};
-        P.m = s.m[l];
-        P.mc = s.m[l + 1];
         P.tab = tab(l);
         P.tabc = direct ? tab(l + 1) : nullptr;
         P.sid = s.sid;
@@ -1486,49 +1060,25 @@ static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, doub
         P.rsteps = c->d_rsteps;
         P.pin = pin;
         P.aux = aux;
-        P.rows = POST_ROWS;
-        P.zc = POST_ZC;
-        P.nrb = (P.m + POST_ROWS - 1) / POST_ROWS;
-        P.nzb = (P.m + POST_ZC - 1) / POST_ZC;
-        const int xrows = std::min(P.m, POST_ROWS + 2);
+        P.zc = zc_post > 0 ? std::min(zc_post, m) : m;
+        const int nzb = (m + P.zc - 1) / P.zc;
         const bool has_q = P.epi == EPI_UZAWA_P || P.epi == EPI_SCALE_DOT ||
                            P.epi == EPI_SCALE_DOTONLY;
-        P.words = band_words(xrows, P.m);
-        P.qwords = has_q ? band_words(std::min(P.m, POST_ROWS), P.m) : 0;
-        P.cwords = band_words(std::min(P.mc, POST_ROWS / 2 + 3), P.mc);
-        P.xwords = xrows * P.m;
-        const size_t smem = sizeof(double) * ((size_t)B3_RING * (P.words + P.qwords) +
-                                              3 * (size_t)P.cwords + 3 * (size_t)P.xwords +
-                                              P.m + 2);
-        const dim3 g((unsigned)(P.nrb * P.nzb), (unsigned)count);
+        const int lp = band3_lp(m);
+        const int nrb = lp == 6 ? C3Geom<6>::NRB : 1;
         const bool dot = top && epi_dot(epi);
         if (dot) {
-            ensure_partials(c, (size_t)g.x * g.y);
+            ensure_partials(c, (size_t)nrb * nzb * count);
             P.part = c->d_part;
         }
-        const double fine = (double)P.m * P.m * P.m, coarse = (double)P.mc * P.mc * P.mc;
+        const double fine = (double)m * m * m, coarse = (double)mc * mc * mc;
         double words = fine + coarse;
         if (P.epi != EPI_DOT_TAU && P.epi != EPI_SCALE_DOTONLY) words += fine;
         if (has_q) words += fine;
+        dim3 g;
         {
             ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE, 8.0 * count * words);
-            const bool small = (POST_ROWS + 2) * P.m <= 4 * B3T;
-            zdispatch(s.shape3[l], [&](auto PT) {
-                constexpr uint32_t PAT = decltype(PT)::value;
-                auto launch = [&](auto kern) {
-                    static bool attr = false;
-                    if (!attr) {
-                        PINT_CUDA_CHECK(cudaFuncSetAttribute(
-                            kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                        attr = true;
-                    }
-                    kern<<<g, B3T, smem, c->stream>>>(P);
-                };
-                if (small)
-                    launch(kb3_post<PAT, 4>);
-                else
-                    launch(kb3_post<PAT, 8>);
-            });
+            dispatch_c3<false>(s.shape3[l], lp, nzb, count, has_q, c->stream, P, &g);
         }
         PINT_LAUNCHED(c);
         PINT_CUDA_CHECK(cudaGetLastError());
@@ -1550,9 +1100,11 @@ void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, in
         PINT_CUDA_CHECK(cudaMalloc(&c->d_t3b, need * sizeof(double) + 16));
         c->t3_cap = need;
     }
-    // the band kernels hold up to 8 points per thread: m <= 127 (every 3D config)
+    // fused band kernels for the level shapes of the BASELINE meshes (m = 2^k - 1 <= 63)
     static const bool old_path = getenv("PINT_3D_OLD") != nullptr;
-    if (!old_path && s.m[0] <= 127) {
+    bool band_ok = !old_path;
+    for (int l = 0; l + 1 < L; ++l) band_ok = band_ok && band3_lp(s.m[l]) != 0;
+    if (band_ok) {
         vcycle3_band(c, s, count, b, out, epi, scale, pin, aux, acc_slot);
         return;
     }
