@@ -1025,7 +1025,9 @@ static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, doub
                          double scale, const double* pin, const double* aux, int acc_slot) {
     const int L = s.levels;
     auto tab = [&](int l) { return s.tab + (size_t)l * s.n_sets * 28; };
-    static const int zc_post = env_int("PINT_3D_POST_ZC", 0), zc_pre = env_int("PINT_3D_PRE_ZC", 0);
+    // z chunks per unit (A/B on c3, profiles/r2_c3_zc_sweep.txt): 32 fine slices
+    // (post) and 16 coarse slices (pre) halve the last-wave tail of whole columns
+    static const int zc_post = env_int("PINT_3D_POST_ZC", 32), zc_pre = env_int("PINT_3D_PRE_ZC", 16);
     const double* bl = b;
     for (int l = 0; l + 1 < L; ++l) {
         const int m = s.m[l], mc = s.m[l + 1];
