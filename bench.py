@@ -130,11 +130,20 @@ class ClockSampler:
 # CPU oracle arm (reference algorithm restated in numpy/scipy)
 # ----------------------------------------------------------------------------
 
-def cpu_oracle_rate(cells=CELLS, n_slice=64, iters=4, repeats=1):
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_rate(cells=CELLS, n_slice=64, iters=4, repeats=1, threads=1):
     """Marginal per-iteration time of the oracle Uzawa on an N-slice of the
-    c2 grid ((t(k=iters) - t(k=iters/2)) / (iters/2))."""
+    c2 grid ((t(k=iters) - t(k=iters/2)) / (iters/2)), with
+    `threads` workers on the per-step / per-mode loops (parallel.py:19-43)."""
     import oracle as orc
 
+    orc.set_num_threads(threads)
     load = c2_load(cells, n_slice)
     n = (cells - 1) ** 2
     nodes = orc.time_nodes("uniform", n_slice, T_END * n_slice / NSTEPS)
@@ -150,32 +159,50 @@ def cpu_oracle_rate(cells=CELLS, n_slice=64, iters=4, repeats=1):
         dt = (times[-1] - times[half - 1]) / (iters - half)
         best = dt if best is None else min(best, dt)
         del res
+    orc.set_num_threads(1)
     return n_slice * n / best, best
 
 
 def run_reference(args):
+    """The reference algorithm on the host cores (the CPU oracle, pinned
+    bit-for-bit to the pure-Python reference, which cannot travel to the GPU
+    box): each step times the marginal Uzawa iteration on an N = 64 slice of
+    the c2 grid with every host thread the reference's pool can use, and
+    with one thread; `value` is the better of the two."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     steps, warm = max(1, args.steps), max(0, args.warmup)
     iters = 2 * max(1, min(steps, 3))
-    rates = []
+    cores = host_cores()
+    rates = {1: [], cores: []}
     t0 = time.perf_counter()
     for k in range(warm + steps):
-        rate, dt = cpu_oracle_rate(iters=iters)
-        if k >= warm:
-            rates.append((rate, dt))
+        for th in sorted(rates):
+            rate, dt = cpu_oracle_rate(iters=iters, threads=th)
+            if k >= warm:
+                rates[th].append((rate, dt))
     wall = time.perf_counter() - t0
-    val = float(np.median([r for r, _ in rates]))
+    med = {th: (float(np.median([r for r, _ in v])), float(np.median([d for _, d in v])))
+           for th, v in rates.items()}
+    best = max(med, key=lambda th: med[th][0])
+    val, dt = med[best]
     line = {
         "metric": "space-time DoF/s per Uzawa iteration", "value": val,
         "unit": "DoF/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": float(np.median([d for _, d in rates])) * 1e3 * (NSTEPS / 64),
+        "ms_per_step": dt * 1e3 * (NSTEPS / 64),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD, "sample": "N=64 slice of the c2 grid, marginal "
-                   "per-iteration time of the CPU oracle; ms_per_step scaled linearly to N=1024"},
-        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": 1, "kind": "port",
+        "config": {"workload": WORKLOAD, "same_config": False,
+                   "sample": "N=64 slice (1/16 of the time steps) of the c2 grid, marginal "
+                             "per-iteration time of the CPU oracle; ms_per_step is that time "
+                             "EXTRAPOLATED linearly to N=1024 (the full-size reference run "
+                             "took 31 s per iteration, SURVEY 8(d), so the extrapolation "
+                             "favours the CPU)"},
+        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": best, "kind": "port",
+                         "host_cores": cores,
+                         "by_threads": {str(th): {"DoF_per_s": med[th][0], "s_per_iter": med[th][1]}
+                                        for th in med},
                          "sample": f"oracle uzawa, cells=256, N=64 slice, {iters} iterations "
                                    f"per step, marginal; wall {wall:.1f}s"},
         "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -214,13 +241,8 @@ OTHER_CONFIGS = {
 }
 
 
-def measure_config(name, steps=3, warm=2):
-    """Per-iteration device time of one more BASELINE config on this GPU
-    (CUDA events on the library stream, state resident in HBM), with the
-    iteration roofline fraction and the per-kernel shares."""
-    import ctypes
-    import gc
-
+def build_config(name):
+    """(pg, spec, system, at, ht, setup seconds) of OTHER_CONFIGS[name]."""
     import paper_1802_08126_b200 as pg
 
     c = OTHER_CONFIGS[name]
@@ -238,18 +260,64 @@ def measure_config(name, steps=3, warm=2):
         u0 = rng.uniform(0.0, 1.0, n) if name == "c3" else np.zeros(n)
         spec = pg.problem_from_arrays(space, cells, grid, load, u0, alpha=1.0)
     system = pg.TimeGlobalSystem(spec)
-    pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy(space, cells))
-    pg.build_schur_preconditioner(spec, "mg")
+    at = pg.BlockDiagSolver(spec, "mg", hierarchy=pg.build_mg_hierarchy(space, cells))
+    ht = pg.build_schur_preconditioner(spec, "mg")
+    return pg, spec, system, at, ht, time.perf_counter() - t0
+
+
+# iteration caps of the convergence runs: the reference default 200 (solvers.py:24)
+# except c4, whose count grows with the mesh (~10^3 at cells=512)
+MAX_ITER = {"c3": 200, "c5": 200, "c4": 4000}
+
+
+def converge_config(name, max_iter=None):
+    """One uzawa_solve of a BASELINE config to tol 1e-8 through the public API
+    (host numpy in / out): iterations, time-to-tol (BASELINE's second metric),
+    clocks during the solve."""
+    import gc
+
+    max_iter = max_iter or MAX_ITER[name]
+    pg, spec, system, at, ht, setup = build_config(name)
+    N, n = spec.N, spec.dim
+    with ClockSampler(0) as clk:
+        t0 = time.perf_counter()
+        (p, u), hist = pg.uzawa_solve(system, at, ht,
+                                      pg.UzawaConfig(omega=0.9, tol=1e-8, max_iter=max_iter))
+        wall = time.perf_counter() - t0
+    out = {"iterations": hist.iterations, "converged": bool(hist.converged),
+           "max_iter": max_iter, "time_to_tol_s": wall, "setup_s": setup,
+           "first_residual": hist.residual[0] if hist.residual else None,
+           "final_residual": hist.residual[-1] if hist.residual else None,
+           "e2e_DoF_per_s": N * n * hist.iterations / wall if wall > 0 else None,
+           "h2d_bytes": int(8 * N * n), "d2h_bytes": int(16 * N * n),
+           "clocks": clk.summary()}
+    del p, u, system, at, ht, spec
+    gc.collect()
+    return out
+
+
+def measure_config(name, steps=3, warm=2, converge=True, budget_s=None):
+    """Per-iteration device time of one more BASELINE config on this GPU
+    (CUDA events on the library stream, state resident in HBM), with the
+    iteration roofline fraction and the per-kernel shares; then the solve to
+    tol 1e-8 through the public API (iterations, time-to-tol, clocks).  A
+    config whose projected solve exceeds `budget_s` is run with the iteration
+    cap that fits the budget and reported as not converged."""
+    import ctypes
+    import gc
+
+    c = OTHER_CONFIGS[name]
+    pg, spec, system, at, ht, setup = build_config(name)
+    N, n = spec.N, spec.dim
     ctx = system._gp.ctx
-    setup = time.perf_counter() - t0
     f = np.ascontiguousarray(system.rhs)
-    del load
     ref = ctypes.c_double()
     ctx.call("pint_uzawa_begin", f.ctypes.data, None, None, ctypes.byref(ref))
     nums = np.zeros(max(steps, warm, 2))
     ms = ctypes.c_double()
     ctx.call("pint_uzawa_run", 0.9, warm, nums.ctypes.data, ctypes.byref(ms))
-    ctx.call("pint_uzawa_run", 0.9, steps, nums.ctypes.data, ctypes.byref(ms))
+    with ClockSampler(0) as clk:
+        ctx.call("pint_uzawa_run", 0.9, steps, nums.ctypes.data, ctypes.byref(ms))
     ms_it = ms.value / steps
     ctx.call("pint_profile", 1)
     ctx.call("pint_uzawa_run", 0.9, 1, nums.ctypes.data, ctypes.byref(ms))
@@ -262,11 +330,38 @@ def measure_config(name, steps=3, warm=2):
     out = {"workload": c["workload"], "n": n, "N": N, "ms_per_iter": ms_it,
            "value": N * n / (ms_it / 1e3), "unit": "DoF/s", "setup_s": setup,
            "iteration_frac": iter_bytes / (ms_it / 1e3) / 1e9 / hbm,
+           "clocks": clk.summary(),
            "dominant_kernel": {"name": dom[0], "share": dom[1][0] / tot,
                                "GBps": dom[1][2] / dom[1][0] / 1e6 if dom[1][0] else None},
            "kernel_shares": {k: round(v[0] / tot, 4) for k, v in
                              sorted(stats.items(), key=lambda kv: -kv[1][0]) if v[1]}}
-    del system, spec, ctx, f
+    del f
+    if converge:
+        max_iter = MAX_ITER[name]
+        if budget_s is not None:
+            max_iter = max(10, min(max_iter, int(budget_s / (ms_it / 1e3))))
+        with ClockSampler(0) as clk2:
+            t0 = time.perf_counter()
+            try:
+                (p, u), hist = pg.uzawa_solve(
+                    system, at, ht, pg.UzawaConfig(omega=0.9, tol=1e-8, max_iter=max_iter))
+                wall = time.perf_counter() - t0
+                out["solve"] = {
+                    "iterations": hist.iterations, "converged": bool(hist.converged),
+                    "max_iter": max_iter, "reference_default_max_iter": 200,
+                    "time_to_tol_s": wall if hist.converged else None, "wall_s": wall,
+                    "first_residual": hist.residual[0] if hist.residual else None,
+                    "final_residual": hist.residual[-1] if hist.residual else None,
+                    "e2e_DoF_per_s": N * n * hist.iterations / wall,
+                    "h2d_bytes": int(8 * N * n), "d2h_bytes": int(16 * N * n)}
+                del p, u
+            except pg.SolverDivergenceError as e:
+                # the reference's own divergence rule (solvers.py:236-237)
+                out["solve"] = {"converged": False, "diverged": True, "omega": 0.9,
+                                "max_iter": max_iter, "error": str(e),
+                                "wall_s": time.perf_counter() - t0}
+        out["solve"]["clocks"] = clk2.summary()
+    del system, spec, ctx, at, ht
     gc.collect()
     return out
 
@@ -494,16 +589,26 @@ def run_gpu(args):
         torch.cuda.empty_cache()
         for name in ("c3", "c5", "c4"):
             try:
-                others[name] = measure_config(name)
+                # c4 needs ~10^3 iterations: its solve gets a wall budget
+                others[name] = measure_config(name, converge=not args.no_converge,
+                                              budget_s=args.c4_budget if name == "c4" else None)
             except Exception as e:  # report, do not lose the headline line
                 others[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
             gc.collect()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, dt = cpu_oracle_rate(iters=4)
-        cpu = {"value": rate, "unit": "DoF/s", "cores": 1, "kind": "port",
-               "sample": "CPU oracle uzawa (numpy/scipy restatement of the reference), "
-                         f"cells=256, N=64 slice, marginal s/iter={dt:.3f}"}
+        cores = host_cores()
+        rate1, dt1 = cpu_oracle_rate(iters=4, threads=1)
+        ratec, dtc = cpu_oracle_rate(iters=4, threads=cores) if cores > 1 else (rate1, dt1)
+        best = cores if ratec > rate1 else 1
+        cpu = {"value": max(rate1, ratec), "unit": "DoF/s", "cores": best, "kind": "port",
+               "host_cores": cores,
+               "by_threads": {"1": {"DoF_per_s": rate1, "s_per_iter": dt1},
+                              str(cores): {"DoF_per_s": ratec, "s_per_iter": dtc}},
+               "sample": "CPU oracle uzawa (numpy/scipy restatement of the reference, its "
+                         "thread pool on the per-step / per-mode loops), cells=256, N=64 "
+                         f"slice, marginal s/iter: {dt1:.3f} (1 thread), {dtc:.3f} "
+                         f"({cores} threads)"}
     if rank == 0:
         line = {
             "metric": "space-time DoF/s per Uzawa iteration", "value": value, "unit": "DoF/s",
@@ -544,6 +649,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-other", action="store_true",
                     help="skip the per-iteration measurements of configs c3, c5 (G=1), c4")
+    ap.add_argument("--no-converge", action="store_true",
+                    help="other configs: per-iteration timing only, no solve to tol")
+    ap.add_argument("--c4-budget", type=float, default=240.0,
+                    help="wall budget (s) of the c4 solve; its iteration cap is "
+                         "min(4000, budget / measured iteration time)")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the time-partitioned driver even on one GPU (validation)")
     args = ap.parse_args()

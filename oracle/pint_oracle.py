@@ -44,6 +44,7 @@ __all__ = [
     "frequency_weights", "SchurInv", "BlockInv",
     "UzawaResult", "uzawa", "sequential_euler", "ExactNorms",
     "MinresResult", "op_saddle", "minres",
+    "set_num_threads", "get_num_threads",
 ]
 
 
@@ -570,6 +571,44 @@ def frequency_weights(N: int) -> np.ndarray:
     return 2.0 * np.sin((2 * k - 1) * np.pi / (4 * N))
 
 
+# ----------------------------------------------------------------------------
+# thread pool of the block loops  (parallel.py:19-43)
+# ----------------------------------------------------------------------------
+
+_POOL = None
+_THREADS = 1
+
+
+def set_num_threads(n: int) -> None:
+    """Process-wide pool for the per-step / per-mode loops of BlockInv and
+    SchurInv (parallel.py:19-29); 1 = serial.  Slots are disjoint, so results
+    do not depend on the thread count (parallel.py:1-6)."""
+    global _POOL, _THREADS
+    if n < 1:
+        raise OracleInputError("thread count must be >= 1")
+    if _POOL is not None:
+        _POOL.shutdown(wait=True)
+        _POOL = None
+    _THREADS = n
+    if n > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(max_workers=n)
+
+
+def get_num_threads() -> int:
+    return _THREADS
+
+
+def _block_map(fn, count: int) -> None:
+    """fn(k) for k < count, on the pool when there is one (parallel.py:36-43)."""
+    if _POOL is None or count < 2:
+        for k in range(count):
+            fn(k)
+    else:
+        list(_POOL.map(fn, range(count)))
+
+
 class SchurInv:
     """H~^{-1} = Phi^{-1} diag(scale * H_k^{-1} A_ref H_k^{-1}) Phi^{-T}
     with one MG V-cycle per H_k^{-1} (schur.py:30-52, 62-76)."""
@@ -592,10 +631,14 @@ class SchurInv:
         rh = dst_inverse_T(r) if self.dense is None else self.dense @ r
         out = np.empty_like(rh)
         s = 2.0 * self.tau_ref / self.N
-        for k, sol in enumerate(self.solvers):
+
+        def mode(k):  # schur.py:69-75
+            sol = self.solvers[k]
             y = sol.apply(rh[k])
             y = self.a_ref.dot(y)
             out[k] = s * sol.apply(y)
+
+        _block_map(mode, len(self.solvers))
         return dst_inverse(out) if self.dense is None else self.dense.T @ out
 
 
@@ -615,8 +658,11 @@ class BlockInv:
 
     def apply(self, b: np.ndarray) -> np.ndarray:
         out = np.empty_like(b)
-        for k, sol in enumerate(self.solvers):
-            out[k] = sol.apply(b[k]) / self.steps[k]
+
+        def step(k):  # solvers.py:145-149
+            out[k] = self.solvers[k].apply(b[k]) / self.steps[k]
+
+        _block_map(step, len(self.solvers))
         return out
 
 

@@ -1067,7 +1067,7 @@ static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, doub
         const bool has_q = P.epi == EPI_UZAWA_P || P.epi == EPI_SCALE_DOT ||
                            P.epi == EPI_SCALE_DOTONLY;
         const int lp = band3_lp(m);
-        const int nrb = lp == 6 ? C3Geom<6>::NRB : 1;
+        const int nrb = lp == 6 ? C3Geom<6>::NRB : lp == 5 ? C3Geom<5>::NRB : 1;
         const bool dot = top && epi_dot(epi);
         if (dot) {
             ensure_partials(c, (size_t)nrb * nzb * count);

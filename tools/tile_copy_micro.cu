@@ -2,6 +2,7 @@
 // access pattern): each CTA moves W adjacent columns x N rows, row segments
 // of W doubles at a stride of n doubles.  Measures achieved GB/s vs W.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 template <int W, int LB>
@@ -89,24 +90,36 @@ void run(const double* a, double* b, int N, int n) {
     printf("W=%3d  %.3f ms  %.0f GB/s\n", W, ms, bytes / ms / 1e6);
 }
 
-int main() {
-    const int N = 1024, n = 65025;
+int main(int argc, char** argv) {
+    // usage: tile_copy_micro [row pitch in doubles ...]; default: the c2 slab (odd pitch)
+    // and the same slab padded to a multiple of 32 doubles
+    const int N = 1024;
+    int pitches[8] = {65025, 65056}, np = 2;
+    if (argc > 1) {
+        np = 0;
+        for (int i = 1; i < argc && np < 8; ++i) pitches[np++] = atoi(argv[i]);
+    }
     double *a, *b;
-    cudaMalloc(&a, sizeof(double) * (size_t)N * (n + 1));
-    cudaMalloc(&b, sizeof(double) * (size_t)N * (n + 1));
-    cudaMemset(a, 0, sizeof(double) * (size_t)N * n);
-    run<4>(a, b, N, n);
-    run<8>(a, b, N, n);
-    run<16>(a, b, N, n);
-    run<32>(a, b, N, n);
-    run<64>(a, b, N, n);
-    run<128>(a, b, N, n);
-    // contiguous reference: one "column tile" = whole rows
-    run<512>(a, b, N, n);
-    run2<8>(a, b, N, 65026);
-    run2<16>(a, b, N, 65026);
-    run2<32>(a, b, N, 65026);
-    run2<64>(a, b, N, 65026);
-    run<1024>(a, b, N, n);
+    cudaMalloc(&a, sizeof(double) * (size_t)N * 66000);
+    cudaMalloc(&b, sizeof(double) * (size_t)N * 66000);
+    cudaMemset(a, 0, sizeof(double) * (size_t)N * 66000);
+    for (int k = 0; k < np; ++k) {
+        const int n = pitches[k];
+        printf("== row pitch %d doubles (%s)\n", n, n % 32 == 0 ? "256-byte aligned rows" : "unaligned rows");
+        run<4>(a, b, N, n);
+        run<8>(a, b, N, n);
+        run<16>(a, b, N, n);
+        run<32>(a, b, N, n);
+        run<64>(a, b, N, n);
+        run<128>(a, b, N, n);
+        run<512>(a, b, N, n);
+        if (n % 2 == 0) {
+            run2<8>(a, b, N, n);
+            run2<16>(a, b, N, n);
+            run2<32>(a, b, N, n);
+            run2<64>(a, b, N, n);
+        }
+        run<1024>(a, b, N, n);
+    }
     return 0;
 }
