@@ -470,6 +470,10 @@ def run_gpu_partitioned(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
+    # NCCL_DEBUG=VERSION makes NCCL print its version on stdout, in front of the
+    # one JSON line this script owes the driver
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     steps, warm = args.steps, max(3, args.warmup)
     head = measure_partitioned("c2", world, rank, local, steps, warm, e2e=True)

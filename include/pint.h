@@ -81,7 +81,7 @@ int pint_get_arith(const pint_ctx* ctx);
  * ProblemSpec (problems.py:153-182) as consumed by TimeGlobalSystem
  * (operators.py:29-99).
  *
- *   dims        2 (3 reserved)
+ *   dims        2 or 3 (3: unit cube, Kuhn-split P1, 27-point tables; ops3d.cu)
  *   m           interior points per side (cells - 1)
  *   N           time steps owned by this context
  *   steps[N]    tau_n (TimeGrid.steps, problems.py:49-51)

@@ -232,8 +232,9 @@ class LoopbackComm:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cells,N,world", [(32, 16, 2), (128, 12, 3)])
-def test_gpu_local_ops_partitioned(cells, N, world):
+@pytest.mark.parametrize("space,cells,N,world", [("2d", 32, 16, 2), ("2d", 128, 12, 3),
+                                                 ("3d", 16, 8, 2), ("3d", 32, 9, 3)])
+def test_gpu_local_ops_partitioned(space, cells, N, world):
     """GpuLocalOps (libpint building blocks with ghost planes, column DSTs,
     per-rank mode sets) driven by dist_uzawa_solve for `world` ranks on one
     GPU (threads + loopback transport): same history as the oracle."""
@@ -243,14 +244,14 @@ def test_gpu_local_ops_partitioned(cells, N, world):
     import paper_1802_08126_b200 as pg
     from paper_1802_08126_b200.distributed import GpuLocalOps, Partition, dist_uzawa_solve
 
-    n = (cells - 1) ** 2
+    n = (cells - 1) ** (3 if space == "3d" else 2)
     rng = np.random.default_rng(cells)
     load = rng.standard_normal((N, n))
     nodes = orc.time_nodes("uniform", N, 0.25)
-    pb = orc.heat_problem("2d", cells, nodes, load=load, u_init=np.zeros(n))
-    spec = pg.problem_from_arrays("2d", cells, pg.TimeGrid(nodes), load, np.zeros(n))
+    pb = orc.heat_problem(space, cells, nodes, load=load, u_init=np.zeros(n))
+    spec = pg.problem_from_arrays(space, cells, pg.TimeGrid(nodes), load, np.zeros(n))
     f_all = orc.fold_rhs(pb)
-    hier = pg.build_mg_hierarchy("2d", cells)
+    hier = pg.build_mg_hierarchy(space, cells)
     part = Partition(N, world)
     shared = {"barrier": threading.Barrier(world), "box": [None] * world}
     results = [None] * world
@@ -272,7 +273,7 @@ def test_gpu_local_ops_partitioned(cells, N, world):
     for t in threads:
         t.join()
     assert not errors, errors
-    lev = orc.mg_levels("2d", cells)
+    lev = orc.mg_levels(space, cells)
     ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), 0.9, 1e-300, 8)
     res = np.array(results[0][2].residual)
     np.testing.assert_allclose(res, ref.residual, rtol=1e-10)
