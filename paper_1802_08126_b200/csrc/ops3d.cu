@@ -540,9 +540,18 @@ __global__ void __launch_bounds__(ZX * ZY)
     const double sc = scale ? __ldg(scale + pl) : 1.0;
     const double* v = in + pl * n;
     double* o = out + pl * n;
-    zmarch<PAT, false>(t, m, v, c, 1.0, [&](int, int li, double s, double) {
-        o[li] = scale ? sc * s : s;
-    });
+    // 7-point operators (A_ref y1): window slices requested one point ahead
+    // (zmarch_pf), 0.59 -> 0.53 ms on c3; the 15-point mass is slower that way
+    // (78 registers: r1 1.51 -> 1.58 ms, z 1.74 -> 1.82 ms)
+    if constexpr (PAT != PAT_A7) {
+        zmarch<PAT, false>(t, m, v, c, 1.0, [&](int, int li, double s, double) {
+            o[li] = scale ? sc * s : s;
+        });
+    } else {
+        zmarch_pf<PAT, false>(
+            t, m, v, c, 1.0, [&](int, bool) { return 0; },
+            [&](int li, double s, double, int) { o[li] = scale ? sc * s : s; });
+    }
 }
 
 // r1 = ((Mu_t - Mu_{t-1}) - s_t A p_t) - f_t   (OP_R1 of k3_timeop, Mu precomputed)
@@ -884,12 +893,41 @@ bool epi_dot(int epi) {
 }  // namespace
 
 // M applied to every plane of [qmin, qmax] of src into dst (same plane indexing)
-static void mass_planes3(pint_ctx* c, const double* src, double* dst, int qmin, int qmax) {
-    const uint32_t pm = pattern_of(c->h_mass.data(), 1);
-    zdispatch(pm, [&](auto P) {
-        kz_apply<decltype(P)::value><<<zgrid(c->m, qmax - qmin + 1), dim3(ZX, ZY), 0, c->stream>>>(
-            c->m, qmin, c->d_mass, 0, nullptr, nullptr, src, dst);
+// dst_t = S src_t for planes t0 .. t0 + count - 1 with one shared stencil: the TMA
+// band kernel on the 63^3 grid, the z-marching kernel elsewhere (and PINT_3D_OLD)
+static void apply_shared3(pint_ctx* c, uint32_t pattern, const double* st, int t0, int count,
+                          const double* src, double* dst) {
+    static const bool old_path = getenv("PINT_3D_OLD") != nullptr;
+    static const int zc = getenv("PINT_3D_APPLY_ZC") ? atoi(getenv("PINT_3D_APPLY_ZC")) : 32;
+    if (c->m == A3_M && !old_path) {
+        Apply3 P{};
+        P.tab = st;
+        P.in = src;
+        P.out = dst;
+        P.t0 = t0;
+        P.zc = std::max(1, std::min(zc, A3_M));
+        const dim3 g((unsigned)(A3_NRB * ((A3_M + P.zc - 1) / P.zc)), (unsigned)count);
+        const size_t smem = sizeof(double) * (size_t)(A3_NS + 1) * A3_SW;
+        zdispatch(pattern, [&](auto PT) {
+            auto kern = kc3_apply<decltype(PT)::value>;
+            static bool attr = false;  // one per pattern instantiation
+            if (!attr) {
+                PINT_CUDA_CHECK(cudaFuncSetAttribute(
+                    kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap3));
+                attr = true;
+            }
+            kern<<<g, C3T, smem, c->stream>>>(P);
+        });
+        return;
+    }
+    zdispatch(pattern, [&](auto P) {
+        kz_apply<decltype(P)::value><<<zgrid(c->m, count), dim3(ZX, ZY), 0, c->stream>>>(
+            c->m, t0, st, 0, nullptr, nullptr, src, dst);
     });
+}
+
+static void mass_planes3(pint_ctx* c, const double* src, double* dst, int qmin, int qmax) {
+    apply_shared3(c, pattern_of(c->h_mass.data(), 1), c->d_mass, qmin, qmax - qmin + 1, src, dst);
     PINT_LAUNCHED(c);
 }
 
@@ -958,10 +996,7 @@ void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const
 void launch_apply3(pint_ctx* c, const double* st, const double* in, double* out, int count) {
     ProfScope prof(c, K_AREF, 16.0 * (double)count * c->n);
     const uint32_t pm = st == c->d_aref ? pattern_of(c->h_aref.data(), 1) : PAT_F27;
-    zdispatch(pm, [&](auto P) {
-        kz_apply<decltype(P)::value><<<zgrid(c->m, count), dim3(ZX, ZY), 0, c->stream>>>(
-            c->m, 0, st, 0, nullptr, nullptr, in, out);
-    });
+    apply_shared3(c, pm, st, 0, count, in, out);
     PINT_LAUNCHED(c);
     PINT_CUDA_CHECK(cudaGetLastError());
 }
