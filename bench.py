@@ -586,6 +586,22 @@ def run_gpu(args):
 
     others = {}
     if rank == 0 and world == 1 and not args.no_other:
+        # second solver entry point on the headline config (solvers.py:267-327)
+        try:
+            t0 = time.perf_counter()
+            _, mh = pg.minres_solve(system, at, ht, tol=1e-8, max_iter=500)
+            mw = time.perf_counter() - t0
+            others["c2_minres"] = {
+                "workload": WORKLOAD + "; minres_solve (block-diagonally preconditioned MINRES)",
+                "iterations": mh.iterations, "converged": bool(mh.converged),
+                "time_to_tol_s": mw,
+                "ms_per_iter": (mh.wall_seconds[-1] / max(1, mh.iterations) * 1e3
+                                if mh.wall_seconds else None),
+                "final_residual": mh.residual[-1] if mh.residual else None,
+                "note": "wall clock from host numpy f to host numpy (p, u); each iteration "
+                        "applies the saddle operator, A~^-1 and H~^-1 once"}
+        except Exception as e:
+            others["c2_minres"] = {"error": f"{type(e).__name__}: {e}"[:300]}
         del system, at, ht, spec, gp, ctx
         import gc
 

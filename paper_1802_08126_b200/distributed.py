@@ -65,14 +65,16 @@ class Comm:
     """The collectives the time-partitioned iteration needs, on a process
     group (default: the world)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, pipelined=None):
+        """pipelined: run the transposes as chunked asynchronous all-to-alls
+        (default: on NCCL; the CPU tests force it on gloo to cover that path)."""
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         # P2POp takes GLOBAL peer ranks; rank/world above are group-local
         self._global = [q if group is None else dist.get_global_rank(group, q)
                         for q in range(self.world)]
-        self.nccl = dist.get_backend(group) == "nccl"
+        self.nccl = (dist.get_backend(group) == "nccl") if pipelined is None else bool(pipelined)
 
     def peer(self, q: int) -> int:
         return self._global[q]

@@ -314,9 +314,13 @@ def minres_solve(system, atilde, htilde, tol: float = 1e-8, max_iter: int = 500)
     tmp, tmp2 = new(), new()
 
     # cheap positivity probe of the preconditioner (solvers.py:297-302)
-    rng = np.random.default_rng(1234)
+    # (three seeded N(0,1) probes as in the reference; drawn on the device --
+    # the host generator costs seconds per probe at config-2 size)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
     for _ in range(3):
-        w = upload(rng.standard_normal(2 * nd))
+        w = torch.randn(2 * nd, dtype=torch.float64, device=dev, generator=gen)
+        torch.cuda.synchronize(dev)
         precond(w, tmp)
         if dot(w, tmp) <= 0.0:
             from .errors import NotSpdError

@@ -134,7 +134,7 @@ class OracleLocalOps:
         dot.fill_(float(np.sum(z * wv)))
 
 
-def _worker(rank, world, port, out_dir, space="2d"):
+def _worker(rank, world, port, out_dir, space="2d", pipelined=False):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -148,7 +148,7 @@ def _worker(rank, world, port, out_dir, space="2d"):
         part = Partition(pb.N, world)
         ops = OracleLocalOps(pb, part, rank)
         f = torch.from_numpy(np.ascontiguousarray(orc.fold_rhs(pb)[part.slice(rank)]))
-        p, u, hist = dist_uzawa_solve(ops, Comm(), pb.N, pb.dim, f,
+        p, u, hist = dist_uzawa_solve(ops, Comm(pipelined=pipelined), pb.N, pb.dim, f,
                                       UzawaConfig(omega=_OMEGA[space], tol=1e-10, max_iter=300))
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), p=p.numpy(), u=u.numpy(),
                  res=np.array(hist.residual), conv=hist.converged)
@@ -162,12 +162,17 @@ _SHAPES = {"2d": dict(cells=8, N=12, T=0.5, seed=4, space="2d"),
 _OMEGA = {"2d": 0.9, "3d": 0.5}
 
 
-@pytest.mark.parametrize("world,space", [(2, "2d"), (3, "2d"), (2, "3d"), (3, "3d")])
-def test_time_partitioned_uzawa_matches_single_process(world, space, tmp_path):
+@pytest.mark.parametrize("world,space,pipelined",
+                         [(2, "2d", False), (3, "2d", False), (2, "3d", False), (3, "3d", False),
+                          # the NCCL code path (chunked asynchronous all-to-all transposes,
+                          # Transposer.apply) forced onto gloo
+                          (2, "2d", True), (3, "2d", True), (3, "3d", True)])
+def test_time_partitioned_uzawa_matches_single_process(world, space, pipelined, tmp_path):
     import oracle as orc
     from paper_1802_08126_b200.distributed import Partition
 
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), space), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), space, pipelined), nprocs=world,
+             join=True)
     pb = _problem(**_SHAPES[space])
     lev = orc.mg_levels(space, pb.cells)
     ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), _OMEGA[space], 1e-10, 300)
