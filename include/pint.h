@@ -123,6 +123,15 @@ int pint_apply_Abd(pint_ctx* ctx, const double* in, double* out);
  * ------------------------------------------------------------------------- */
 int pint_mg_set(pint_ctx* ctx, int which, int levels, const int* level_m,
                 int n_sets, const double* tables, const int* sid);
+/* V-cycle options of a configured set (MgVCycleSolver(cycles=, smooth_steps=),
+ * spatial.py:116-169): `cycles` V-cycles with residual correction
+ * (spatial.py:163-169) and `smooth_steps` damped-Jacobi sweeps before and
+ * after the coarse correction (spatial.py:152-160).  (1, 1), the setting of
+ * every BASELINE config and the default after pint_mg_set, runs the fused
+ * band kernels; anything else runs general thread-per-point kernels
+ * (mg_generic.cu), bit-identical to the reference's products.  Not available
+ * for field mode. */
+int pint_mg_set_options(pint_ctx* ctx, int which, int cycles, int smooth_steps);
 
 /* ---------------------------------------------------------------------------
  * Field mode (EXTENSION, BASELINE config 4): 2D stiffness operators that are

@@ -212,21 +212,25 @@ class GpuProblem(HostProblem):
             f = np.ascontiguousarray(grid_fields(spec.a_ref, self.m))
             ctx.call("pint_field_aref", 0, f.ctypes.data)
 
-    def set_atilde(self, hierarchy: MgHierarchy, damping: float):
+    def set_atilde(self, hierarchy: MgHierarchy, damping: float, cycles: int = 1,
+                   smooth_steps: int = 1):
         if self.field is not None:
             self._set_field(MG_ATILDE, hierarchy, damping, None)
         else:
             tab, sid = self.atilde_tables(hierarchy, damping)
             self._upload_set(MG_ATILDE, hierarchy, tab, sid)
+        self.ctx.call("pint_mg_set_options", MG_ATILDE, int(cycles), int(smooth_steps))
         self.atilde_ready = True
 
-    def set_htilde(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray):
+    def set_htilde(self, hierarchy: MgHierarchy, damping: float, mu: np.ndarray, cycles: int = 1,
+                   smooth_steps: int = 1):
         if self.field is not None:
             self._set_field(MG_HTILDE, hierarchy, damping,
                             np.ascontiguousarray(mu, dtype=np.float64))
         else:
             tab, sid = self.htilde_tables(hierarchy, damping, mu)
             self._upload_set(MG_HTILDE, hierarchy, tab, sid)
+        self.ctx.call("pint_mg_set_options", MG_HTILDE, int(cycles), int(smooth_steps))
         self.htilde_ready = True
 
     def ensure_exact(self):

@@ -67,6 +67,7 @@ _SIGNATURES = {
     "pint_apply_Kt": (_I, [_P, _P, _P]),
     "pint_apply_Abd": (_I, [_P, _P, _P]),
     "pint_mg_set": (_I, [_P, _I, _I, _P, _I, _P, _P]),
+    "pint_mg_set_options": (_I, [_P, _I, _I, _I]),
     "pint_vcycle": (_I, [_P, _I, _I, _P, _P]),
     "pint_atilde_inv": (_I, [_P, _P, _P]),
     "pint_htilde_inv": (_I, [_P, _P, _P]),

@@ -183,6 +183,9 @@ void free_slabs(pint_ctx* c) {
     c->lev_b.clear();
     c->lev_x.clear();
     c->lev_cap.clear();
+    for (double* p : c->gen_scratch) dfree(p);
+    c->gen_scratch.clear();
+    c->gen_cap.clear();
 }
 
 void free_field_set(FieldMg& F) {
@@ -564,6 +567,25 @@ static void enable_field(pint_ctx* c) {
         c->d_fref = dalloc<double>((size_t)3 * c->n);
         c->field = true;
     }
+}
+
+
+int pint_mg_set_options(pint_ctx* c, int which, int cycles, int smooth_steps) {
+    return guarded(c, [&] {
+        require_problem(c);
+        if (which != PINT_MG_ATILDE && which != PINT_MG_HTILDE && which != PINT_MG_EULER)
+            pint_throw(PINT_INPUT, "unknown multigrid set");
+        if (cycles < 1 || smooth_steps < 1)
+            pint_throw(PINT_INPUT, "cycles and smooth_steps must be >= 1");
+        if (c->field && (cycles != 1 || smooth_steps != 1))
+            pint_throw(PINT_INPUT, "cycles / smooth_steps other than 1 are not available for "
+                                   "per-point stiffness fields");
+        MgSet& s = c->mg[which];
+        if (!c->field && !s.ready) pint_throw(PINT_INPUT, "multigrid set not configured");
+        graph_reset(c);  // the captured step holds the launches of the previous setting
+        s.cycles = cycles;
+        s.smooth = smooth_steps;
+    });
 }
 
 int pint_field_set(pint_ctx* c, int step0, int count, const double* fields) {

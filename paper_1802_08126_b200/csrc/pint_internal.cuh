@@ -53,6 +53,7 @@ struct MgSet {
     int* sid = nullptr;       // device [B]
     std::vector<int> shape;   // per level: which stencil positions can be non-zero
     std::vector<uint32_t> shape3;  // 3D: per level, 27-bit union of non-zero positions
+    int cycles = 1, smooth = 1;    // spatial.py:148-169; != 1 runs mg_generic.cu
     bool ready = false;
 };
 
@@ -146,6 +147,8 @@ struct pint_ctx {
 
     // level work buffers (levels >= 1): rhs and solution, N planes each
     std::vector<double*> lev_b, lev_x;
+    std::vector<double*> gen_scratch;  // mg_generic.cu work vectors
+    std::vector<size_t> gen_cap;
     std::vector<size_t> lev_cap;
 
     // slabs [N][n]
@@ -253,6 +256,10 @@ PINT_VARIANT_API
 namespace fast {
 PINT_VARIANT_API
 }
+// general cycles / smooth_steps (mg_generic.cu)
+bool vcycle_is_generic(const pint_ctx* c, int which);
+void vcycle_generic(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
+                    double scale, const double* pin, const double* aux, int acc_slot);
 // 3D (ops3d.cu)
 void launch_timeop3(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                     double* out);

@@ -26,11 +26,17 @@ void launch_band_apply(pint_ctx* c, const double* st_dev, const double* st_host,
 
 void vcycle(pint_ctx* c, int which, int count, const double* b, double* out, int epi,
             double scale, const double* pin, const double* aux, int acc_slot, bool aref_in) {
+    if (vcycle_is_generic(c, which)) {
+        if (aref_in) pint_throw(PINT_INPUT, "fused A_ref input needs the V(1,1) kernels");
+        vcycle_generic(c, which, count, b, out, epi, scale, pin, aux, acc_slot);
+        return;
+    }
     if (c->exact) exact::vcycle(c, which, count, b, out, epi, scale, pin, aux, acc_slot, aref_in);
     else fast::vcycle(c, which, count, b, out, epi, scale, pin, aux, acc_slot, aref_in);
 }
 
 bool vcycle_aref_fusable(const pint_ctx* c, int which) {
+    if (vcycle_is_generic(c, which)) return false;
     return c->exact ? exact::vcycle_aref_fusable(c, which) : fast::vcycle_aref_fusable(c, which);
 }
 

@@ -45,9 +45,10 @@ class SchurPreconditioner:
         self.plan = DstPlan(self.N)
         self.solver_kind = solver_kind
         self.hierarchy = hierarchy
+        self.cycles, self.smooth_steps = int(cycles), int(smooth_steps)
         self._gp = gpu_problem(spec, device)
         self._gp.set_htilde(hierarchy, self._gp.default_damping() if damping is None else damping,
-                            self.mu)
+                            self.mu, self.cycles, self.smooth_steps)
 
     def apply_inverse(self, r):
         """One preconditioner action (schur.py:62-76)."""

@@ -109,8 +109,10 @@ class BlockDiagSolver:
         self.kind = kind
         self.steps = spec.grid.steps
         self.hierarchy = hierarchy
+        self.cycles, self.smooth_steps = int(cycles), int(smooth_steps)
         self._gp = gpu_problem(spec, device)
-        self._gp.set_atilde(hierarchy, self._gp.default_damping() if damping is None else damping)
+        self._gp.set_atilde(hierarchy, self._gp.default_damping() if damping is None else damping,
+                            self.cycles, self.smooth_steps)
 
     def apply_inverse(self, b):
         shape = (self.spec.N, self.spec.dim)

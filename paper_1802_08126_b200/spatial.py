@@ -195,9 +195,12 @@ class SpatialSolver:
 
 
 def _check_mg_options(cycles: int, smooth_steps: int, damping):
-    if cycles != 1 or smooth_steps != 1:
-        raise InputError("the GPU V-cycle implements cycles=1, smooth_steps=1 "
-                         "(the configuration of every BASELINE config)")
+    """cycles / smooth_steps as in spatial.py:116-169.  (1, 1) -- every
+    BASELINE config -- runs the fused band kernels; other values run the
+    general kernels of csrc/mg_generic.cu (pint_mg_set_options)."""
+    for name, v in (("cycles", cycles), ("smooth_steps", smooth_steps)):
+        if int(v) != v or v < 1:
+            raise InputError(f"{name} must be a positive integer")
 
 
 class MgVCycleSolver(SpatialSolver):
@@ -244,6 +247,7 @@ class MgVCycleSolver(SpatialSolver):
         tab = np.ascontiguousarray(self._tables)
         ctx.call("pint_mg_set", MG_ATILDE, len(lm), lm.ctypes.data, 1, tab.ctypes.data,
                  sid.ctypes.data)
+        ctx.call("pint_mg_set_options", MG_ATILDE, int(self.cycles), int(self.smooth_steps))
         self._cap = batch
 
     def apply(self, b):
