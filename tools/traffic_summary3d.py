@@ -19,7 +19,7 @@ def family(name):
         return "timeop_r1"
     if "kz_z" in name:
         return "timeop_z"
-    if "kz_apply" in name:
+    if "kz_apply" in name or "kc3_apply" in name:
         return "mass_or_aref"
     if "k_dst_reg<1" in name or "k_dst_fft<1" in name:
         return "dst_inverse_transpose"
