@@ -1063,8 +1063,14 @@ static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, doub
     // z chunks per unit (A/B on c3, profiles/r2_c3_zc_sweep.txt): 32 fine slices
     // (post) and 16 coarse slices (pre) halve the last-wave tail of whole columns
     static const int zc_post = env_int("PINT_3D_POST_ZC", 32), zc_pre = env_int("PINT_3D_PRE_ZC", 16);
+    // levels lt .. L-1 (m <= 15, below the finest) run in the shared-memory tail
+    static const bool no_tail = getenv("PINT_3D_NO_TAIL") != nullptr;
+    int lt = 1;
+    while (lt < L && s.m[lt] > T3_MAXM) ++lt;
+    const bool tail = !no_tail && lt <= L - 2 && L - lt <= T3_MAXLEV;
+    const int ldown = tail ? lt : L - 1;  // band kernels serve levels 0 .. ldown - 1
     const double* bl = b;
-    for (int l = 0; l + 1 < L; ++l) {
+    for (int l = 0; l < ldown; ++l) {
         const int m = s.m[l], mc = s.m[l + 1];
         Band3 P{};
         P.tab = tab(l);
@@ -1080,7 +1086,32 @@ static void vcycle3_band(pint_ctx* c, MgSet& s, int count, const double* b, doub
         PINT_CUDA_CHECK(cudaGetLastError());
         bl = c->lev_b[l + 1];
     }
-    for (int l = L - 2; l >= 0; --l) {
+    if (tail) {
+        Tail3 T{};
+        T.nlev = L - lt;
+        size_t words = 0;
+        for (int j = 0; j < T.nlev; ++j) {
+            T.m[j] = s.m[lt + j];
+            T.tab[j] = tab(lt + j);
+            const size_t n3 = (size_t)T.m[j] * T.m[j] * T.m[j];
+            words += 2 * ((n3 + 1) & ~(size_t)1);
+        }
+        words += (size_t)T.m[0] * T.m[0] * T.m[0] + 2;
+        T.sid = s.sid;
+        T.b = c->lev_b[lt];
+        T.x = c->lev_x[lt];
+        static bool attr = false;
+        if (!attr) {
+            PINT_CUDA_CHECK(cudaFuncSetAttribute(kc3_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem_cap3));
+            attr = true;
+        }
+        ProfScope prof(c, K_MG_TAIL, 16.0 * count * (double)T.m[0] * T.m[0] * T.m[0]);
+        kc3_tail<<<count, C3T, words * sizeof(double), c->stream>>>(T);
+        PINT_LAUNCHED(c);
+        PINT_CUDA_CHECK(cudaGetLastError());
+    }
+    for (int l = ldown - 1; l >= 0; --l) {
         const bool top = l == 0;
         const bool direct = l + 1 == L - 1;
         const int m = s.m[l], mc = s.m[l + 1];
