@@ -23,6 +23,7 @@
 // so results are bit-identical to scipy's csr_matvec on the same matrices.
 // Round-1 form: one thread per point, neighbours through L1/L2.
 #include <algorithm>
+#include <cstdlib>
 
 #include "pint_device.cuh"
 #include "pint_internal.cuh"
@@ -231,6 +232,41 @@ __global__ void __launch_bounds__(FT)
             const int fy = 2 * Y + a, fx = 2 * X + q;
             const double r = __ldg(bp + (size_t)fy * m + fx) - frow<MODE>(A, t, xp, m, fx, fy);
             const double term = (wt[a] * wt[q]) * r;
+            v = (a == 0 && q == 0) ? term : v + term;
+        }
+    bc[t * nc + g] = v;
+}
+
+// r = b - A x0, one thread per FINE point (k_f_rr evaluates every fine
+// residual once per coarse point it feeds: 2.25 times on average)
+template <int MODE>
+__global__ void __launch_bounds__(FT)
+    k_f_resid(int m, Src A, const double* __restrict__ b, const double* __restrict__ x0,
+              double* __restrict__ r) {
+    const size_t n = (size_t)m * m;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)n) return;
+    const int t = blockIdx.y;
+    const int y = (int)(g / m), x = (int)(g - (long long)y * m);
+    r[t * n + g] = __ldg(b + t * n + g) - frow<MODE>(A, t, x0 + (size_t)t * n, m, x, y);
+}
+
+// b_c = P^T r from stored residuals: same nine terms, order and weights as k_f_rr
+__global__ void __launch_bounds__(FT)
+    k_f_restrict(int m, int mc, const double* __restrict__ r, double* __restrict__ bc) {
+    const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
+    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
+    if (g >= (long long)nc) return;
+    const int t = blockIdx.y;
+    const int Y = (int)(g / mc), X = (int)(g - (long long)Y * mc);
+    const double* rp = r + (size_t)t * n;
+    const double wt[3] = {0.5, 1.0, 0.5};
+    double v = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double term = (wt[a] * wt[q]) * __ldg(rp + (size_t)(2 * Y + a) * m + (2 * X + q));
             v = (a == 0 && q == 0) ? term : v + term;
         }
     bc[t * nc + g] = v;
@@ -503,12 +539,19 @@ namespace {
 
 template <int MODE>
 void pre_level(pint_ctx* c, const Src& S, int m, int mc, int count, double damping,
-               const double* b, double* x0, double* bc, bool fine) {
+               const double* b, double* x0, double* bc, bool fine, double* rwork) {
     ProfScope prof(c, fine ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
                    8.0 * count * (3.0 * m * m + (double)mc * mc));
     k_f_x0<MODE><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(m, S, damping, b, x0);
-    k_f_rr<MODE><<<pt_grid((size_t)mc * mc, count), FT, 0, c->stream>>>(m, mc, S, b, x0, bc);
-    c->launches += 2;
+    static const bool fused_rr = getenv("PINT_FIELD_RR") != nullptr;  // round-1 form (A/B)
+    if (fused_rr || !rwork) {
+        k_f_rr<MODE><<<pt_grid((size_t)mc * mc, count), FT, 0, c->stream>>>(m, mc, S, b, x0, bc);
+        c->launches += 2;
+        return;
+    }
+    k_f_resid<MODE><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(m, S, b, x0, rwork);
+    k_f_restrict<<<pt_grid((size_t)mc * mc, count), FT, 0, c->stream>>>(m, mc, rwork, bc);
+    c->launches += 3;
 }
 
 template <int MODE>
@@ -560,17 +603,31 @@ void vcycle_field(pint_ctx* c, int which, int count, const double* b, double* ou
     const Src S0 = fine_src(c, which);
     // descend: x0 = dinv b kept per level (the prolongation adds to it)
     const double* bl = b;
+    // residual work planes: the fine level borrows the 3D path's slab-sized
+    // scratch, level l >= 1 its own (not yet written) solution buffer lev_x[l]
+    {
+        const size_t need = (size_t)count * c->n;
+        if (c->t3_cap < need) {
+            if (c->d_t3a) cudaFree(c->d_t3a);
+            if (c->d_t3b) cudaFree(c->d_t3b);
+            c->d_t3b = nullptr;
+            PINT_CUDA_CHECK(cudaMalloc(&c->d_t3a, need * sizeof(double) + 16));
+            PINT_CUDA_CHECK(cudaMalloc(&c->d_t3b, 16));
+            c->t3_cap = need;
+        }
+    }
     for (int l = 0; l + 1 < L; ++l) {
         const int m = F.m[l], mc = F.m[l + 1];
         double* x0 = l == 0 ? c->d_ft : c->lev_t[l];
+        double* rw = l == 0 ? c->d_t3a : c->lev_x[l];
         if (l == 0) {
             if (which == PINT_MG_ATILDE)
-                pre_level<FM_A>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true);
+                pre_level<FM_A>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true, rw);
             else
-                pre_level<FM_H>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true);
+                pre_level<FM_H>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true, rw);
         } else {
             pre_level<FM_9>(c, coarse_src(F, l), m, mc, count, F.damping, bl, x0, c->lev_b[l + 1],
-                            false);
+                            false, rw);
         }
         bl = c->lev_b[l + 1];
     }
