@@ -23,6 +23,7 @@
 // so results are bit-identical to scipy's csr_matvec on the same matrices.
 // Round-1 form: one thread per point, neighbours through L1/L2.
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 
 #include "pint_device.cuh"
@@ -76,21 +77,61 @@ __device__ __forceinline__ bool structural(int k) {
     return true;
 }
 
-// CSR row sum at (x, y) of plane v (m x m): sum = 0; sum += a_k v_k in column order
+// CSR row sum at (x, y) of plane v (m x m): sum = 0; sum += a_k v_k in column order.
+// Same terms, coefficients and order as evaluating coef<MODE>() for k = 0..8
+// (structural positions whose neighbour exists), with the row's base
+// pointers formed once: ncu of the generic loop showed 220 instructions per
+// point, almost all 64-bit index arithmetic.
 template <int MODE>
 __device__ __forceinline__ double frow(const Src& S, int s, const double* __restrict__ v, int m,
                                       int x, int y) {
     const int i = y * m + x;
+    const ptrdiff_t n = (ptrdiff_t)m * m;
     const bool w = x > 0, e = x < m - 1, so = y > 0, no = y < m - 1;
-    const bool ok[9] = {so && w, so, so && e, w, true, e, no && w, no, no && e};
-    const int off[9] = {-m - 1, -m, -m + 1, -1, 0, 1, m - 1, m, m + 1};
+    const double* f = S.f + (size_t)s * S.set_stride + i;  // centre entry of this row
+    const double* vi = v + i;
     double r = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-        if (!structural<MODE>(k) || !ok[k]) continue;
-        r = r + coef<MODE>(S, s, k, m, x, y) * __ldg(v + i + off[k]);
+    if constexpr (MODE == FM_9) {
+        if (so && w) r = r + __ldg(f) * __ldg(vi - m - 1);
+        if (so) r = r + __ldg(f + n) * __ldg(vi - m);
+        if (so && e) r = r + __ldg(f + 2 * n) * __ldg(vi - m + 1);
+        if (w) r = r + __ldg(f + 3 * n) * __ldg(vi - 1);
+        r = r + __ldg(f + 4 * n) * __ldg(vi);
+        if (e) r = r + __ldg(f + 5 * n) * __ldg(vi + 1);
+        if (no && w) r = r + __ldg(f + 6 * n) * __ldg(vi + m - 1);
+        if (no) r = r + __ldg(f + 7 * n) * __ldg(vi + m);
+        if (no && e) r = r + __ldg(f + 8 * n) * __ldg(vi + m + 1);
+        return r;
+    } else {
+        // compact fields: centre f, east f + n, north f + 2n; S / W are the
+        // north / east entries of rows i - m / i - 1
+        const double aS = so ? __ldg(f + 2 * n - m) : 0.0;
+        const double aW = w ? __ldg(f + n - 1) : 0.0;
+        const double aC = __ldg(f);
+        const double aE = e ? __ldg(f + n) : 0.0;
+        const double aN = no ? __ldg(f + 2 * n) : 0.0;
+        if constexpr (MODE == FM_A) {
+            if (so) r = r + aS * __ldg(vi - m);
+            if (w) r = r + aW * __ldg(vi - 1);
+            r = r + aC * __ldg(vi);
+            if (e) r = r + aE * __ldg(vi + 1);
+            if (no) r = r + aN * __ldg(vi + m);
+        } else {
+            // mu_k M + tau A_ref entry: add_matrices(mu_k, M, 1.0, A_ref.scaled(tau_ref))
+            // (schur.py:41-47, linalg.py:118-127); SW / NE carry mass only
+            const double mu = __ldg(S.mu + s), tau = S.tau;
+            const double* ms = S.mass;
+            auto hc = [&](int k, double a) { return mu * __ldg(ms + k) + 1.0 * (tau * a); };
+            if (so && w) r = r + hc(0, 0.0) * __ldg(vi - m - 1);
+            if (so) r = r + hc(1, aS) * __ldg(vi - m);
+            if (w) r = r + hc(3, aW) * __ldg(vi - 1);
+            r = r + hc(4, aC) * __ldg(vi);
+            if (e) r = r + hc(5, aE) * __ldg(vi + 1);
+            if (no) r = r + hc(7, aN) * __ldg(vi + m);
+            if (no && e) r = r + hc(8, 0.0) * __ldg(vi + m + 1);
+        }
+        return r;
     }
-    return r;
 }
 
 // ---- assembly ------------------------------------------------------------------
@@ -107,7 +148,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)n) return;
     const int t = blockIdx.y;
-    const int jj = (int)(g / m), ii = (int)(g - (long long)jj * m);
+    const int g32 = (int)g;
+    const int jj = g32 / m, ii = g32 - jj * m;
     const int i = ii + 1, j = jj + 1;
     const double* W = w + (size_t)t * c * c;
     auto cw = [&](int ci, int cj) { return __ldg(W + (size_t)cj * c + ci); };
@@ -205,7 +247,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)n) return;
     const int t = blockIdx.y;
-    const int y = (int)(g / m), x = (int)(g - (long long)y * m);
+    const int g32 = (int)g;  // g < n < 2^31: 32-bit division, not the 64-bit routine
+    const int y = g32 / m, x = g32 - y * m;
     const double d = damping / coef<MODE>(A, t, 4, m, x, y);
     x0[t * n + g] = d * __ldg(b + t * n + g);
 }
@@ -220,7 +263,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)nc) return;
     const int t = blockIdx.y;
-    const int Y = (int)(g / mc), X = (int)(g - (long long)Y * mc);
+    const int g32 = (int)g;
+    const int Y = g32 / mc, X = g32 - Y * mc;
     const double* bp = b + (size_t)t * n;
     const double* xp = x0 + (size_t)t * n;
     const double wt[3] = {0.5, 1.0, 0.5};
@@ -247,7 +291,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)n) return;
     const int t = blockIdx.y;
-    const int y = (int)(g / m), x = (int)(g - (long long)y * m);
+    const int g32 = (int)g;  // g < n < 2^31: 32-bit division, not the 64-bit routine
+    const int y = g32 / m, x = g32 - y * m;
     r[t * n + g] = __ldg(b + t * n + g) - frow<MODE>(A, t, x0 + (size_t)t * n, m, x, y);
 }
 
@@ -258,7 +303,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)nc) return;
     const int t = blockIdx.y;
-    const int Y = (int)(g / mc), X = (int)(g - (long long)Y * mc);
+    const int g32 = (int)g;
+    const int Y = g32 / mc, X = g32 - Y * mc;
     const double* rp = r + (size_t)t * n;
     const double wt[3] = {0.5, 1.0, 0.5};
     double v = 0.0;
@@ -285,7 +331,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)n) return;
     const int t = blockIdx.y;
-    const int y = (int)(g / m), xx = (int)(g - (long long)y * m);
+    const int g32 = (int)g;
+    const int y = g32 / m, xx = g32 - y * m;
     const double ac = direct ? __ldg(ac9 + (size_t)t * ac_stride + 4 * nc) : 1.0;
     int ja, jb, ia, ib;
     double wa, wb, ua, ub;
@@ -336,7 +383,8 @@ __global__ void __launch_bounds__(FT) k_f_smooth(Src A, FSmooth P) {
     const int t = blockIdx.y;
     double acc = 0.0;
     if (g < (long long)n) {
-        const int y = (int)(g / m), x = (int)(g - (long long)y * m);
+        const int g32 = (int)g;  // g < n < 2^31: 32-bit division, not the 64-bit routine
+    const int y = g32 / m, x = g32 - y * m;
         const size_t gi = (size_t)t * n + g;
         const double d = P.damping / coef<MODE>(A, t, 4, m, x, y);
         const double bv = __ldg(P.b + gi);
@@ -380,7 +428,8 @@ __global__ void __launch_bounds__(FT)
     const long long g = (long long)blockIdx.x * FT + threadIdx.x;
     if (g >= (long long)nc) return;
     const int s = blockIdx.y;
-    const int Y = (int)(g / mc), X = (int)(g - (long long)Y * mc);
+    const int g32 = (int)g;
+    const int Y = g32 / mc, X = g32 - Y * mc;
     const double wt[3] = {0.5, 1.0, 0.5};
     // fine box (2X-1 .. 2X+3) x (2Y-1 .. 2Y+3)
     double B[5][5];
