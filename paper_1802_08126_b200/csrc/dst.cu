@@ -250,7 +250,12 @@ __global__ void __launch_bounds__(DST_THREADS, 3) k_dst_fft(DstArgs a) {
 // compile-time multiples of one per-thread base address.
 // ---------------------------------------------------------------------------
 
-__host__ __device__ constexpr int dst_reg_pairs(int lg) { return lg >= 12 ? 1 : 4096 >> lg; }
+// column pairs per CTA: 64 KB tiles up to N = 1024; 128 KB tiles (one CTA per SM)
+// for N = 2048 / 4096, where wider row segments beat the lost CTA overlap
+// (N = 4096: 1.26 -> 1.45 TB/s, N = 2048: 1.64 -> 1.70 TB/s); N = 8192: one pair
+__host__ __device__ constexpr int dst_reg_pairs(int lg) {
+    return lg >= 13 ? 1 : lg >= 11 ? 8192 >> lg : 4096 >> lg;
+}
 
 namespace dstreg {
 
@@ -746,7 +751,8 @@ void dst_plan_build(DstPlan& d, int N) {
             d.reg_p = dst_reg_pairs(lg);
             if (const char* e = getenv("PINT_DST_P")) {
                 const int want = atoi(e);
-                if ((lg == 10 && (want == 2 || want == 4)) || (lg == 9 && (want == 4 || want == 8)))
+                if ((lg == 10 && (want == 2 || want == 4)) || (lg == 9 && (want == 4 || want == 8)) ||
+                    (lg == 11 && (want == 2 || want == 4)) || (lg == 12 && (want == 1 || want == 2)))
                     d.reg_p = want;
             }
             static bool attr_done = false;
@@ -760,6 +766,7 @@ void dst_plan_build(DstPlan& d, int N) {
                                                      PV * (16 << LGV)));
                 PINT_REGATTR(8, 16) PINT_REGATTR(9, 8) PINT_REGATTR(9, 4) PINT_REGATTR(10, 4)
                 PINT_REGATTR(10, 2) PINT_REGATTR(11, 2) PINT_REGATTR(12, 1) PINT_REGATTR(13, 1)
+                PINT_REGATTR(11, 4) PINT_REGATTR(12, 2)
 #undef PINT_REGATTR
                 attr_done = true;
             }
@@ -832,7 +839,7 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
         else launch(dstreg::k_dst_reg<1, LGV, PV>, dstreg::reg_threads<LGV, PV>());             \
     }
         PINT_REGL(8, 16) PINT_REGL(9, 8) PINT_REGL(9, 4) PINT_REGL(10, 4) PINT_REGL(10, 2)
-        PINT_REGL(11, 2) PINT_REGL(12, 1) PINT_REGL(13, 1)
+        PINT_REGL(11, 2) PINT_REGL(12, 1) PINT_REGL(13, 1) PINT_REGL(11, 4) PINT_REGL(12, 2)
 #undef PINT_REGL
     } else if (d.fast) {
         const int W = 2 * d.pairs;
