@@ -239,32 +239,35 @@ __global__ void __launch_bounds__(FX* FY)
 // unconditional division
 __device__ __noinline__ double fdiv_rn(double x, double y) { return x / y; }
 
+// The V-cycle kernels below run one thread per point of a 64 x 4 tile of a
+// plane (blockIdx.z = plane): no index divisions, 32-bit offsets inside the
+// plane (ncu of the linear-index form: 100-220 instructions per point, almost
+// all index arithmetic; the prolongation issue bound at 82 %).
+constexpr int GX = 64, GY = 4;
+
 // x0 = dinv * b with dinv = damping / diag  (spatial.py:142, 153)
 template <int MODE>
 __global__ void __launch_bounds__(FT)
     k_f_x0(int m, Src A, double damping, const double* __restrict__ b, double* __restrict__ x0) {
-    const size_t n = (size_t)m * m;
-    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
-    if (g >= (long long)n) return;
-    const int t = blockIdx.y;
-    const int g32 = (int)g;  // g < n < 2^31: 32-bit division, not the 64-bit routine
-    const int y = g32 / m, x = g32 - y * m;
+    const int x = blockIdx.x * GX + threadIdx.x, y = blockIdx.y * GY + threadIdx.y;
+    if (x >= m || y >= m) return;
+    const int t = blockIdx.z;
+    const size_t gi = (size_t)t * m * m + (y * m + x);
     const double d = damping / coef<MODE>(A, t, 4, m, x, y);
-    x0[t * n + g] = d * __ldg(b + t * n + g);
+    x0[gi] = d * __ldg(b + gi);
 }
 
 // b_c = P^T (b - A x0): the nine fine residuals of each coarse point, summed
 // over ascending fine index with weights (1/4, 1/2, 1) (spatial.py:156)
+// (round-1 form, kept for A/B: PINT_FIELD_RR)
 template <int MODE>
 __global__ void __launch_bounds__(FT)
     k_f_rr(int m, int mc, Src A, const double* __restrict__ b, const double* __restrict__ x0,
            double* __restrict__ bc) {
+    const int X = blockIdx.x * GX + threadIdx.x, Y = blockIdx.y * GY + threadIdx.y;
+    if (X >= mc || Y >= mc) return;
+    const int t = blockIdx.z;
     const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
-    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
-    if (g >= (long long)nc) return;
-    const int t = blockIdx.y;
-    const int g32 = (int)g;
-    const int Y = g32 / mc, X = g32 - Y * mc;
     const double* bp = b + (size_t)t * n;
     const double* xp = x0 + (size_t)t * n;
     const double wt[3] = {0.5, 1.0, 0.5};
@@ -274,11 +277,11 @@ __global__ void __launch_bounds__(FT)
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const int fy = 2 * Y + a, fx = 2 * X + q;
-            const double r = __ldg(bp + (size_t)fy * m + fx) - frow<MODE>(A, t, xp, m, fx, fy);
+            const double r = __ldg(bp + fy * m + fx) - frow<MODE>(A, t, xp, m, fx, fy);
             const double term = (wt[a] * wt[q]) * r;
             v = (a == 0 && q == 0) ? term : v + term;
         }
-    bc[t * nc + g] = v;
+    bc[t * nc + (Y * mc + X)] = v;
 }
 
 // r = b - A x0, one thread per FINE point (k_f_rr evaluates every fine
@@ -287,77 +290,71 @@ template <int MODE>
 __global__ void __launch_bounds__(FT)
     k_f_resid(int m, Src A, const double* __restrict__ b, const double* __restrict__ x0,
               double* __restrict__ r) {
-    const size_t n = (size_t)m * m;
-    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
-    if (g >= (long long)n) return;
-    const int t = blockIdx.y;
-    const int g32 = (int)g;  // g < n < 2^31: 32-bit division, not the 64-bit routine
-    const int y = g32 / m, x = g32 - y * m;
-    r[t * n + g] = __ldg(b + t * n + g) - frow<MODE>(A, t, x0 + (size_t)t * n, m, x, y);
+    const int x = blockIdx.x * GX + threadIdx.x, y = blockIdx.y * GY + threadIdx.y;
+    if (x >= m || y >= m) return;
+    const int t = blockIdx.z;
+    const size_t pb = (size_t)t * m * m;
+    const int i = y * m + x;
+    r[pb + i] = __ldg(b + pb + i) - frow<MODE>(A, t, x0 + pb, m, x, y);
 }
 
 // b_c = P^T r from stored residuals: same nine terms, order and weights as k_f_rr
 __global__ void __launch_bounds__(FT)
     k_f_restrict(int m, int mc, const double* __restrict__ r, double* __restrict__ bc) {
-    const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
-    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
-    if (g >= (long long)nc) return;
-    const int t = blockIdx.y;
-    const int g32 = (int)g;
-    const int Y = g32 / mc, X = g32 - Y * mc;
-    const double* rp = r + (size_t)t * n;
+    const int X = blockIdx.x * GX + threadIdx.x, Y = blockIdx.y * GY + threadIdx.y;
+    if (X >= mc || Y >= mc) return;
+    const int t = blockIdx.z;
+    const double* rp = r + (size_t)t * m * m + (2 * Y) * m + 2 * X;
     const double wt[3] = {0.5, 1.0, 0.5};
     double v = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            const double term = (wt[a] * wt[q]) * __ldg(rp + (size_t)(2 * Y + a) * m + (2 * X + q));
+            const double term = (wt[a] * wt[q]) * __ldg(rp + a * m + q);
             v = (a == 0 && q == 0) ? term : v + term;
         }
-    bc[t * nc + g] = v;
+    bc[(size_t)t * mc * mc + (Y * mc + X)] = v;
 }
 
 // x = x0 + P e (csr_matvec of P, ascending coarse index); on the last
-// level above the 1x1 coarsest grid e = b_c / a_c (spatial.py:149-150, 157)
+// level above the 1x1 coarsest grid e = b_c / a_c (spatial.py:149-150, 157).
+// Per axis an odd coordinate has one term (weight 1), an even one the two
+// neighbours (weight 1/2 each, those inside the coarse grid).
 template <bool DIRECT>
 __global__ void __launch_bounds__(FT)
     k_f_prolong(int m, int mc, const double* __restrict__ ac9, size_t ac_stride,
                 const double* __restrict__ ec, double* __restrict__ x) {
     // DIRECT is a template parameter: a runtime flag lets the compiler
     // evaluate e / 1.0 speculatively for every term
-    constexpr bool direct = DIRECT;
-    const size_t n = (size_t)m * m, nc = (size_t)mc * mc;
-    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
-    if (g >= (long long)n) return;
-    const int t = blockIdx.y;
-    const int g32 = (int)g;
-    const int y = g32 / m, xx = g32 - y * m;
-    const double ac = direct ? __ldg(ac9 + (size_t)t * ac_stride + 4 * nc) : 1.0;
-    int ja, jb, ia, ib;
-    double wa, wb, ua, ub;
-    if (y & 1) { ja = (y - 1) >> 1; wa = 1.0; jb = -1; wb = 0.0; }
-    else { ja = (y >> 1) - 1; wa = 0.5; jb = y >> 1; wb = 0.5; }
-    if (xx & 1) { ia = (xx - 1) >> 1; ua = 1.0; ib = -1; ub = 0.0; }
-    else { ia = (xx >> 1) - 1; ua = 0.5; ib = xx >> 1; ub = 0.5; }
-    const bool va = ja >= 0, vb = jb >= 0 && jb < mc;
-    const bool ha = ia >= 0, hb = ib >= 0 && ib < mc;
-    const double* ep = ec + (size_t)t * nc;
+    const int xx = blockIdx.x * GX + threadIdx.x, y = blockIdx.y * GY + threadIdx.y;
+    if (xx >= m || y >= m) return;
+    const int t = blockIdx.z;
+    const int nc = mc * mc;
+    const double ac = DIRECT ? __ldg(ac9 + (size_t)t * ac_stride + 4 * (size_t)nc) : 1.0;
+    const bool yo = y & 1, xo = xx & 1;
+    const int ja = (y - 1) >> 1, ia = (xx - 1) >> 1;      // first term of each axis
+    const bool va = ja >= 0, vb = !yo && ja + 1 < mc;      // rows ja, ja + 1
+    const bool ha = ia >= 0, hb = !xo && ia + 1 < mc;      // columns ia, ia + 1
+    // every existing term carries the weight wy * wx (1, 1/2 or 1/4)
+    const double w = (yo ? 1.0 : 0.5) * (xo ? 1.0 : 0.5);
+    const double* ep = ec + (size_t)t * nc + (ja * mc + ia);
     double pe = 0.0;
     bool first = true;
-    auto add = [&](bool ok, double w, int jy, int jx) {
+    auto add = [&](bool ok, int off) {
         if (!ok) return;
-        double e = __ldg(ep + (size_t)jy * mc + jx);
-        if (direct) e = e / ac;
+        double e = __ldg(ep + off);
+        if (DIRECT) e = e / ac;
         const double term = w * e;
         pe = first ? term : pe + term;
         first = false;
     };
-    add(va && ha, wa * ua, ja, ia);
-    add(va && hb, wa * ub, ja, ib);
-    add(vb && ha, wb * ua, jb, ia);
-    add(vb && hb, wb * ub, jb, ib);
-    x[t * n + g] = x[t * n + g] + pe;
+    add(va && ha, 0);
+    add(va && hb, 1);
+    add(vb && ha, mc);
+    add(vb && hb, mc + 1);
+    double* xp = x + (size_t)t * m * m + (y * m + xx);
+    *xp = *xp + pe;
 }
 
 struct FSmooth {
@@ -378,14 +375,12 @@ struct FSmooth {
 template <int MODE>
 __global__ void __launch_bounds__(FT) k_f_smooth(Src A, FSmooth P) {
     const int m = P.m;
-    const size_t n = (size_t)m * m;
-    const long long g = (long long)blockIdx.x * FT + threadIdx.x;
-    const int t = blockIdx.y;
+    const int x = blockIdx.x * GX + threadIdx.x, y = blockIdx.y * GY + threadIdx.y;
+    const int t = blockIdx.z;
     double acc = 0.0;
-    if (g < (long long)n) {
-        const int g32 = (int)g;  // g < n < 2^31: 32-bit division, not the 64-bit routine
-    const int y = g32 / m, x = g32 - y * m;
-        const size_t gi = (size_t)t * n + g;
+    if (x < m && y < m) {
+        const size_t n = (size_t)m * m;
+        const size_t gi = (size_t)t * n + (y * m + x);
         const double d = P.damping / coef<MODE>(A, t, 4, m, x, y);
         const double bv = __ldg(P.b + gi);
         const double xn = __ldg(P.x + gi) + d * (bv - frow<MODE>(A, t, P.x + (size_t)t * n, m, x, y));
@@ -413,7 +408,8 @@ __global__ void __launch_bounds__(FT) k_f_smooth(Src A, FSmooth P) {
     }
     if (P.part) {
         const double s = block_sum<FT>(acc);
-        if (threadIdx.x == 0) P.part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            P.part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
     }
 }
 
@@ -481,6 +477,10 @@ __global__ void __launch_bounds__(FT)
 
 dim3 tile_grid(int m, int planes) {
     return dim3((m + FX - 1) / FX, (m + FY - 1) / FY, (planes + FG - 1) / FG);
+}
+
+dim3 grid2(int m, int planes) {  // 64 x 4 tiles of an m x m plane, one plane per z
+    return dim3((m + GX - 1) / GX, (m + GY - 1) / GY, planes);
 }
 
 dim3 pt_grid(size_t pts, int planes) {
@@ -591,15 +591,15 @@ void pre_level(pint_ctx* c, const Src& S, int m, int mc, int count, double dampi
                const double* b, double* x0, double* bc, bool fine, double* rwork) {
     ProfScope prof(c, fine ? K_MG_PRE_FINE : K_MG_PRE_COARSE,
                    8.0 * count * (3.0 * m * m + (double)mc * mc));
-    k_f_x0<MODE><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(m, S, damping, b, x0);
+    k_f_x0<MODE><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(m, S, damping, b, x0);
     static const bool fused_rr = getenv("PINT_FIELD_RR") != nullptr;  // round-1 form (A/B)
     if (fused_rr || !rwork) {
-        k_f_rr<MODE><<<pt_grid((size_t)mc * mc, count), FT, 0, c->stream>>>(m, mc, S, b, x0, bc);
+        k_f_rr<MODE><<<grid2(mc, count), dim3(GX, GY), 0, c->stream>>>(m, mc, S, b, x0, bc);
         c->launches += 2;
         return;
     }
-    k_f_resid<MODE><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(m, S, b, x0, rwork);
-    k_f_restrict<<<pt_grid((size_t)mc * mc, count), FT, 0, c->stream>>>(m, mc, rwork, bc);
+    k_f_resid<MODE><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(m, S, b, x0, rwork);
+    k_f_restrict<<<grid2(mc, count), dim3(GX, GY), 0, c->stream>>>(m, mc, rwork, bc);
     c->launches += 3;
 }
 
@@ -614,10 +614,10 @@ void post_level(pint_ctx* c, const Src& S, const FieldMg& F, int l, int count, c
     ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE,
                    8.0 * count * (4.0 * m * m + (double)mc * mc));
     if (direct)
-        k_f_prolong<true><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(
+        k_f_prolong<true><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(
             m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, ec, x);
     else
-        k_f_prolong<false><<<pt_grid((size_t)m * m, count), FT, 0, c->stream>>>(
+        k_f_prolong<false><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(
             m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, ec, x);
     FSmooth P{};
     P.m = m;
@@ -631,15 +631,16 @@ void post_level(pint_ctx* c, const Src& S, const FieldMg& F, int l, int count, c
     P.rsteps = c->d_rsteps;
     P.pin = pin;
     P.aux = aux;
-    const dim3 g = pt_grid((size_t)m * m, count);
+    const dim3 g = grid2(m, count);
+    const size_t nblk = (size_t)g.x * g.y * g.z;
     const bool dot = top && epi_dot(epi);
     if (dot) {
-        ensure_partials(c, (size_t)g.x * g.y);
+        ensure_partials(c, nblk);
         P.part = c->d_part;
     }
-    k_f_smooth<MODE><<<g, FT, 0, c->stream>>>(S, P);
+    k_f_smooth<MODE><<<g, dim3(GX, GY), 0, c->stream>>>(S, P);
     c->launches += 2;
-    if (dot) reduce_partials(c, (int)(g.x * g.y), acc_slot);
+    if (dot) reduce_partials(c, (int)nblk, acc_slot);
 }
 
 }  // namespace
