@@ -157,6 +157,42 @@ def test_dst_naive_formulas(N):
         assert err <= tol, (kind, err, tol)
 
 
+def test_dst_n8192_sampled_rows():
+    """N = 8192 is the time axis of BASELINE config 5 at G = 8 (one column pair
+    per CTA, 128 KB tile): sampled output rows of all four transforms against
+    the naive sine-kernel sums in extended precision, round trip, adjointness."""
+    N = 8192
+    rng = np.random.default_rng(8192)
+    u = rng.standard_normal((N, 9))
+    plan = pg.DstPlan(N)
+    rows = np.array([0, 1, 2, 17, 1023, 4095, 4096, 4097, 6000, 8190, 8191])
+    k = np.arange(1, N + 1, dtype=np.int64)
+    ul = u.astype(np.longdouble)
+    w = np.ones(N, dtype=np.longdouble)
+    w[-1] = 0.5
+    tol = 1e-13 * np.sqrt(N / 128)
+
+    def srow(a, b):  # sin((2a - 1) b pi / 2N) for index arrays a (modes), b (steps)
+        r = ((2 * a - 1) * b) % (4 * N)
+        return np.sin(r.astype(np.longdouble) * np.pi / (2 * N))
+
+    got = {kind: getattr(plan, kind)(u) for kind in
+           ("inverse", "inverse_transpose", "forward", "forward_transpose")}
+    for r in rows:
+        col = srow(k, np.int64(r + 1))      # S[:, r]: all modes at step r+1
+        row = srow(np.int64(r + 1), k)      # S[r, :]: mode r+1 at all steps
+        ref = {"inverse": col @ ul, "inverse_transpose": row @ ul,
+               "forward": (2.0 / N) * (row @ (w[:, None] * ul)),
+               "forward_transpose": (2.0 / N) * w[r] * (col @ ul)}
+        for kind, val in ref.items():
+            err = float(np.max(np.abs(got[kind][r] - val.astype(np.float64))))
+            assert err <= tol, (kind, int(r), err, tol)
+    np.testing.assert_allclose(plan.inverse(plan.forward(u)), u, atol=1e-11)
+    v = rng.standard_normal((N, 9))
+    assert np.sum(plan.forward(u) * v) == pytest.approx(np.sum(u * plan.forward_transpose(v)),
+                                                        abs=1e-10)
+
+
 @pytest.mark.parametrize("N", [1, 2, 3, 8, 64, 1024])
 def test_dst_round_trip_and_adjoint(N):
     """pkg/tests/test_dst.py:44-70: inverse(forward(u)) = u; <Fu, v> = <u, F^T v>."""
