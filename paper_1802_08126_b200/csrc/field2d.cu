@@ -33,7 +33,10 @@ namespace pint {
 
 namespace {
 
-constexpr int FX = 32, FY = 8, FG = 8;  // 32x8 tile, 8 time planes per CTA (marching ops)
+#ifndef PINT_FG
+#define PINT_FG 16
+#endif
+constexpr int FX = 32, FY = 8, FG = PINT_FG;  // 32x8 tile, FG time planes per CTA (marching ops)
 constexpr int FT = 256;
 
 enum FieldMode : int { FM_A = 0, FM_H = 1, FM_9 = 2 };
