@@ -10,8 +10,11 @@
 // sums over ascending fine index, prolongation over ascending coarse index,
 // so results are bit-identical to the oracle's scipy products.
 //
-// Round-1 form: thread per point, neighbours through L1/L2 (no TMA bands),
-// one launch per level and phase over every plane of the batch.
+// Three generations live here: the generic K / K^T / A_bd applies (k3_timeop,
+// thread per point); the z-marching register-window kernels (kz_*: r1, z and,
+// for grids the band kernels are not built for, the V-cycle phases); and the
+// TMA band kernels of mg3_band_kernels.inc (kc3_*: fused V-cycle, stencil
+// applies, shared-memory tail), which carry the c3 / c5 hot path.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -154,16 +157,6 @@ __global__ void __launch_bounds__(T3)
 }
 
 __global__ void __launch_bounds__(T3)
-    k3_apply(int m, const double* __restrict__ st, const double* __restrict__ in,
-             double* __restrict__ out) {
-    const Pt q = point3(m);
-    if (!q.ok) return;
-    const long long n = (long long)m * m * m;
-    const long long t = blockIdx.y;
-    out[t * n + q.i] = st27(st, in + t * n, m, q.x, q.y, q.z);
-}
-
-__global__ void __launch_bounds__(T3)
     k3_fold(int m, const double* __restrict__ steps, const double* __restrict__ mass,
             const double* __restrict__ load, const double* __restrict__ u0,
             double* __restrict__ f) {
@@ -177,98 +170,6 @@ __global__ void __launch_bounds__(T3)
 }
 
 // ---- multigrid ---------------------------------------------------------------
-// r = b - A (dinv*b)   (spatial.py:153,156: x = dinv*b; r = b - A x)
-__global__ void __launch_bounds__(T3)
-    k3_residual(int m, const double* __restrict__ tab, const int* __restrict__ sid,
-                const double* __restrict__ b, double* __restrict__ r) {
-    const Pt q = point3(m);
-    if (!q.ok) return;
-    const long long n = (long long)m * m * m;
-    const long long t = blockIdx.y;
-    const double* tb = tab + (size_t)__ldg(sid + t) * 28;
-    const double d = __ldg(tb + 27);
-    const double* bp = b + t * n;
-    r[t * n + q.i] = __ldg(bp + q.i) - st27_scaled(tb, d, bp, m, q.x, q.y, q.z);
-}
-
-// b_c = P^T r: ascending fine index (z, y, x) over the 27 fine nodes of the
-// coarse node, weights (wz*wy)*wx with w = 0.5, 1, 0.5  (kron of spatial.py:75-84)
-__global__ void __launch_bounds__(T3)
-    k3_restrict(int m, int mc, const double* __restrict__ r, double* __restrict__ bc) {
-    const Pt q = point3(mc);
-    if (!q.ok) return;
-    const long long n = (long long)m * m * m, nc = (long long)mc * mc * mc;
-    const long long t = blockIdx.y;
-    const double* rp = r + t * n;
-    const double w[3] = {0.5, 1.0, 0.5};
-    double s = 0.0;
-    int k = 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc, ++k) {
-                const long long fi = ((long long)(2 * q.z + a) * m + (2 * q.y + bb)) * m + (2 * q.x + cc);
-                const double tterm = ((w[a] * w[bb]) * w[cc]) * __ldg(rp + fi);
-                s = (k == 0) ? tterm : s + tterm;
-            }
-    bc[t * nc + q.i] = s;
-}
-
-__device__ __forceinline__ void pro_terms(int f, int mc, int* j, double* w, int& cnt) {
-    if (f & 1) {
-        j[0] = (f - 1) >> 1;
-        w[0] = 1.0;
-        cnt = 1;
-    } else {
-        cnt = 0;
-        if ((f >> 1) - 1 >= 0) {
-            j[cnt] = (f >> 1) - 1;
-            w[cnt] = 0.5;
-            ++cnt;
-        }
-        if ((f >> 1) < mc) {
-            j[cnt] = f >> 1;
-            w[cnt] = 0.5;
-            ++cnt;
-        }
-    }
-}
-
-// x = dinv*b + P e (csr_matvec of P over ascending coarse index); e = b_c / a_c
-// on the 1x1x1 coarsest grid (spatial.py:149-150, 157)
-__global__ void __launch_bounds__(T3)
-    k3_prolong(int m, int mc, const double* __restrict__ tab, const double* __restrict__ tabc,
-               const int* __restrict__ sid, int direct, const double* __restrict__ b,
-               const double* __restrict__ ec, double* __restrict__ x) {
-    const Pt q = point3(m);
-    if (!q.ok) return;
-    const long long n = (long long)m * m * m, nc = (long long)mc * mc * mc;
-    const long long t = blockIdx.y;
-    const int set = __ldg(sid + t);
-    const double d = __ldg(tab + (size_t)set * 28 + 27);
-    const double ac = direct ? __ldg(tabc + (size_t)set * 28 + 13) : 1.0;
-    int jz[2], jy[2], jx[2], nz, ny, nx;
-    double wz[2], wy[2], wx[2];
-    pro_terms(q.z, mc, jz, wz, nz);
-    pro_terms(q.y, mc, jy, wy, ny);
-    pro_terms(q.x, mc, jx, wx, nx);
-    const double* ep = ec + t * nc;
-    double pe = 0.0;
-    bool first = true;
-    for (int a = 0; a < nz; ++a)
-        for (int bb = 0; bb < ny; ++bb)
-            for (int cc = 0; cc < nx; ++cc) {
-                double e = __ldg(ep + ((long long)jz[a] * mc + jy[bb]) * mc + jx[cc]);
-                if (direct) e = e / ac;
-                const double tterm = ((wz[a] * wy[bb]) * wx[cc]) * e;
-                pe = first ? tterm : pe + tterm;
-                first = false;
-            }
-    x[t * n + q.i] = d * __ldg(b + t * n + q.i) + pe;
-}
-
 struct Smooth3 {
     int m;
     const double* tab;
@@ -284,49 +185,6 @@ struct Smooth3 {
     const double* aux;
     double* part;
 };
-
-// x += dinv*(b - A x) (spatial.py:159-160) + the finest-level epilogues
-__global__ void __launch_bounds__(T3) k3_smooth(Smooth3 a) {
-    const Pt q = point3(a.m);
-    const long long n = (long long)a.m * a.m * a.m;
-    const long long t = blockIdx.y;
-    double acc = 0.0;
-    if (q.ok) {
-        const double* tb = a.tab + (size_t)__ldg(a.sid + t) * 28;
-        const double d = __ldg(tb + 27);
-        const long long gi = t * n + q.i;
-        const double bv = __ldg(a.b + gi);
-        const double xv = __ldg(a.x + gi);
-        const double xn = xv + d * (bv - st27(tb, a.x + t * n, a.m, q.x, q.y, q.z));
-        auto divtau = [&](double v) {
-            const double r = __ldg(a.rsteps + t);
-            return r > 0.0 ? v * r : v / __ldg(a.steps + t);
-        };
-        switch (a.epi) {
-            case EPI_PLAIN: a.out[gi] = xn; break;
-            case EPI_DIV_TAU: a.out[gi] = divtau(xn); break;
-            case EPI_UZAWA_P: {
-                const double dp = divtau(xn);
-                a.out[gi] = __ldg(a.pin + gi) + dp;
-                acc = bv * dp;
-                break;
-            }
-            case EPI_DOT_TAU: acc = bv * divtau(xn); break;
-            case EPI_SCALE: a.out[gi] = a.scale * xn; break;
-            case EPI_SCALE_DOT: {
-                const double w = a.scale * xn;
-                a.out[gi] = w;
-                acc = __ldg(a.aux + gi) * w;
-                break;
-            }
-            case EPI_SCALE_DOTONLY: acc = __ldg(a.aux + gi) * (a.scale * xn); break;
-        }
-    }
-    if (a.part) {
-        const double s = block_sum<T3>(acc);
-        if (threadIdx.x == 0) a.part[(long long)blockIdx.y * gridDim.x + blockIdx.x] = s;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // z-marching stencil engine (round-1 rewrite of the thread-per-point form).
@@ -829,7 +687,7 @@ __global__ void __launch_bounds__(ZX * ZY)
 
 // b_c = P^T r: for coarse (Z, Y, X) the 27 fine nodes (2Z+a, 2Y+bb, 2X+cc) in
 // ascending fine index, weights (wa*wb)*wc with w = (0.5, 1, 0.5) (kron of
-// spatial.py:75-84, same order as k3_restrict).  z-marching over coarse Z:
+// spatial.py:75-84, same order as the oracle).  z-marching over coarse Z:
 // fine plane 2Z+2 is plane 2(Z+1) of the next coarse point.
 __global__ void __launch_bounds__(ZX * ZY)
     kz_restrict(int m, int mc, const double* __restrict__ r, double* __restrict__ bc) {
