@@ -81,29 +81,77 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clock and throttle reasons during the timed region: NVML in process
+    (a few ms per sample, so even the 35 ms headline region gets several),
+    nvidia-smi every 0.2 s when pynvml is not importable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index=0):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.source = None
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml as nv
+
+        nv.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        idx = self.index
+        if vis and all(v.strip().isdigit() for v in vis.split(",")):
+            ids = [int(v) for v in vis.split(",")]
+            idx = ids[self.index] if self.index < len(ids) else self.index
+        h = nv.nvmlDeviceGetHandleByIndex(idx)
+        bits = [(nv.nvmlClocksEventReasonHwSlowdown, "hw_slowdown"),
+                (nv.nvmlClocksEventReasonHwThermalSlowdown, "hw_thermal_slowdown"),
+                (nv.nvmlClocksEventReasonSwThermalSlowdown, "sw_thermal_slowdown"),
+                (nv.nvmlClocksEventReasonSwPowerCap, "sw_power_cap")]
+        try:
+            get_reasons = nv.nvmlDeviceGetCurrentClocksEventReasons
+        except AttributeError:
+            get_reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        self.source = "nvml"
+        while not self._stop.is_set():
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            self.mx.append(mx)
+            r = get_reasons(h)
+            for bit, name in bits:
+                if r & bit:
+                    self.reasons.add(name)
+            self._stop.wait(0.004)
+
+    def _run_smi(self):
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
                     ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+                    r = [x.strip() for x in out.stdout.strip().split(",")]
+                    if r[0].replace(".", "").isdigit():
+                        self.sm.append(float(r[0]))
+                    if r[1].replace(".", "").isdigit():
+                        self.mx.append(float(r[1]))
+                    for i, name in enumerate(self.NAMES):
+                        if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
+                            self.reasons.add(name)
             except Exception:
                 return
             self._stop.wait(0.2)
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            if not self.sm:
+                self._run_smi()
 
     def __enter__(self):
         self._t.start()
@@ -114,16 +162,10 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return None
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": self.source}
 
 
 # ----------------------------------------------------------------------------
