@@ -150,6 +150,20 @@ int pint_field_set(pint_ctx* ctx, int step0, int count, const double* fields);
  * cell_w[count][cells][cells] ([j][i] for cell (i, j)), the element loop of
  * problems.py:99-138 with w_e K_e (bit-identical to the scipy assembly). */
 int pint_field_assemble(pint_ctx* ctx, int step0, int count, const double* cell_w);
+/* Separable family (instead of pint_field_set / pint_field_assemble): the
+ * cell weight of step n is sum_r weights[n][r] * cell_w[r] (terms <=
+ * PINT_FSEP_MAX = 3; config 4: a = (1 + 0.1 U) + (0.5 sin 2 pi t_n) r^2).
+ * The stiffness is linear in the weight, so A_n = sum_r weights[n][r] A(w_r)
+ * and, because the Galerkin product is linear too, every coarse operator is
+ * the same combination of `terms` coarse tables: the device keeps
+ * [terms][3][n] fine and [terms][9][m_l^2] coarse tables (cache resident)
+ * instead of [N][3][n] / [N][9][m_l^2] slabs (25.7 + 2 x 25.6 GB at config 4)
+ * and forms every coefficient in registers.  The H~ set of such a problem
+ * uses the same form with the two terms (M, A_ref) and weights (mu_k,
+ * tau_ref).  Each coefficient differs from the per-step assembly by
+ * rounding (a few ulps), so this path is held to a tolerance, not to bit
+ * equality (tests/test_gpu_field.py). */
+int pint_field_separable(pint_ctx* ctx, int terms, const double* cell_w, const double* weights);
 /* A_ref (schur.py:41-47): fields[3][n], or (fields == NULL) a copy of step `step`. */
 int pint_field_aref(pint_ctx* ctx, int step, const double* fields);
 /* Field multigrid set: Galerkin coarse rows of every step (A~) or mode

@@ -191,7 +191,10 @@ class GpuProblem(HostProblem):
     def _upload_fields(self):
         """Per-point stiffness of every step and of A_ref into HBM."""
         spec, ctx = self.spec, self.ctx
-        if self.field == "family":
+        if self.field == "family" and spec.stiffness.terms is not None:
+            a, c = spec.stiffness.terms
+            ctx.call("pint_field_separable", int(a.shape[0]), a.ctypes.data, c.ctypes.data)
+        elif self.field == "family":
             fam = spec.stiffness
             for n0 in range(0, self.N, self._FIELD_CHUNK):
                 n1 = min(self.N, n0 + self._FIELD_CHUNK)

@@ -99,6 +99,7 @@ _SIGNATURES = {
     "pint_launch_count": (ctypes.c_longlong, [_P]),
     "pint_field_set": (_I, [_P, _I, _I, _P]),
     "pint_field_assemble": (_I, [_P, _I, _I, _P]),
+    "pint_field_separable": (_I, [_P, _I, _P, _P]),
     "pint_field_aref": (_I, [_P, _I, _P]),
     "pint_mg_set_field": (_I, [_P, _I, _I, _P, _D, _P]),
     "pint_sequential_euler": (_I, [_P, _P, _P, _P, _D, _I, _IP, _DP]),

@@ -191,6 +191,7 @@ void free_slabs(pint_ctx* c) {
 void free_field_set(FieldMg& F) {
     for (double* p : F.f9) dfree(p);
     dfree(F.d_mu);
+    if (F.own_sc) dfree(F.d_sc);
     F = FieldMg{};
 }
 
@@ -199,9 +200,14 @@ void free_field(pint_ctx* c) {
     dfree(c->d_fa);
     dfree(c->d_fref);
     dfree(c->d_ft);
+    dfree(c->d_fsep);
+    dfree(c->d_fsc);
+    dfree(c->d_unit);
     for (double* p : c->lev_t) dfree(p);
     c->lev_t.clear();
-    c->d_fa = c->d_fref = c->d_ft = nullptr;
+    c->d_fa = c->d_fref = c->d_ft = c->d_fsep = c->d_fsc = c->d_unit = nullptr;
+    c->fsep_R = 0;
+    c->h_fsc.clear();
     c->field = false;
     c->fref_ready = false;
 }
@@ -561,11 +567,18 @@ static void enable_field(pint_ctx* c) {
     require_problem(c);
     if (c->dims != 2) pint_throw(PINT_INPUT, "per-point stiffness fields are 2D");
     if (!c->field) {
+        c->d_fref = dalloc<double>((size_t)3 * c->n);
+        c->field = true;
+    }
+}
+
+// per-step compact fields [N][3][n] (not held by separable families)
+static void ensure_step_fields(pint_ctx* c) {
+    if (c->fsep_R) pint_throw(PINT_INPUT, "the stiffness family was declared separable");
+    if (!c->d_fa) {
         c->d_fa = dalloc<double>((size_t)c->N * 3 * c->n);
         PINT_CUDA_CHECK(cudaMemsetAsync(c->d_fa, 0, (size_t)c->N * 3 * c->n * sizeof(double),
                                         c->stream));
-        c->d_fref = dalloc<double>((size_t)3 * c->n);
-        c->field = true;
     }
 }
 
@@ -591,6 +604,7 @@ int pint_mg_set_options(pint_ctx* c, int which, int cycles, int smooth_steps) {
 int pint_field_set(pint_ctx* c, int step0, int count, const double* fields) {
     return guarded(c, [&] {
         enable_field(c);
+        ensure_step_fields(c);
         if (step0 < 0 || count < 0 || step0 + count > c->N || !fields)
             pint_throw(PINT_DIMENSION, "bad step range");
         const size_t cnt = (size_t)count * 3 * c->n;
@@ -603,6 +617,7 @@ int pint_field_set(pint_ctx* c, int step0, int count, const double* fields) {
 int pint_field_assemble(pint_ctx* c, int step0, int count, const double* cell_w) {
     return guarded(c, [&] {
         enable_field(c);
+        ensure_step_fields(c);
         if (step0 < 0 || count < 0 || step0 + count > c->N || !cell_w)
             pint_throw(PINT_DIMENSION, "bad step range");
         if (count == 0) return;
@@ -621,6 +636,41 @@ int pint_field_assemble(pint_ctx* c, int step0, int count, const double* cell_w)
     });
 }
 
+int pint_field_separable(pint_ctx* c, int terms, const double* cell_w, const double* weights) {
+    return guarded(c, [&] {
+        enable_field(c);
+        if (terms < 1 || terms > PINT_FSEP_MAX || !cell_w || !weights)
+            pint_throw(PINT_INPUT, "bad separable family (1 .. PINT_FSEP_MAX terms)");
+        if (c->d_fa) pint_throw(PINT_INPUT, "per-step stiffness fields are already set");
+        graph_reset(c);
+        for (FieldMg& F : c->fmg) free_field_set(F);  // their tables belong to the old family
+        const size_t cw = (size_t)(c->m + 1) * (c->m + 1) * terms;
+        double* tmp = dalloc<double>(cw);
+        PINT_CUDA_CHECK(cudaMemcpyAsync(tmp, cell_w, cw * sizeof(double), cudaMemcpyDefault,
+                                        c->stream));
+        dfree(c->d_fsep);
+        dfree(c->d_fsc);
+        c->d_fsep = dalloc<double>((size_t)terms * 3 * c->n);
+        pint::field_assemble(c, 0, terms, tmp, c->d_fsep);
+        c->h_fsc.assign((size_t)c->N * terms, 0.0);
+        if (is_device_ptr(weights)) {
+            PINT_CUDA_CHECK(cudaMemcpyAsync(c->h_fsc.data(), weights, c->h_fsc.size() * sizeof(double),
+                                            cudaMemcpyDeviceToHost, c->stream));
+            PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        } else {
+            std::copy(weights, weights + c->h_fsc.size(), c->h_fsc.begin());
+        }
+        c->d_fsc = upload(c, c->h_fsc.data(), c->h_fsc.size());
+        if (!c->d_unit) {
+            const double unit[2] = {1.0, 0.0};
+            c->d_unit = upload(c, unit, 2);
+        }
+        c->fsep_R = terms;
+        PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        dfree(tmp);
+    });
+}
+
 int pint_field_aref(pint_ctx* c, int step, const double* fields) {
     return guarded(c, [&] {
         enable_field(c);
@@ -630,9 +680,14 @@ int pint_field_aref(pint_ctx* c, int step, const double* fields) {
                                             cudaMemcpyDefault, c->stream));
         } else {
             if (step < 0 || step >= c->N) pint_throw(PINT_DIMENSION, "bad A_ref step");
-            PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_fref, c->d_fa + (size_t)step * cnt,
-                                            cnt * sizeof(double), cudaMemcpyDeviceToDevice,
-                                            c->stream));
+            if (c->fsep_R) {
+                pint::field_sep_step(c, step, c->d_fref);
+            } else {
+                if (!c->d_fa) pint_throw(PINT_INPUT, "no stiffness fields set");
+                PINT_CUDA_CHECK(cudaMemcpyAsync(c->d_fref, c->d_fa + (size_t)step * cnt,
+                                                cnt * sizeof(double), cudaMemcpyDeviceToDevice,
+                                                c->stream));
+            }
         }
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         c->fref_ready = true;
@@ -662,18 +717,41 @@ int pint_mg_set_field(pint_ctx* c, int which, int levels, const int* level_m, do
         F.m.assign(level_m, level_m + levels);
         F.damping = damping;
         F.f9.assign(levels, nullptr);
+        if (!c->fsep_R && !c->d_fa) pint_throw(PINT_INPUT, "no stiffness fields set");
+        // separable family: R term tables per level, weights (1 .. , s_n) for A~
+        // and (mu_k, tau_ref) for H_k = mu_k M + tau_ref A_ref
+        F.sep = !c->fsep_R ? 0 : which == PINT_MG_ATILDE ? c->fsep_R : 2;
+        const size_t rows = F.sep ? (size_t)F.sep : (size_t)c->N;
         for (int l = 1; l < levels; ++l)
-            F.f9[l] = dalloc<double>((size_t)c->N * 9 * level_m[l] * level_m[l]);
+            F.f9[l] = dalloc<double>(rows * 9 * level_m[l] * level_m[l]);
         if (mu) F.d_mu = upload(c, mu, c->N);
+        std::vector<double> hsc;
+        if (F.sep && which == PINT_MG_ATILDE) {
+            F.d_sc = c->d_fsc;
+            hsc = c->h_fsc;
+        } else if (F.sep) {
+            hsc.resize((size_t)c->N * 2);
+            for (int k = 0; k < c->N; ++k) {
+                hsc[2 * (size_t)k] = mu[k];
+                hsc[2 * (size_t)k + 1] = c->tau_ref;
+            }
+            F.d_sc = upload(c, hsc.data(), hsc.size());
+            F.own_sc = true;
+        }
         pint::field_galerkin(c, which);
         // coarsest pivots (spatial.py:143 factorises the 1x1 operator)
-        std::vector<double> piv((size_t)c->N * 9);
+        std::vector<double> piv(rows * 9);
         PINT_CUDA_CHECK(cudaMemcpyAsync(piv.data(), F.f9[levels - 1], piv.size() * sizeof(double),
                                         cudaMemcpyDeviceToHost, c->stream));
         PINT_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        for (int s = 0; s < c->N; ++s)
-            if (!(piv[(size_t)s * 9 + 4] > 0.0))
-                pint_throw(PINT_NOT_SPD, "non-positive pivot: operator is not SPD");
+        for (int s = 0; s < c->N; ++s) {
+            double pv = 0.0;
+            if (F.sep)
+                for (int r = 0; r < F.sep; ++r) pv += hsc[(size_t)s * F.sep + r] * piv[(size_t)r * 9 + 4];
+            else
+                pv = piv[(size_t)s * 9 + 4];
+            if (!(pv > 0.0)) pint_throw(PINT_NOT_SPD, "non-positive pivot: operator is not SPD");
+        }
         ensure_levels(c, F.m);
         if (!c->d_ft) c->d_ft = dalloc<double>(slab(c));
         if (c->lev_t.size() < (size_t)levels) c->lev_t.resize(levels, nullptr);

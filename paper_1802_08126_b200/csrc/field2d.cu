@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>
+#include <type_traits>
 
 #include "pint_device.cuh"
 #include "pint_internal.cuh"
@@ -39,15 +40,51 @@ namespace {
 constexpr int FX = 32, FY = 8, FG = PINT_FG;  // 32x8 tile, FG time planes per CTA (marching ops)
 constexpr int FT = 256;
 
-enum FieldMode : int { FM_A = 0, FM_H = 1, FM_9 = 2 };
+// FM_SA / FM_S9 (separable families, pint_field_separable): the operator of
+// set s is sum_r sc[s][r] T_r with R time-independent term tables T_r (compact
+// [R][3][n] on the fine level, [R][9][m_l^2] Galerkin rows below), so the
+// per-set coefficients are formed in registers from cache-resident tables
+// instead of being streamed from [sets][..] slabs.
+enum FieldMode : int { FM_A = 0, FM_H = 1, FM_9 = 2, FM_SA = 3, FM_S9 = 4 };
+constexpr int FSEP_MAX = PINT_FSEP_MAX;
 
 struct Src {
-    const double* f = nullptr;     // FM_A: compact [sets][3][n]; FM_9: [sets][9][n]
+    const double* f = nullptr;     // FM_A: compact [sets][3][n]; FM_9: [sets][9][n]; FM_S*: term tables
     size_t set_stride = 0;         // doubles between consecutive sets (0: shared by all)
-    const double* mass = nullptr;  // FM_H: constant mass stencil [9]
+    const double* mass = nullptr;  // FM_H: constant mass stencil [9] (device copy, unused by the kernels)
+    double massv[9] = {};          // FM_H: the same stencil by value (kernel-parameter constants: no
+                                   // load instructions; ncu showed the fine H~ residual LSU bound at 92 %)
     const double* mu = nullptr;    // FM_H: per-set weight mu_k
     double tau = 0.0;              // FM_H: tau_ref
+    const double* sc = nullptr;    // FM_S*: per-set term weights [sets][R]
+    int R = 0;                     // FM_S*: number of terms (<= FSEP_MAX)
+    size_t term_stride = 0;        // FM_S*: doubles between term tables
 };
+
+// term weights of set s in registers
+struct SepW {
+    double w[FSEP_MAX];
+    int R;
+    ptrdiff_t ts;
+};
+
+__device__ __forceinline__ SepW sep_load(const Src& S, int s) {
+    SepW W;
+    W.R = S.R;
+    W.ts = (ptrdiff_t)S.term_stride;
+#pragma unroll
+    for (int r = 0; r < FSEP_MAX; ++r) W.w[r] = r < S.R ? __ldg(S.sc + (size_t)s * S.R + r) : 0.0;
+    return W;
+}
+
+// sum_r w_r T_r[p]
+__device__ __forceinline__ double sep_at(const SepW& W, const double* p) {
+    double v = W.w[0] * __ldg(p);
+#pragma unroll
+    for (int r = 1; r < FSEP_MAX; ++r)
+        if (r < W.R) v = fma(W.w[r], __ldg(p + r * W.ts), v);
+    return v;
+}
 
 // coefficient k (CSR position SW,S,SE,W,C,E,NW,N,NE) of row (x, y) of set s;
 // only called when that neighbour exists
@@ -55,6 +92,18 @@ template <int MODE>
 __device__ __forceinline__ double coef(const Src& S, int s, int k, int m, int x, int y) {
     const size_t n = (size_t)m * m;
     const size_t i = (size_t)y * m + x;
+    if (MODE == FM_SA || MODE == FM_S9) {
+        const SepW W = sep_load(S, s);
+        if (MODE == FM_S9) return sep_at(W, S.f + (size_t)k * n + i);
+        switch (k) {
+            case 1: return sep_at(W, S.f + 2 * n + i - m);
+            case 3: return sep_at(W, S.f + n + i - 1);
+            case 4: return sep_at(W, S.f + i);
+            case 5: return sep_at(W, S.f + n + i);
+            case 7: return sep_at(W, S.f + 2 * n + i);
+            default: return 0.0;
+        }
+    }
     const double* f = S.f + (size_t)s * S.set_stride;
     if (MODE == FM_9) return __ldg(f + (size_t)k * n + i);
     double a;
@@ -68,14 +117,14 @@ __device__ __forceinline__ double coef(const Src& S, int s, int k, int m, int x,
     }
     if (MODE == FM_A) return a;
     // add_matrices(mu_k, M, 1.0, A_ref.scaled(tau_ref)) entry (schur.py:41-47, linalg.py:118-127)
-    return __ldg(S.mu + s) * __ldg(S.mass + k) + 1.0 * (S.tau * a);
+    return __ldg(S.mu + s) * S.massv[k] + 1.0 * (S.tau * a);
 }
 
 template <int MODE>
 __device__ __forceinline__ bool structural(int k) {
     // FM_A: only S, W, C, E, N can be non-zero (SW / NE are stored zeros);
     // FM_H: SE / NW are absent from both M and A
-    if (MODE == FM_A) return k == 1 || k == 3 || k == 4 || k == 5 || k == 7;
+    if (MODE == FM_A || MODE == FM_SA) return k == 1 || k == 3 || k == 4 || k == 5 || k == 7;
     if (MODE == FM_H) return k != 2 && k != 6;
     return true;
 }
@@ -91,9 +140,31 @@ __device__ __forceinline__ double frow(const Src& S, int s, const double* __rest
     const int i = y * m + x;
     const ptrdiff_t n = (ptrdiff_t)m * m;
     const bool w = x > 0, e = x < m - 1, so = y > 0, no = y < m - 1;
-    const double* f = S.f + (size_t)s * S.set_stride + i;  // centre entry of this row
     const double* vi = v + i;
     double r = 0.0;
+    if constexpr (MODE == FM_S9 || MODE == FM_SA) {
+        const SepW W = sep_load(S, s);
+        const double* f = S.f + i;
+        if constexpr (MODE == FM_S9) {
+            if (so && w) r = r + sep_at(W, f) * __ldg(vi - m - 1);
+            if (so) r = r + sep_at(W, f + n) * __ldg(vi - m);
+            if (so && e) r = r + sep_at(W, f + 2 * n) * __ldg(vi - m + 1);
+            if (w) r = r + sep_at(W, f + 3 * n) * __ldg(vi - 1);
+            r = r + sep_at(W, f + 4 * n) * __ldg(vi);
+            if (e) r = r + sep_at(W, f + 5 * n) * __ldg(vi + 1);
+            if (no && w) r = r + sep_at(W, f + 6 * n) * __ldg(vi + m - 1);
+            if (no) r = r + sep_at(W, f + 7 * n) * __ldg(vi + m);
+            if (no && e) r = r + sep_at(W, f + 8 * n) * __ldg(vi + m + 1);
+        } else {
+            if (so) r = r + sep_at(W, f + 2 * n - m) * __ldg(vi - m);
+            if (w) r = r + sep_at(W, f + n - 1) * __ldg(vi - 1);
+            r = r + sep_at(W, f) * __ldg(vi);
+            if (e) r = r + sep_at(W, f + n) * __ldg(vi + 1);
+            if (no) r = r + sep_at(W, f + 2 * n) * __ldg(vi + m);
+        }
+        return r;
+    }
+    const double* f = S.f + (size_t)s * S.set_stride + i;  // centre entry of this row
     if constexpr (MODE == FM_9) {
         if (so && w) r = r + __ldg(f) * __ldg(vi - m - 1);
         if (so) r = r + __ldg(f + n) * __ldg(vi - m);
@@ -123,8 +194,7 @@ __device__ __forceinline__ double frow(const Src& S, int s, const double* __rest
             // mu_k M + tau A_ref entry: add_matrices(mu_k, M, 1.0, A_ref.scaled(tau_ref))
             // (schur.py:41-47, linalg.py:118-127); SW / NE carry mass only
             const double mu = __ldg(S.mu + s), tau = S.tau;
-            const double* ms = S.mass;
-            auto hc = [&](int k, double a) { return mu * __ldg(ms + k) + 1.0 * (tau * a); };
+            auto hc = [&](int k, double a) { return mu * S.massv[k] + 1.0 * (tau * a); };
             if (so && w) r = r + hc(0, 0.0) * __ldg(vi - m - 1);
             if (so) r = r + hc(1, aS) * __ldg(vi - m);
             if (w) r = r + hc(3, aW) * __ldg(vi - 1);
@@ -172,7 +242,7 @@ __global__ void __launch_bounds__(FT)
 }
 
 // ---- time-global operators ---------------------------------------------------------
-template <int OP>
+template <int OP, int MODE>
 __global__ void __launch_bounds__(FX* FY)
     k_f_timeop(int m, int N, int qmin, int qmax, const double* __restrict__ mass, Src A,
                const double* __restrict__ ascale, const double* __restrict__ u,
@@ -190,7 +260,7 @@ __global__ void __launch_bounds__(FX* FY)
     for (int k = 0; k < 9; ++k) cm[k] = __ldg(mass + k);
     auto Mv = [&](const double* v, long long t) { return stencil9_global(cm, v + t * (long long)n, m, x, y); };
     auto Av = [&](const double* v, int t) {
-        return __ldg(ascale + t) * frow<FM_A>(A, t, v + (size_t)t * n, m, x, y);
+        return __ldg(ascale + t) * frow<MODE>(A, t, v + (size_t)t * n, m, x, y);
     };
     if (OP == OP_ABD) {
         for (int t = n0; t < n1; ++t) out[t * n + i] = Av(u, t);
@@ -324,17 +394,16 @@ __global__ void __launch_bounds__(FT)
 // level above the 1x1 coarsest grid e = b_c / a_c (spatial.py:149-150, 157).
 // Per axis an odd coordinate has one term (weight 1), an even one the two
 // neighbours (weight 1/2 each, those inside the coarse grid).
-template <bool DIRECT>
+template <bool DIRECT, int MODE>
 __global__ void __launch_bounds__(FT)
-    k_f_prolong(int m, int mc, const double* __restrict__ ac9, size_t ac_stride,
-                const double* __restrict__ ec, double* __restrict__ x) {
+    k_f_prolong(int m, int mc, Src Ac, const double* __restrict__ ec, double* __restrict__ x) {
     // DIRECT is a template parameter: a runtime flag lets the compiler
     // evaluate e / 1.0 speculatively for every term
     const int xx = blockIdx.x * GX + threadIdx.x, y = blockIdx.y * GY + threadIdx.y;
     if (xx >= m || y >= m) return;
     const int t = blockIdx.z;
     const int nc = mc * mc;
-    const double ac = DIRECT ? __ldg(ac9 + (size_t)t * ac_stride + 4 * (size_t)nc) : 1.0;
+    const double ac = DIRECT ? coef<MODE>(Ac, t, 4, mc, 0, 0) : 1.0;  // DIRECT: mc == 1
     const bool yo = y & 1, xo = xx & 1;
     const int ja = (y - 1) >> 1, ia = (xx - 1) >> 1;      // first term of each axis
     const bool va = ja >= 0, vb = !yo && ja + 1 < mc;      // rows ja, ja + 1
@@ -497,13 +566,19 @@ bool epi_dot(int epi) {
 
 Src fine_src(pint_ctx* c, int which) {
     Src S;
-    if (which == PINT_MG_ATILDE) {
+    if (which == PINT_MG_ATILDE && c->fsep_R) {
+        S.f = c->d_fsep;
+        S.sc = c->d_fsc;
+        S.R = c->fsep_R;
+        S.term_stride = 3 * (size_t)c->n;
+    } else if (which == PINT_MG_ATILDE) {
         S.f = c->d_fa;
         S.set_stride = 3 * (size_t)c->n;
     } else {
         S.f = c->d_fref;
         S.set_stride = 0;
         S.mass = c->d_mass;
+        for (int k = 0; k < 9; ++k) S.massv[k] = c->h_mass[k];
         S.mu = c->fmg[which].d_mu;
         S.tau = c->tau_ref;
     }
@@ -513,16 +588,23 @@ Src fine_src(pint_ctx* c, int which) {
 Src coarse_src(const FieldMg& F, int l) {
     Src S;
     S.f = F.f9[l];
-    S.set_stride = 9 * (size_t)F.m[l] * F.m[l];
+    if (F.sep) {  // R term tables [R][9][m_l^2], weights [sets][R]
+        S.sc = F.d_sc;
+        S.R = F.sep;
+        S.term_stride = 9 * (size_t)F.m[l] * F.m[l];
+    } else {
+        S.set_stride = 9 * (size_t)F.m[l] * F.m[l];
+    }
     return S;
 }
 
 }  // namespace
 
-void field_assemble(pint_ctx* c, int step0, int count, const double* w_dev) {
+void field_assemble(pint_ctx* c, int step0, int count, const double* w_dev, double* dst) {
     const int cells = c->m + 1;
+    if (!dst) dst = c->d_fa;
     k_f_assemble<<<pt_grid((size_t)c->n, count), FT, 0, c->stream>>>(
-        cells, w_dev, c->d_fa + (size_t)step0 * 3 * c->n);
+        cells, w_dev, dst + (size_t)step0 * 3 * c->n);
     PINT_LAUNCHED(c);
     PINT_CUDA_CHECK(cudaGetLastError());
 }
@@ -533,26 +615,29 @@ void launch_timeop_field(pint_ctx* c, int op, const double* u, const double* p, 
     static const int kid[] = {K_TIMEOP_K, K_TIMEOP_KT, K_TIMEOP_ABD, K_TIMEOP_R1, K_TIMEOP_Z};
     static const int passes[] = {2, 2, 5, 7, 7};   // + 3 compact coefficient fields
     ProfScope prof(c, kid[op], 8.0 * passes[op] * (double)c->N * c->n);
-    Src A;
-    A.f = c->d_fa;
-    A.set_stride = 3 * (size_t)c->n;
+    const Src A = fine_src(c, PINT_MG_ATILDE);
     const dim3 g = tile_grid(c->m, c->N), b(FX, FY);
     const int qmin = c->has_prev ? -1 : 0, qmax = c->has_next ? c->N : c->N - 1;
-    switch (op) {
-        case OP_ABD:
-            k_f_timeop<OP_ABD><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
-                                                       c->d_ascale, u, p, f, out);
-            break;
-        case OP_R1:
-            k_f_timeop<OP_R1><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
-                                                      c->d_ascale, u, p, f, out);
-            break;
-        case OP_Z:
-            k_f_timeop<OP_Z><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
-                                                     c->d_ascale, u, p, f, out);
-            break;
-        default: pint_throw(PINT_INPUT, "unknown time operator");
-    }
+    auto run = [&](auto mode_tag) {
+        constexpr int MODE = decltype(mode_tag)::value;
+        switch (op) {
+            case OP_ABD:
+                k_f_timeop<OP_ABD, MODE><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
+                                                                 c->d_ascale, u, p, f, out);
+                break;
+            case OP_R1:
+                k_f_timeop<OP_R1, MODE><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
+                                                                c->d_ascale, u, p, f, out);
+                break;
+            case OP_Z:
+                k_f_timeop<OP_Z, MODE><<<g, b, 0, c->stream>>>(c->m, c->N, qmin, qmax, c->d_mass, A,
+                                                               c->d_ascale, u, p, f, out);
+                break;
+            default: pint_throw(PINT_INPUT, "unknown time operator");
+        }
+    };
+    if (c->fsep_R) run(std::integral_constant<int, FM_SA>{});
+    else run(std::integral_constant<int, FM_A>{});
     PINT_LAUNCHED(c);
     PINT_CUDA_CHECK(cudaGetLastError());
 }
@@ -568,11 +653,58 @@ void launch_aref_field(pint_ctx* c, const double* in, double* out, int count) {
     PINT_CUDA_CHECK(cudaGetLastError());
 }
 
+// out[3][n] = sum_r sc[step][r] T_r: the compact field of one step of a
+// separable family (A_ref = A_step, pint_field_aref)
+__global__ void __launch_bounds__(FT)
+    k_f_sep_combine(size_t cnt, Src S, int step, double* __restrict__ out) {
+    const size_t g = (size_t)blockIdx.x * FT + threadIdx.x;
+    if (g >= cnt) return;
+    out[g] = sep_at(sep_load(S, step), S.f + g);
+}
+
+void field_sep_step(pint_ctx* c, int step, double* out) {
+    const Src S = fine_src(c, PINT_MG_ATILDE);
+    const size_t cnt = 3 * (size_t)c->n;
+    k_f_sep_combine<<<(unsigned)((cnt + FT - 1) / FT), FT, 0, c->stream>>>(cnt, S, step, out);
+    PINT_LAUNCHED(c);
+    PINT_CUDA_CHECK(cudaGetLastError());
+}
+
 void field_galerkin(pint_ctx* c, int which) {
     FieldMg& F = c->fmg[which];
     for (int l = 0; l + 1 < F.levels; ++l) {
         const int m = F.m[l], mc = F.m[l + 1];
-        const dim3 g = pt_grid((size_t)mc * mc, c->N);
+        const size_t nc = (size_t)mc * mc;
+        if (F.sep) {
+            // Galerkin rows of every TERM (the product is linear in the operator)
+            if (l == 0 && which == PINT_MG_ATILDE) {
+                Src S;  // the R term fields as R plain compact sets
+                S.f = c->d_fsep;
+                S.set_stride = 3 * (size_t)c->n;
+                k_f_galerkin<FM_A><<<pt_grid(nc, F.sep), FT, 0, c->stream>>>(m, mc, S, F.f9[1]);
+            } else if (l == 0) {
+                // H_k = mu_k M + tau_ref A_ref: term 0 = M (mu = 1, tau = 0), term 1 = A_ref
+                Src S;
+                S.f = c->d_fref;
+                S.mass = c->d_mass;
+                for (int k = 0; k < 9; ++k) S.massv[k] = c->h_mass[k];
+                S.mu = c->d_unit;  // {1.0, 0.0}
+                S.tau = 0.0;
+                k_f_galerkin<FM_H><<<pt_grid(nc, 1), FT, 0, c->stream>>>(m, mc, S, F.f9[1]);
+                S.mu = c->d_unit + 1;
+                S.tau = 1.0;
+                k_f_galerkin<FM_H><<<pt_grid(nc, 1), FT, 0, c->stream>>>(m, mc, S, F.f9[1] + 9 * nc);
+            } else {
+                Src S;
+                S.f = F.f9[l];
+                S.set_stride = 9 * (size_t)m * m;
+                k_f_galerkin<FM_9><<<pt_grid(nc, F.sep), FT, 0, c->stream>>>(m, mc, S, F.f9[l + 1]);
+            }
+            PINT_LAUNCHED(c);
+            PINT_CUDA_CHECK(cudaGetLastError());
+            continue;
+        }
+        const dim3 g = pt_grid(nc, c->N);
         if (l == 0) {
             const Src S = fine_src(c, which);
             if (which == PINT_MG_ATILDE)
@@ -616,12 +748,13 @@ void post_level(pint_ctx* c, const Src& S, const FieldMg& F, int l, int count, c
     const double* ec = direct ? c->lev_b[l + 1] : c->lev_x[l + 1];
     ProfScope prof(c, top ? K_MG_POST_FINE : K_MG_POST_COARSE,
                    8.0 * count * (4.0 * m * m + (double)mc * mc));
-    if (direct)
-        k_f_prolong<true><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(
-            m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, ec, x);
+    const Src Ac = coarse_src(F, l + 1);
+    if (direct && F.sep)
+        k_f_prolong<true, FM_S9><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(m, mc, Ac, ec, x);
+    else if (direct)
+        k_f_prolong<true, FM_9><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(m, mc, Ac, ec, x);
     else
-        k_f_prolong<false><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(
-            m, mc, F.f9[l + 1], 9 * (size_t)mc * mc, ec, x);
+        k_f_prolong<false, FM_9><<<grid2(m, count), dim3(GX, GY), 0, c->stream>>>(m, mc, Ac, ec, x);
     FSmooth P{};
     P.m = m;
     P.b = b;
@@ -674,10 +807,15 @@ void vcycle_field(pint_ctx* c, int which, int count, const double* b, double* ou
         double* x0 = l == 0 ? c->d_ft : c->lev_t[l];
         double* rw = l == 0 ? c->d_t3a : c->lev_x[l];
         if (l == 0) {
-            if (which == PINT_MG_ATILDE)
+            if (which == PINT_MG_ATILDE && F.sep)
+                pre_level<FM_SA>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true, rw);
+            else if (which == PINT_MG_ATILDE)
                 pre_level<FM_A>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true, rw);
             else
                 pre_level<FM_H>(c, S0, m, mc, count, F.damping, bl, x0, c->lev_b[1], true, rw);
+        } else if (F.sep) {
+            pre_level<FM_S9>(c, coarse_src(F, l), m, mc, count, F.damping, bl, x0, c->lev_b[l + 1],
+                             false, rw);
         } else {
             pre_level<FM_9>(c, coarse_src(F, l), m, mc, count, F.damping, bl, x0, c->lev_b[l + 1],
                             false, rw);
@@ -688,10 +826,15 @@ void vcycle_field(pint_ctx* c, int which, int count, const double* b, double* ou
     for (int l = L - 2; l >= 0; --l) {
         double* x = l == 0 ? c->d_ft : c->lev_t[l];
         if (l == 0) {
-            if (which == PINT_MG_ATILDE)
+            if (which == PINT_MG_ATILDE && F.sep)
+                post_level<FM_SA>(c, S0, F, 0, count, b, x, out, epi, scale, pin, aux, acc_slot);
+            else if (which == PINT_MG_ATILDE)
                 post_level<FM_A>(c, S0, F, 0, count, b, x, out, epi, scale, pin, aux, acc_slot);
             else
                 post_level<FM_H>(c, S0, F, 0, count, b, x, out, epi, scale, pin, aux, acc_slot);
+        } else if (F.sep) {
+            post_level<FM_S9>(c, coarse_src(F, l), F, l, count, c->lev_b[l], x, c->lev_x[l],
+                              EPI_PLAIN, 1.0, nullptr, nullptr, 0);
         } else {
             post_level<FM_9>(c, coarse_src(F, l), F, l, count, c->lev_b[l], x, c->lev_x[l],
                              EPI_PLAIN, 1.0, nullptr, nullptr, 0);

@@ -22,6 +22,7 @@
 
 #define PINT_S2 9   // 2D stencil size
 #define PINT_TW 10  // table row: 9 coefficients + dinv
+#define PINT_FSEP_MAX 3  // terms of a separable stiffness family (pint_field_separable)
 #define PINT_EX_BUFS 11  // work buffers of the diagnostic exact solves (exact_solve.cu)
 
 struct PintFail {
@@ -63,8 +64,11 @@ struct FieldMg {
     int levels = 0;
     std::vector<int> m;
     double damping = 0.0;
-    std::vector<double*> f9;  // [l] device [N][9][m_l^2], l >= 1 (f9[0] unused)
+    std::vector<double*> f9;  // [l] device [N][9][m_l^2], l >= 1 (f9[0] unused); separable: [sep][9][m_l^2]
     double* d_mu = nullptr;   // H~: per-mode weights [N]
+    int sep = 0;              // separable form: number of term tables (0: per-set rows)
+    double* d_sc = nullptr;   // separable: term weights [N][sep] (A~: the family's; H~: (mu_k, tau_ref), owned)
+    bool own_sc = false;
     bool ready = false;
 };
 
@@ -138,6 +142,13 @@ struct pint_ctx {
     bool field = false;
     double* d_fa = nullptr;      // [N][3][n] compact fine A_n (centre, east, north)
     double* d_fref = nullptr;    // [3][n] compact A_ref
+    // separable family A_n = sum_r sc[n][r] A(w_r) (pint_field_separable): the
+    // R compact term fields and the weights replace d_fa
+    int fsep_R = 0;
+    double* d_fsep = nullptr;    // [R][3][n]
+    double* d_fsc = nullptr;     // [N][R]
+    std::vector<double> h_fsc;
+    double* d_unit = nullptr;    // {1.0, 0.0}
     bool fref_ready = false;
     FieldMg fmg[2];
     double* d_ft = nullptr;      // [N][n] fine-level V-cycle work slab
@@ -269,7 +280,8 @@ void vcycle3(pint_ctx* c, int which, int count, const double* b, double* out, in
              double scale, const double* pin, const double* aux, int acc_slot);
 
 // field mode, 2D per-point stiffness (field2d.cu)
-void field_assemble(pint_ctx* c, int step0, int count, const double* w_dev);
+void field_assemble(pint_ctx* c, int step0, int count, const double* w_dev, double* dst = nullptr);
+void field_sep_step(pint_ctx* c, int step, double* out);  // out[3][n] = compact field of one step of a separable family
 void field_galerkin(pint_ctx* c, int which);
 void launch_timeop_field(pint_ctx* c, int op, const double* u, const double* p, const double* f,
                          double* out);

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CFG))
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--N", type=int, default=0)
+    ap.add_argument("--separable", action="store_true", help="c4: separable family (pint_field_separable)")
     args = ap.parse_args()
     import paper_1802_08126_b200 as pg
 
@@ -38,7 +39,7 @@ def main():
     if args.config.startswith("c4"):
         load = np.random.default_rng(1).standard_normal((N, n))
         spec = pg.make_weighted_problem(cells, grid, pg.c4_cell_weights(cells, grid, seed=0),
-                                        load, np.zeros(n), alpha=1.0)
+                                        load, np.zeros(n), alpha=1.0, separable=args.separable)
     else:
         rng = np.random.default_rng(0)
         load = rng.standard_normal((N, n))
