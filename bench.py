@@ -423,6 +423,9 @@ PART_CONFIGS = {
     # BASELINE configs[2] (strong scaling 1/2/4/8) and configs[4] (weak: N = 1024 G)
     "c3": dict(space="3d", cells=64, N=512, T=1.0, weak=False),
     "c5": dict(space="3d", cells=64, N=1024, T=1.0, weak=True),
+    # BASELINE config 4 ("time-sharded across 8 B200"): per-step coefficient
+    # fields, every rank assembles those of its own steps
+    "c4": dict(space="2d", cells=512, N=4096, T=2.0, weak=False),
 }
 
 
@@ -435,6 +438,8 @@ def _part_problem(name, world, rank):
 
     c = PART_CONFIGS[name]
     N = c["N"] * (world if c["weak"] else 1)
+    if name == "c4" and os.environ.get("PINT_BENCH_C4_N"):
+        N = int(os.environ["PINT_BENCH_C4_N"])  # one-GPU validation of this path (163 GB at N = 4096)
     T = c["T"] * N / c["N"] if c["weak"] else c["T"]
     grid = pg.build_time_grid("uniform", N, T)
     n = (c["cells"] - 1) ** (3 if c["space"] == "3d" else 2)
@@ -445,10 +450,15 @@ def _part_problem(name, world, rank):
         mine = load[sl]
     else:
         # only this rank's slab exists on the host (c5 at G = 8 is 16 GB in all)
-        mine = np.stack([np.random.default_rng((0, t)).standard_normal(n)
+        mine = np.stack([np.random.default_rng((1 if name == "c4" else 0, t)).standard_normal(n)
                          for t in range(sl.start, sl.stop)])
         load = np.broadcast_to(np.zeros(1), (N, n))
-    spec = pg.problem_from_arrays(c["space"], c["cells"], grid, load, np.zeros(n), alpha=1.0)
+    if name == "c4":
+        spec = pg.make_weighted_problem(c["cells"], grid,
+                                        pg.c4_cell_weights(c["cells"], grid, seed=0), load,
+                                        np.zeros(n), alpha=1.0)
+    else:
+        spec = pg.problem_from_arrays(c["space"], c["cells"], grid, load, np.zeros(n), alpha=1.0)
     f_loc = np.ascontiguousarray(spec.grid.steps[sl, None] * mine)  # fold_rhs, u0 = 0
     return spec, f_loc, part
 
@@ -517,7 +527,9 @@ def run_gpu_partitioned(args, world, rank, local):
     """N > 1 GPUs (or --partitioned): the headline c2 time axis split across
     ranks (strong scaling, the same workload as the N = 1 line so the driver's
     scaling efficiency compares like with like), plus BASELINE's own
-    multi-GPU configs c3 (strong) and c5 (weak, N = 1024 G) as other_configs."""
+    multi-GPU configs c3 (strong), c5 (weak, N = 1024 G) and c4 (strong, field
+    mode; per-iteration time only: it diverges at omega = 0.9 in the reference
+    algorithm too) as other_configs."""
     import torch
     import torch.distributed as dist
 
@@ -530,7 +542,9 @@ def run_gpu_partitioned(args, world, rank, local):
     head = measure_partitioned("c2", world, rank, local, steps, warm, e2e=True)
     others = {}
     if not args.no_other:
-        for name in ("c3", "c5"):
+        for name in ("c3", "c5", "c4"):
+            if name == "c4" and world == 1 and not os.environ.get("PINT_BENCH_C4_N"):
+                continue  # does not fit one GPU next to the driver's own slabs
             try:
                 others[name] = measure_partitioned(name, world, rank, local, max(2, steps // 3),
                                                    3)
@@ -659,6 +673,8 @@ def run_gpu(args):
         gc.collect()
         torch.cuda.empty_cache()
         for name in ("c3", "c5", "c4"):
+            if name == "c4" and world == 1 and not os.environ.get("PINT_BENCH_C4_N"):
+                continue  # does not fit one GPU next to the driver's own slabs
             try:
                 # c4 needs ~10^3 iterations: its solve gets a wall budget
                 others[name] = measure_config(name, converge=not args.no_converge,

@@ -334,9 +334,11 @@ def dist_uzawa_solve(ops: LocalOps, comm, N: int, n: int, f_local: torch.Tensor,
 
 
 class GpuLocalOps(LocalOps):
-    """libpint building blocks for this rank's steps / modes (CUDA tensors);
-    2D and 3D problems with stencil operators (the A(x,t) field mode is not
-    partitioned)."""
+    """libpint building blocks for this rank's steps / modes (CUDA tensors):
+    2D and 3D problems with stencil operators, and 2D per-point stiffness
+    fields (BASELINE config 4: every rank holds the coefficient fields of
+    its own steps, or the term tables of a separable family, the A_ref field
+    and the H~ hierarchies of its own modes)."""
 
     def __init__(self, spec, hierarchy, part: Partition, rank: int, device=None,
                  damping: float | None = None):
@@ -344,9 +346,9 @@ class GpuLocalOps(LocalOps):
         from ._native import MG_ATILDE, MG_HTILDE, Context
         from .schur import frequency_weights
 
+        from .linalg import grid_fields
+
         hp = HostProblem(spec)
-        if hp.field is not None:
-            raise InputError("per-point stiffness fields are not time-partitioned")
         if damping is None:
             damping = hp.default_damping()
         sl = part.slice(rank)
@@ -371,17 +373,46 @@ class GpuLocalOps(LocalOps):
         ctx.call("pint_set_partition", self.n0, self.N, int(self.n0 > 0),
                  int(self.n0 + self.nl < self.N))
         lm = np.asarray(hierarchy.level_m, dtype=np.int32)
+        mu = frequency_weights(self.N)[sl]
+        if hp.field is not None:
+            self._upload_fields(hp, spec, sl, grid_fields)
+            ctx.call("pint_mg_set_field", MG_ATILDE, len(lm), lm.ctypes.data, float(damping), None)
+            mu = np.ascontiguousarray(mu, dtype=np.float64)
+            ctx.call("pint_mg_set_field", MG_HTILDE, len(lm), lm.ctypes.data, float(damping),
+                     mu.ctypes.data)
+            return
         tab_a, sid_a = hp.atilde_tables(hierarchy, damping)
         tab_a = np.ascontiguousarray(tab_a)
         sid_a = np.ascontiguousarray(sid_a[sl])
         ctx.call("pint_mg_set", MG_ATILDE, len(lm), lm.ctypes.data, tab_a.shape[1],
                  tab_a.ctypes.data, sid_a.ctypes.data)
-        mu = frequency_weights(self.N)[sl]
         tab_h, _ = hp.htilde_tables(hierarchy, damping, mu)
         tab_h = np.ascontiguousarray(tab_h)
         sid_h = np.arange(self.nl, dtype=np.int32)
         ctx.call("pint_mg_set", MG_HTILDE, len(lm), lm.ctypes.data, self.nl,
                  tab_h.ctypes.data, sid_h.ctypes.data)
+
+    _FIELD_CHUNK = 32
+
+    def _upload_fields(self, hp, spec, sl, grid_fields):
+        """Coefficient fields of the local steps (GpuProblem._upload_fields on
+        the slice) and the A_ref field, which every rank needs in full."""
+        ctx, fam = self.ctx, spec.stiffness
+        if hp.field == "family" and fam.terms is not None:
+            a, c = fam.terms
+            c = np.ascontiguousarray(c[sl])
+            ctx.call("pint_field_separable", int(a.shape[0]), a.ctypes.data, c.ctypes.data)
+        elif hp.field == "family":
+            for k0 in range(0, self.nl, self._FIELD_CHUNK):
+                k1 = min(self.nl, k0 + self._FIELD_CHUNK)
+                w = np.ascontiguousarray(fam.cell_weights(self.n0 + k0, self.n0 + k1))
+                ctx.call("pint_field_assemble", k0, k1 - k0, w.ctypes.data)
+        else:
+            for k in range(self.nl):
+                f = np.ascontiguousarray(grid_fields(spec.stiffness[self.n0 + k], hp.m))
+                ctx.call("pint_field_set", k, 1, f.ctypes.data)
+        f = np.ascontiguousarray(grid_fields(spec.a_ref, hp.m))
+        ctx.call("pint_field_aref", 0, f.ctypes.data)
 
     def r1(self, u_ext, p_ext, f, out):
         self.ctx.call("pint_residual_r1", u_ext[1].data_ptr(), p_ext[1].data_ptr(),
