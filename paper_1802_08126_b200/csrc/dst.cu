@@ -27,6 +27,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "band.cuh"
 #include "pint_internal.cuh"
 
@@ -356,6 +358,54 @@ __device__ __forceinline__ void dft(double2* x) {
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
+// The 15 twiddles W^{j s}, s = 1..15, of a radix-16 butterfly from the four
+// table entries s = 1, 2, 4, 8 (binary composition, at most three complex
+// products deep).  ncu (profiles/r2_dst_bigN_traffic.txt): the streamed tile
+// (cp.async.ca) evicts the tables from what L1 the shared-memory carve-out
+// leaves, so every table read is an L2 round trip -- 3.6x the data's own L2
+// sectors at N = 4096; computing 11 of the 15 costs 44 fp64 instructions per
+// butterfly on a pipe that is 25 % busy.
+//   t: table [s-1][j] with row stride B (entries), already offset by j
+__device__ __forceinline__ void twiddle16(const double2* __restrict__ t, int B, double2* w) {
+    w[1] = __ldg(t);
+    w[2] = __ldg(t + B);
+    w[4] = __ldg(t + 3 * B);
+    w[8] = __ldg(t + 7 * B);
+    w[3] = cmul(w[1], w[2]);
+    w[5] = cmul(w[4], w[1]);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
+    w[9] = cmul(w[8], w[1]);
+    w[10] = cmul(w[8], w[2]);
+    w[11] = cmul(w[8], w[3]);
+    w[12] = cmul(w[8], w[4]);
+    w[13] = cmul(w[8], w[5]);
+    w[14] = cmul(w[8], w[6]);
+    w[15] = cmul(w[8], w[7]);
+}
+
+// (cos, sin)(pi s / 32), s = 0..15: q_{j + s N/16} = q_j * this  (tq[k] = (cos, sin)(pi k / 2N))
+__device__ __forceinline__ double2 rot32(int s) {
+    constexpr double c[16][2] = {
+        {1.0, 0.0},
+        {0.995184726672196886245, 0.0980171403295606019942},
+        {0.980785280403230449126, 0.195090322016128267848},
+        {0.956940335732208864936, 0.290284677254462367636},
+        {0.923879532511286756128, 0.382683432365089771728},
+        {0.881921264348355029713, 0.471396736825997648556},
+        {0.831469612302545237079, 0.555570233019602224743},
+        {0.773010453362736960811, 0.634393284163645498215},
+        {0.707106781186547524401, 0.707106781186547524401},
+        {0.634393284163645498215, 0.773010453362736960811},
+        {0.555570233019602224743, 0.831469612302545237079},
+        {0.471396736825997648556, 0.881921264348355029713},
+        {0.382683432365089771728, 0.923879532511286756128},
+        {0.290284677254462367636, 0.956940335732208864936},
+        {0.195090322016128267848, 0.980785280403230449126},
+        {0.0980171403295606019942, 0.995184726672196886245}};
+    return make_double2(c[s][0], c[s][1]);
+}
+
 // radix schedule: pass 1 radix 16, final radix 4, middle passes in between
 //   2^8: 16.4.4  2^9: 16.8.4  2^10: 16.16.4  2^11: 16.8.4.4  2^12: 16.16.4.4  2^13: 16.16.8.4
 __host__ __device__ constexpr int sched_np(int lg) { return lg <= 10 ? 3 : 4; }
@@ -505,8 +555,9 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
             // j > 0: k' = (B - j) + (15 - s) B;  j = 0: k' = (16 - s) B mod N
             const int jp = j == 0 ? 0 : B - j;
             const double2* pp = buf + ((jp << lgP) + pr);
-            const double2* q = a.tq + j;
-            const double2* qq = a.tq + jp;
+            // q at k = j + s B and k' = jp + sp B from q_j, q_jp and the constants
+            // (cos, sin)(pi s / 32): 2 table reads instead of 32
+            const double2 qj = __ldg(a.tq + j), qjp = __ldg(a.tq + jp);
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 double2 zk = p[(s << lgB) << lgP];
@@ -516,7 +567,10 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
                     zk = make_double2(zk.x * a.in_last, zk.y * a.in_last);
                     zp = zk;
                 }
-                const double2 qk = __ldg(q + (s << lgB)), qp = __ldg(qq + (sp << lgB));
+                const double2 qk = s == 0 ? qj : cmul(qj, rot32(s));
+                // j > 0: sp = 15 - s is a compile-time index; j == 0: (16 - s) & 15
+                const double2 qp0 = cmul(qjp, rot32((16 - s) & 15)), qp1 = cmul(qjp, rot32(15 - s));
+                const double2 qp = j == 0 ? (s == 0 ? qjp : qp0) : qp1;
                 const double2 u1 = cadd(cmul(make_double2(qk.x, -qk.y), zk), cmul(qp, zp));
                 x[s] = make_double2(0.5 * u1.x, 0.5 * u1.y);
             }
@@ -528,9 +582,10 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
 #pragma unroll
             for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = x[s];
         } else {
-            const double2* w = a.twp[0] + j;  // [s-1][j], j < N/16
+            double2 w[16];
+            twiddle16(a.twp[0] + j, B, w);  // [s-1][j], j < N/16
 #pragma unroll
-            for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + ((s - 1) << lgB)));
+            for (int s = 1; s < 16; ++s) p[(s << lgB) << lgP] = cmul(x[s], w[s]);
         }
     }
     __syncthreads();
@@ -585,8 +640,9 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
             load_group(freq_group<LG>(u == 0 ? N / 8 : Q4 - u), pr, y[i]);
         }
         __syncthreads();
-        auto emit = [&](int m, int pr, double2 C, double2 D) {
-            const double2 q = __ldg(a.tq + m);
+        // q_m = (cos, sin)(pi m / 2N) of m = r + s N/4 is q_r rotated by pi s / 8
+        // (rot32(4 s)): one table read per group instead of four
+        auto emit = [&](int m, int pr, double2 C, double2 D, double2 q) {
             const double va = 0.5 * (q.x * (C.x + D.x) + q.y * (C.y - D.y));
             const double vb = 0.5 * (q.x * (C.y + D.y) - q.y * (C.x - D.x));
             buf[(swz(N - 1 - m) << lgP) + pr] = make_double2(va, vb);
@@ -597,19 +653,21 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
             const int pr = item & (P - 1), u = item >> lgP;
             if (u == 0) {
                 // self-partnered groups r = 0 (N-k = (4-s) N/4) and r = N/8 (N-k = N/8 + (3-s) N/4)
-                emit(0, pr, x[i][0], x[i][0]);
-                emit(Q4, pr, x[i][1], x[i][3]);
-                emit(2 * Q4, pr, x[i][2], x[i][2]);
-                emit(3 * Q4, pr, x[i][3], x[i][1]);
+                emit(0, pr, x[i][0], x[i][0], rot32(0));
+                emit(Q4, pr, x[i][1], x[i][3], rot32(4));
+                emit(2 * Q4, pr, x[i][2], x[i][2], rot32(8));
+                emit(3 * Q4, pr, x[i][3], x[i][1], rot32(12));
 #pragma unroll
-                for (int s = 0; s < 4; ++s) emit(N / 8 + s * Q4, pr, y[i][s], y[i][3 - s]);
+                for (int s = 0; s < 4; ++s)
+                    emit(N / 8 + s * Q4, pr, y[i][s], y[i][3 - s], rot32(2 + 4 * s));
             } else {
                 // k = r + s N/4  <->  N - k = rp + (3 - s) N/4
                 const int r = u, rp = Q4 - u;
+                const double2 qr = __ldg(a.tq + r), qrp = __ldg(a.tq + rp);
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {
-                    emit(r + s * Q4, pr, x[i][s], y[i][3 - s]);
-                    emit(rp + s * Q4, pr, y[i][s], x[i][3 - s]);
+                    emit(r + s * Q4, pr, x[i][s], y[i][3 - s], s == 0 ? qr : cmul(qr, rot32(4 * s)));
+                    emit(rp + s * Q4, pr, y[i][s], x[i][3 - s], s == 0 ? qrp : cmul(qrp, rot32(4 * s)));
                 }
             }
         }
@@ -638,6 +696,236 @@ __global__ void __launch_bounds__(reg_threads<LG, P>(), reg_threads<LG, P>() >= 
 #pragma unroll
             for (int i = 0; i < LB; ++i) {
                 const int row = row0 + (i0 + i) * DR;
+                double v = alpha * sp[(i0 + i) * sstep];
+                if (row == N - 1) v *= a.out_last;
+                out[(i0 + i) * step] = basep ? bv[i] + v : v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster transform for N = 2^11 .. 2^13 (config 4's time axis; the GLOBAL
+// time axis of the time-sharded configs): the N x 8-column tile no longer fits
+// one CTA's shared memory (k_dst_reg falls back to 4- and 2-column tiles,
+// 32- / 16-byte row segments, one CTA per SM: 1.4 / 1.1 TB/s), so a thread-block
+// cluster of CL = N / 1024 CTAs holds it in distributed shared memory, 1024
+// positions x 4 pairs (64 KB) per CTA -- the shape of the N = 1024 kernel,
+// several CTAs per SM.  The algebra, radix schedule and tables are
+// k_dst_reg's.  Who holds what:
+//   staging   CTA q stages the inputs of ITS pass-1 butterflies j in
+//             [q B/CL, (q+1) B/CL), B = N/16: position s B + j at local s B/CL + jj;
+//   pass 1    reads local (S: the Hermitian partner from the CTA that staged
+//             it, a DSMEM read), cluster barrier, DFT-16, twiddle, output s of
+//             butterfly j to its HOME: position p lives in CTA p / (N/CL)
+//             (DSMEM writes), cluster barrier;
+//   middle    sub-blocks of length N/16 are whole inside a CTA: local;
+//   final     radix-4 groups local; S^T reads the partner group (k <-> N-k)
+//             from its home CTA; cluster barrier; results to the home of their
+//             OUTPUT ROW (CTA row / (N/CL)); cluster barrier;
+//   store     every CTA writes its N/CL consecutive output rows.
+// Five cluster barriers per tile; about 2.5 tile volumes cross DSMEM.
+// ---------------------------------------------------------------------------
+namespace cgx = cooperative_groups;
+
+template <int KIND, int LG, int P, int CL>
+__global__ void __launch_bounds__((P << (LG - 4)) / CL, 2) k_dst_cl(DstArgs a) {
+    extern __shared__ double2 buf[];
+    using S = Sched<LG>;
+    constexpr int N = 1 << LG, lgCL = ilog2(CL), lgNL = LG - lgCL, NL = 1 << lgNL;
+    constexpr int NT = (P << (LG - 4)) >> lgCL;
+    constexpr int W = 2 * P, lgP = ilog2(P), lgW = lgP + 1;
+    constexpr int lgB = LG - 4, B = 1 << lgB, lgBL = lgB - lgCL, BL = 1 << lgBL;
+    constexpr int Q4 = N / 4, GL = NL / 4;   // radix-4 groups: all / per CTA
+    static_assert(CL * (16 / CL) == 16 && BL >= 1, "cluster size divides the radix-16 sub-blocks");
+    cgx::cluster_group cluster = cgx::this_cluster();
+    const int q = (int)cluster.block_rank();
+    const int tid = threadIdx.x, n = a.n;
+    const long long c0 = (long long)(blockIdx.x >> lgCL) * W;
+    const int ncol = (int)min((long long)W, (long long)n - c0);
+    double* sd = reinterpret_cast<double*>(buf);
+    auto rbuf = [&](int rank) -> double2* { return cluster.map_shared_rank(buf, rank); };
+    constexpr int DR = NT >> lgW;  // local positions / rows per sweep
+    const int cc = tid & (W - 1), lrow0 = tid >> lgW;
+    const bool cok = cc < ncol;
+    // ---- stage: the inputs of this CTA's butterflies (raw values; signs in pass 1) ----
+    {
+        const double* src0 = a.in + c0 + (cok ? cc : 0);
+        double* dst = sd + ((lrow0 << lgP) + (cc >> 1)) * 2 + (cc & 1);
+        // lp = lrow0 + i DR with lrow0 < DR <= BL: the sub-block s = lp / BL and the
+        // offset inside it are compile-time functions of i, so unrolled the loop
+        // is one multiply-add per copy
+        static_assert(DR <= BL && BL % DR == 0, "staging sweeps stay inside a sub-block");
+        const long long nn = cok ? n : 0;
+        const int pbase = q * BL + lrow0;
+#pragma unroll
+        for (int i = 0; i < NL / DR; ++i) {
+            constexpr int per_s = BL / DR;
+            const int s_ = i / per_s, off = (i % per_s) * DR;
+            const int pos = s_ * B + off + pbase;
+            const int row = KIND == 0 ? (s_ < 8 ? 2 * pos : 2 * (N - 1 - pos) + 1) : N - 1 - pos;
+            cp_async8(dst + (size_t)i * ((DR << lgP) * 2), src0 + row * nn, cok);
+        }
+        cp_async_wait_all();
+    }
+    cluster.sync();
+    // ---- pass 1: radix 16 over the whole column, one butterfly per thread ----
+    {
+        const int pr = tid & (P - 1), jj = tid >> lgP, j = q * BL + jj;
+        const double2* p = buf + ((jj << lgP) + pr);   // staging layout: s at + s BL
+        double2 x[16];
+        if (KIND == 0) {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                double2 v = p[(s << lgBL) << lgP];
+                if (s == 8 && j == 0) v = make_double2(v.x * a.in_last, v.y * a.in_last);
+                x[s] = s < 8 ? v : make_double2(-v.x, -v.y);
+            }
+        } else {
+            // Q_k = (conj(q_k) Z_k + q_{k'} Z_{k'}) / 2,  k' = (N-k) mod N (k_dst_reg);
+            // butterfly jp was staged by CTA jp / BL
+            const int jp = j == 0 ? 0 : B - j;
+            const double2* pp = rbuf(jp >> lgBL) + (((jp & (BL - 1)) << lgP) + pr);
+            const double2 qj = __ldg(a.tq + j), qjp = __ldg(a.tq + jp);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                double2 zk = p[(s << lgBL) << lgP];
+                const int sp = j == 0 ? (16 - s) & 15 : 15 - s;
+                double2 zp = pp[(sp << lgBL) << lgP];
+                if (s == 0 && j == 0) {
+                    zk = make_double2(zk.x * a.in_last, zk.y * a.in_last);
+                    zp = zk;
+                }
+                const double2 qk = s == 0 ? qj : cmul(qj, rot32(s));
+                const double2 qp0 = cmul(qjp, rot32((16 - s) & 15)), qp1 = cmul(qjp, rot32(15 - s));
+                const double2 qp = j == 0 ? (s == 0 ? qjp : qp0) : qp1;
+                const double2 u1 = cadd(cmul(make_double2(qk.x, -qk.y), zk), cmul(qp, zp));
+                x[s] = make_double2(0.5 * u1.x, 0.5 * u1.y);
+            }
+        }
+        cluster.sync();  // every CTA has read its (and its partners') staged inputs
+        dft<16>(x);
+        double2 w[16];
+        if (j != 0) twiddle16(a.twp[0] + j, B, w);
+        // output s -> position s B + j, home CTA s / (16 / CL)
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            double2* hb = rbuf(s >> (4 - lgCL));
+            const int lpos = ((s & (16 / CL - 1)) << lgB) + j;
+            hb[(lpos << lgP) + pr] = (s == 0 || j == 0) ? x[s] : cmul(x[s], w[s]);
+        }
+    }
+    cluster.sync();
+    // ---- middle passes: sub-blocks of length N/16, local ----
+    if constexpr (S::np >= 3) {
+        constexpr int L2 = LG - 4;
+        mid_pass<S::r1, L2, lgNL, P, NT>(buf, a.twp[1]);
+        __syncthreads();
+        if constexpr (S::np == 4) {
+            constexpr int L3 = L2 - ilog2(S::r1);
+            mid_pass<S::r2, L3, lgNL, P, NT>(buf, a.twp[2]);
+            __syncthreads();
+        }
+    }
+    // S^T reads partner groups from other CTAs: their middle passes must be done
+    if constexpr (KIND == 0) cluster.sync();
+    // ---- final radix-4 pass ----
+    auto load_group = [&](const double2* b, int gl, int pr, double2* x) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) x[s] = b[((4 * gl + s) << lgP) + pr];
+        dft4(x[0], x[1], x[2], x[3]);
+    };
+    // result of output row `row` to its home CTA
+    auto put = [&](int row, int pr, double2 v) {
+        rbuf(row >> lgNL)[((row & (NL - 1)) << lgP) + pr] = v;
+    };
+    if (KIND == 1) {
+        constexpr int per = (P * GL) / NT;
+        double2 x[per][4];
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            load_group(buf, item >> lgP, item & (P - 1), x[i]);
+        }
+        cluster.sync();
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            const int pr = item & (P - 1), r = group_freq<LG>(q * GL + (item >> lgP));
+            put(2 * r, pr, x[i][0]);
+            put(2 * (r + Q4), pr, x[i][1]);
+            put(2 * (N - 1 - r - 2 * Q4) + 1, pr, make_double2(-x[i][2].x, -x[i][2].y));
+            put(2 * (N - 1 - r - 3 * Q4) + 1, pr, make_double2(-x[i][3].x, -x[i][3].y));
+        }
+    } else {
+        // units: this CTA's groups whose frequency base r is below N/8, i.e. whose
+        // lowest digit (the last middle pass's) has its top bit clear; the partner
+        // group of r is the group of N/4 - r, read from its home CTA
+        constexpr int lb = ilog2(sched_r(LG, S::np - 2));
+        constexpr int per = (P * (GL / 2)) / NT;
+        double2 x[per][4], y[per][4];
+        int rr[per];
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            const int pr = item & (P - 1), v = item >> lgP;
+            const int gl = ((v >> (lb - 1)) << lb) | (v & ((1 << (lb - 1)) - 1));
+            const int r = group_freq<LG>(q * GL + gl);
+            rr[i] = r;
+            load_group(buf, gl, pr, x[i]);
+            const int gy = freq_group<LG>(r == 0 ? N / 8 : Q4 - r);
+            load_group(rbuf(gy / GL), gy % GL, pr, y[i]);
+        }
+        cluster.sync();
+        auto emit = [&](int m, int pr, double2 C, double2 D, double2 qv) {
+            const double va = 0.5 * (qv.x * (C.x + D.x) + qv.y * (C.y - D.y));
+            const double vb = 0.5 * (qv.x * (C.y + D.y) - qv.y * (C.x - D.x));
+            put(N - 1 - m, pr, make_double2(va, vb));
+        };
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int item = tid + i * NT;
+            const int pr = item & (P - 1), r = rr[i];
+            if (r == 0) {
+                emit(0, pr, x[i][0], x[i][0], rot32(0));
+                emit(Q4, pr, x[i][1], x[i][3], rot32(4));
+                emit(2 * Q4, pr, x[i][2], x[i][2], rot32(8));
+                emit(3 * Q4, pr, x[i][3], x[i][1], rot32(12));
+#pragma unroll
+                for (int s = 0; s < 4; ++s)
+                    emit(N / 8 + s * Q4, pr, y[i][s], y[i][3 - s], rot32(2 + 4 * s));
+            } else {
+                const int rp = Q4 - r;
+                const double2 qr = __ldg(a.tq + r), qrp = __ldg(a.tq + rp);
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    emit(r + s * Q4, pr, x[i][s], y[i][3 - s], s == 0 ? qr : cmul(qr, rot32(4 * s)));
+                    emit(rp + s * Q4, pr, y[i][s], x[i][3 - s], s == 0 ? qrp : cmul(qrp, rot32(4 * s)));
+                }
+            }
+        }
+    }
+    cluster.sync();
+    // ---- store: this CTA's N/CL consecutive output rows ----
+    if (cok) {
+        const long long step = (long long)DR * n;
+        const long long g0 = c0 + (long long)(q * NL + lrow0) * n + cc;
+        double* out = a.out + g0;
+        const double* basep = a.base ? a.base + g0 : nullptr;
+        const double* sp = sd + ((lrow0 << lgP) + (cc >> 1)) * 2 + (cc & 1);
+        constexpr int sstep = (DR << lgP) * 2;
+        constexpr int LB = KIND == 0 ? NL / DR : 8;
+        const double alpha = a.alpha;
+#pragma unroll 1
+        for (int i0 = 0; i0 < NL / DR; i0 += LB) {
+            double bv[LB];
+            if (basep) {
+#pragma unroll
+                for (int i = 0; i < LB; ++i) bv[i] = __ldg(basep + (i0 + i) * step);
+            }
+#pragma unroll
+            for (int i = 0; i < LB; ++i) {
+                const int row = q * NL + lrow0 + (i0 + i) * DR;
                 double v = alpha * sp[(i0 + i) * sstep];
                 if (row == N - 1) v *= a.out_last;
                 out[(i0 + i) * step] = basep ? bv[i] + v : v;
@@ -791,6 +1079,38 @@ void dst_plan_build(DstPlan& d, int N) {
     }
 }
 
+template <int K, int LG, int CL>
+static void launch_dst_cl(pint_ctx* c, const DstArgs& a, long long ncols) {
+    constexpr int P = 4, W = 2 * P, NT = (P << (LG - 4)) / CL;
+    constexpr size_t smem = ((size_t)1 << LG) / CL * P * 16;
+    auto kern = dstreg::k_dst_cl<K, LG, P, CL>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        PINT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(((ncols + W - 1) / W) * CL));
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PINT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
+// N >= 2048: the thread-block-cluster transform (PINT_DST_NOCL: the single-CTA tiles)
+static bool dst_cluster_enabled() {
+    static const bool on = getenv("PINT_DST_NOCL") == nullptr;
+    return on;
+}
+
 void dst_apply(pint_ctx* c, int kind, const double* in, double* out, const double* base,
                double alpha) {
     if (c->dst.N != c->N) pint_throw(PINT_DIMENSION, "transform plan does not match problem");
@@ -828,8 +1148,16 @@ void dst_run(pint_ctx* c, const DstPlan& d, int kind, long long ncols, const dou
     }
     ProfScope prof(c, K == 0 ? K_DST : K_DST_T,
                    8.0 * (double)d.N * (double)ncols * (base ? 3.0 : 2.0));
-    if (d.fast && d.reg_lg) {
-        const int P = d.reg_p;
+    if (d.fast && d.reg_lg >= 12 && dst_cluster_enabled()) {
+        if (d.reg_lg == 12) {
+            if (K == 0) launch_dst_cl<0, 12, 4>(c, a, ncols); else launch_dst_cl<1, 12, 4>(c, a, ncols);
+        } else {
+            if (K == 0) launch_dst_cl<0, 13, 8>(c, a, ncols); else launch_dst_cl<1, 13, 8>(c, a, ncols);
+        }
+    } else if (d.fast && d.reg_lg) {
+        // N = 2048: S (KIND 1) runs 2.5x faster on 64 KB tiles (2 CTAs per SM) than on
+        // 128 KB ones, S^T slightly slower (measured: 1.68 vs 0.95 and 2.00 vs 2.13 TB/s)
+        const int P = (d.reg_lg == 11 && K == 1 && d.reg_p == 4 && !getenv("PINT_DST_P")) ? 2 : d.reg_p;
         const dim3 g((unsigned)((ncols + 2 * P - 1) / (2 * P)));
         const size_t smem = (size_t)P * d.N * 16;
         auto launch = [&](auto kern, int nt) { kern<<<g, nt, smem, c->stream>>>(a); };
