@@ -470,10 +470,29 @@ __device__ __forceinline__ void mid_pass(double2* buf, const double2* __restrict
 #pragma unroll
             for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = x[s];
         } else {
-            // table [s-1][j]: a warp's lanes read consecutive j (one sector run)
+            // table [s-1][j]: a warp's lanes read consecutive j (one sector run);
+            // radix 16 / 8 read the rows s = 1, 2, 4 (, 8) and compose the rest
             const double2* w = tw + j;
+            if constexpr (R == 16) {
+                double2 wv[16];
+                twiddle16(w, 1 << lgB, wv);
 #pragma unroll
-            for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + ((s - 1) << lgB)));
+                for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], wv[s]);
+            } else if constexpr (R == 8) {
+                double2 wv[8];
+                wv[1] = __ldg(w);
+                wv[2] = __ldg(w + (1 << lgB));
+                wv[4] = __ldg(w + (3 << lgB));
+                wv[3] = cmul(wv[1], wv[2]);
+                wv[5] = cmul(wv[4], wv[1]);
+                wv[6] = cmul(wv[4], wv[2]);
+                wv[7] = cmul(wv[4], wv[3]);
+#pragma unroll
+                for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], wv[s]);
+            } else {
+#pragma unroll
+                for (int s = 1; s < R; ++s) p[(s << lgB) << lgP] = cmul(x[s], __ldg(w + ((s - 1) << lgB)));
+            }
         }
     }
 }
