@@ -673,8 +673,6 @@ def run_gpu(args):
         gc.collect()
         torch.cuda.empty_cache()
         for name in ("c3", "c5", "c4"):
-            if name == "c4" and world == 1 and not os.environ.get("PINT_BENCH_C4_N"):
-                continue  # does not fit one GPU next to the driver's own slabs
             try:
                 # c4 needs ~10^3 iterations: its solve gets a wall budget
                 others[name] = measure_config(name, converge=not args.no_converge,
