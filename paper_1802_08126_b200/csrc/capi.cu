@@ -1050,17 +1050,19 @@ int pint_apply_saddle(pint_ctx* c, const double* p, const double* u, double* top
         ensure_uzawa_buffers(c);
         const long long S = (long long)slab(c);
         // top = Abd p - K u ;  bottom = -Kt p - ((K u + Kt u) + Abd u)   (operators.py:107-111)
-        double *ku = c->d_r1, *ktp = c->d_z, *au = c->d_w1;
-        pint::launch_timeop(c, pint::OP_K, u, nullptr, nullptr, ku);
-        pint::launch_timeop(c, pint::OP_ABD, p, nullptr, nullptr, top);
-        pint::launch_lincomb(c, top, top, -1.0, ku, 0.0, nullptr, 1.0, false, S);
-        pint::launch_timeop(c, pint::OP_KT, p, nullptr, nullptr, ktp);
-        pint::launch_timeop(c, pint::OP_KT, u, nullptr, nullptr, bottom);
-        pint::launch_timeop(c, pint::OP_ABD, u, nullptr, nullptr, au);
-        // s = (Ku + Ktu) + Au ; bottom = (-Ktp) - s
-        pint::launch_lincomb(c, bottom, ku, 1.0, bottom, 1.0, au, 1.0, false, S);
-        pint::launch_lincomb(c, bottom, bottom, 0.0, nullptr, 0.0, nullptr, -1.0, true, S);
-        pint::launch_lincomb(c, bottom, bottom, -1.0, ktp, 0.0, nullptr, 1.0, false, S);
+        // are the two fused Uzawa residuals with a zero right-hand side:
+        //   r1(f = 0) = (K u - Abd p) - 0 = -(top)          (a - b == -(b - a) exactly)
+        //   z(f = 0)  = (0 - Kt p) - ((K u + Kt u) + Abd u) = bottom
+        // two launches + one negation instead of six operator passes and four
+        // vector combinations (MINRES applies this twice per iteration)
+        double* zero = c->d_w1;
+        PINT_CUDA_CHECK(cudaMemsetAsync(zero, 0, (size_t)S * sizeof(double), c->stream));
+        c->mu3_trust = false;
+        pint::launch_timeop(c, pint::OP_R1, u, p, zero, top);
+        c->mu3_trust = true;   // the same u: the 3D path reuses M u
+        pint::launch_timeop(c, pint::OP_Z, u, p, zero, bottom);
+        c->mu3_trust = false;
+        pint::launch_lincomb(c, top, top, 0.0, nullptr, 0.0, nullptr, -1.0, true, S);
     });
 }
 

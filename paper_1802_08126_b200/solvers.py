@@ -311,8 +311,14 @@ def minres_solve(system, atilde, htilde, tol: float = 1e-8, max_iter: int = 500)
         torch.cuda.synchronize(dev)  # torch-stream copy before the library stream reads it
         return t
 
-    f = np.ascontiguousarray(system.rhs, dtype=np.float64).ravel()
-    g = upload(np.concatenate([-f, -f]))
+    # g = (-f, -f) formed on the device from one upload of f (the host
+    # concatenation and the second half's transfer cost more than 20 iterations)
+    f_dev = upload(system.rhs)
+    g = new()
+    g[:nd].copy_(f_dev).neg_()
+    g[nd:].copy_(g[:nd])
+    del f_dev
+    torch.cuda.synchronize(dev)
     tmp, tmp2 = new(), new()
 
     # cheap positivity probe of the preconditioner (solvers.py:297-302)
@@ -443,5 +449,8 @@ def minres_solve(system, atilde, htilde, tol: float = 1e-8, max_iter: int = 500)
         info = max_iter if istop == 6 else 0
         hist.converged = info == 0
     ctx.call("pint_sync")
-    xh = x.cpu().numpy()
-    return (xh[:nd].reshape(N, n).copy(), xh[nd:].reshape(N, n).copy()), hist
+    # each half straight into its own numpy array (no host-side re-copy)
+    p_out, u_out = np.empty((N, n)), np.empty((N, n))
+    torch.from_numpy(p_out).copy_(x[:nd].view(N, n))
+    torch.from_numpy(u_out).copy_(x[nd:].view(N, n))
+    return (p_out, u_out), hist
