@@ -39,3 +39,30 @@ def test_band_solves_repeat_bitwise(space, cells, N):
         np.testing.assert_array_equal(r, runs[0][0])
         np.testing.assert_array_equal(p, runs[0][1])
         np.testing.assert_array_equal(u, runs[0][2])
+
+
+@pytest.mark.parametrize("N", [4096, 8192])
+def test_cluster_transform_repeats_bitwise(N):
+    """The N >= 4096 sine transforms run on thread-block clusters whose CTAs
+    exchange the tile through distributed shared memory between cluster
+    barriers (k_dst_cl): three runs of all four transforms on the same slab
+    must agree bit for bit (odd column count, partial last tile), and
+    inverse(forward(x)) = x, inverse_transpose(forward_transpose(x)) = x to
+    rounding (dst.py:57-93)."""
+    import torch
+
+    n = 1003
+    plan = pg.DstPlan(N)
+    xr = np.random.default_rng(N).standard_normal((N, n))
+    x = torch.from_numpy(xr).cuda()
+    outs = []
+    for _ in range(3):
+        a = plan.inverse(plan.forward(x))
+        b = plan.inverse_transpose(plan.forward_transpose(x))
+        torch.cuda.synchronize()
+        outs.append((a.cpu().numpy(), b.cpu().numpy()))
+    for a, b in outs[1:]:
+        np.testing.assert_array_equal(a, outs[0][0])
+        np.testing.assert_array_equal(b, outs[0][1])
+    assert np.max(np.abs(outs[0][0] - xr)) <= 1e-12 * np.max(np.abs(xr))
+    assert np.max(np.abs(outs[0][1] - xr)) <= 1e-12 * np.max(np.abs(xr))
