@@ -31,11 +31,19 @@ def _free_port():
 def _problem(cells=8, N=12, T=0.5, seed=4, space="2d"):
     import oracle as orc
 
-    n = (cells - 1) ** (2 if space == "2d" else 3)
+    n = (cells - 1) ** (3 if space == "3d" else 2)
     rng = np.random.default_rng(seed)
     load = rng.standard_normal((N, n))
     u0 = rng.standard_normal(n)
     nodes = orc.time_nodes("perturbed", N, T, 0.2, seed)
+    if space == "2dw":
+        # BASELINE config 4's family: one operator per step, none a multiple of
+        # another (the general branch of operators.py:92-99 / solvers.py:134-140)
+        import paper_1802_08126_b200 as pg
+
+        w = pg.c4_cell_weights(cells, pg.TimeGrid(nodes), seed=seed)
+        stiff = [orc.stiffness_2d_weighted(cells, w(k)) for k in range(N)]
+        return orc.heat_problem("2d", cells, nodes, load=load, u_init=u0, stiffness=stiff)
     pb = orc.heat_problem(space, cells, nodes, coeff=lambda t: 1.0 + t, load=load, u_init=u0)
     return pb
 
@@ -70,7 +78,9 @@ class OracleLocalOps:
         return self.pb.mass.dot(x.T).T
 
     def _A(self, x, idx):
-        # scales_n * (A_0 x_n), operators.py:92-99 (proportional case)
+        # scales_n * (A_0 x_n), operators.py:92-99 (proportional case); else tau_n (A_n x_n)
+        if self.scales is None:
+            return np.stack([self.steps[i] * self.pb.stiffness[i].dot(v) for i, v in zip(idx, x)])
         return self.scales[idx][:, None] * self.A0.dot(x.T).T
 
     def r1(self, u_ext, p_ext, f, out):
@@ -157,16 +167,19 @@ def _worker(rank, world, port, out_dir, space="2d", pipelined=False):
 
 
 _SHAPES = {"2d": dict(cells=8, N=12, T=0.5, seed=4, space="2d"),
-           "3d": dict(cells=8, N=10, T=0.5, seed=5, space="3d")}
+           "3d": dict(cells=8, N=10, T=0.5, seed=5, space="3d"),
+           "2dw": dict(cells=8, N=11, T=2.0, seed=6, space="2dw")}
 # the 3D case's perturbed grid and c(t) make omega = 0.9 diverge (alpha > 1.15)
-_OMEGA = {"2d": 0.9, "3d": 0.5}
+_OMEGA = {"2d": 0.9, "3d": 0.5, "2dw": 0.5}
 
 
 @pytest.mark.parametrize("world,space,pipelined",
                          [(2, "2d", False), (3, "2d", False), (2, "3d", False), (3, "3d", False),
                           # the NCCL code path (chunked asynchronous all-to-all transposes,
                           # Transposer.apply) forced onto gloo
-                          (2, "2d", True), (3, "2d", True), (3, "3d", True)])
+                          (2, "2d", True), (3, "2d", True), (3, "3d", True),
+                          # config 4's per-step operator family
+                          (2, "2dw", False), (3, "2dw", True)])
 def test_time_partitioned_uzawa_matches_single_process(world, space, pipelined, tmp_path):
     import oracle as orc
     from paper_1802_08126_b200.distributed import Partition
@@ -174,7 +187,7 @@ def test_time_partitioned_uzawa_matches_single_process(world, space, pipelined, 
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), space, pipelined), nprocs=world,
              join=True)
     pb = _problem(**_SHAPES[space])
-    lev = orc.mg_levels(space, pb.cells)
+    lev = orc.mg_levels(pb.space, pb.cells)
     ref = orc.uzawa(pb, orc.BlockInv(pb, lev), orc.SchurInv(pb, lev), _OMEGA[space], 1e-10, 300)
     part = Partition(pb.N, world)
     outs = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
